@@ -1,0 +1,89 @@
+/*
+ * lola_b200.h — C-ABI of the B200-native BFV-RNS hot path for LoLa
+ * (arXiv 1812.10659). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * The reference (packnn, /root/reference/proj) has no FFI: its backend
+ * boundary is the C++ EvalContext / Evaluator / BackendKind interface
+ * (proj/include/packnn/evaluator.hpp:12-91), selected by an
+ * `if (cx_->kind() == BackendKind::Ring)` inside each Evaluator method
+ * (proj/src/evaluator.cpp:84-85,106,166,191,214,262-270,307). Each entry
+ * point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Every function returns 0 on success; nonzero codes follow the
+ *     reference CLI's exit-code map (proj/src/cli.cpp:177-192):
+ *       1 internal/CUDA error, 3 invalid argument (std::invalid_argument),
+ *       4 depth or magnitude budget (depth_error / magnitude_error).
+ *     lb_last_error() returns the message of the calling thread's last error.
+ *   - `stream` is a cudaStream_t (NULL = the legacy default stream).
+ *   - Device pointers are plain `uint64_t*` into device memory.
+ *   - RNS layout is limb-major: a polynomial is `limbs` contiguous length-n
+ *     u64 arrays in [0, q_i); batches of polynomials are contiguous with a
+ *     caller-given stride (in elements).
+ *   - Prime table order inside a context: q_0..q_{L-1} (ciphertext),
+ *     p_0..p_{K-1} (special), t_0..t_{T-1} (plaintext CRT primes).
+ *   - NTT-domain ("evaluation") data is in BIT-REVERSED order:
+ *     element bitrev(k) holds a(psi^(2k+1)), where psi is the reference's
+ *     smallest-base primitive 2n-th root (proj/src/modular.cpp:44-56) and
+ *     NttTables::forward returns the same values in natural order k
+ *     (proj/src/ring.cpp:97-104).
+ */
+#ifndef LOLA_B200_H
+#define LOLA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lb_context lb_context;
+
+typedef struct {
+    uint32_t n;            /* ring degree, power of two in [4096, 32768] */
+    uint32_t num_q;        /* ciphertext RNS primes (L) */
+    uint32_t num_p;        /* special primes for hybrid key switching (K) */
+    uint32_t num_t;        /* plaintext CRT primes (independent BFV instances) */
+    const uint64_t* q;     /* each prime < 2^62, == 1 mod 2n */
+    const uint64_t* p;
+    const uint64_t* t;
+    uint32_t dnum;         /* key-switch digits (0 = num_q) */
+    uint64_t seed;         /* secret key / key material seed */
+} lb_params;
+
+/* ---- errors, setup ----------------------------------------------------- */
+
+const char* lb_last_error(void);
+
+/* Deterministic search: the `count` largest primes below 2^bits that are
+ * == 1 mod 2^log_mod, skipping the `num_exclude` values in `exclude`. */
+int lb_find_primes(uint32_t bits, uint32_t log_mod, uint32_t count, const uint64_t* exclude,
+                   uint32_t num_exclude, uint64_t* out);
+
+/* Replaces EvalContext::EvalContext's table build (proj/src/evaluator.cpp:36-46,
+ * ring.cpp:29-71) for every prime of the chain; also generates the BFV
+ * constants and the secret key from `seed`. */
+int lb_context_create(const lb_params* params, lb_context** out);
+int lb_context_destroy(lb_context* cx);
+int lb_context_prime(const lb_context* cx, uint32_t index, uint64_t* prime, uint64_t* psi);
+int lb_sync(lb_context* cx, void* stream);
+
+/* ---- NTT engine (replaces NttTables::forward / inverse, ring.cpp:97-115) --
+ * data: [polys][limbs][n] (poly stride `poly_stride` elements), limb l of
+ * each poly uses prime table entry first_prime + l. In place. */
+int lb_ntt_forward(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs,
+                   uint32_t first_prime, uint64_t poly_stride, void* stream);
+int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs,
+                   uint32_t first_prime, uint64_t poly_stride, void* stream);
+
+/* ---- measurement ------------------------------------------------------- */
+
+/* Integer-pipe roof: sustained register-resident Harvey/Shoup butterflies per
+ * second (the same butterfly the NTT runs), grid = SMs x blocks_per_sm. */
+int lb_bench_butterfly_peak(uint64_t q, int blocks_per_sm, int iters, double* bfly_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOLA_B200_H */

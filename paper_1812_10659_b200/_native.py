@@ -1,0 +1,87 @@
+"""ctypes binding of the C-ABI in include/lola_b200.h.
+
+The shared library is built in-tree by build.py. There is no fallback: if the
+library is missing or fails to load, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "liblola_b200.so"
+
+u32, u64, i32, i64, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_void_p
+P64 = C.POINTER(C.c_uint64)
+PI64 = C.POINTER(C.c_int64)
+
+
+class LolaError(RuntimeError):
+    """Nonzero status from the C-ABI (1 internal / CUDA)."""
+
+    code = 1
+
+
+class BudgetError(LolaError):
+    """Status 4: depth or magnitude budget exhausted (depth_error / magnitude_error)."""
+
+    code = 4
+
+
+class lb_params(C.Structure):
+    _fields_ = [("n", u32), ("num_q", u32), ("num_p", u32), ("num_t", u32),
+                ("q", P64), ("p", P64), ("t", P64), ("dnum", u32), ("seed", u64)]
+
+
+# name -> argtypes; every function returns int status except lb_last_error.
+_SIGS: dict[str, list] = {
+    "lb_find_primes": [u32, u32, u32, P64, u32, P64],
+    "lb_context_create": [C.POINTER(lb_params), C.POINTER(vp)],
+    "lb_context_destroy": [vp],
+    "lb_context_prime": [vp, u32, P64, P64],
+    "lb_sync": [vp, vp],
+    "lb_ntt_forward": [vp, vp, u32, u32, u32, u64, vp],
+    "lb_ntt_inverse": [vp, vp, u32, u32, u32, u64, vp],
+    "lb_bench_butterfly_peak": [u64, C.c_int, C.c_int, C.POINTER(C.c_double)],
+}
+
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise LolaError(f"native library not built: {LIB_PATH} (run paper_1812_10659_b200/build.py)")
+        l = C.CDLL(str(LIB_PATH))
+        l.lb_last_error.restype = C.c_char_p
+        l.lb_last_error.argtypes = []
+        for name, args in _SIGS.items():
+            fn = getattr(l, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = l
+    return _lib
+
+
+def declared_symbols() -> list[str]:
+    return ["lb_last_error", *_SIGS]
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().lb_last_error().decode(errors="replace")
+    if status == 3:
+        raise ValueError(msg)
+    if status == 4:
+        raise BudgetError(msg)
+    raise LolaError(f"status {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def u64_array(values) -> C.Array:
+    vals = [int(v) for v in values]
+    return (C.c_uint64 * max(1, len(vals)))(*vals)

@@ -1,0 +1,146 @@
+#include <algorithm>
+
+#include "bfv.hpp"
+#include "context.hpp"
+#include "host_math.hpp"
+
+namespace lb {
+
+Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
+    if (n_ < 4096 || n_ > 32768 || (n_ & (n_ - 1)))
+        throw std::invalid_argument("ring degree must be a power of two in [4096, 32768]");
+    logn_ = host::ilog2(n_);
+    if (prm.q.empty()) throw std::invalid_argument("need at least one ciphertext prime");
+    all_.insert(all_.end(), prm.q.begin(), prm.q.end());
+    all_.insert(all_.end(), prm.p.begin(), prm.p.end());
+    all_.insert(all_.end(), prm.t.begin(), prm.t.end());
+    for (size_t i = 0; i < all_.size(); ++i) {
+        const uint64_t q = all_[i];
+        if (q >= (uint64_t{1} << 62)) throw std::invalid_argument("primes must be below 2^62");
+        if ((q - 1) % (2ull * n_)) throw std::invalid_argument("prime " + std::to_string(q) + " != 1 mod 2n");
+        for (size_t j = 0; j < i; ++j)
+            if (all_[j] == q) throw std::invalid_argument("repeated prime " + std::to_string(q));
+    }
+    dnum_ = prm.dnum ? prm.dnum : L();
+    if (dnum_ > L()) throw std::invalid_argument("dnum exceeds the number of ciphertext primes");
+
+    LB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+    // Twiddle tables: per prime, fwd[N] and inv[N] (value, Shoup companion).
+    const size_t per_prime = 2ull * n_;  // ulonglong2 entries
+    std::vector<ulonglong2> tables(per_prime * all_.size());
+    std::vector<PrimeDev> devs(all_.size());
+    d_tables_ = DeviceBuffer(tables.size() * sizeof(ulonglong2), stream_);
+    auto* d_tab = d_tables_.get<ulonglong2>();
+    for (size_t i = 0; i < all_.size(); ++i) {
+        const uint64_t q = all_[i];
+        const uint64_t psi = host::root_of_unity(q, 2ull * n_);
+        const uint64_t psi_inv = host::invm(psi, q);
+        psi_.push_back(psi);
+        std::vector<uint64_t> pw(n_), ipw(n_);
+        uint64_t a = 1, b = 1;
+        for (uint32_t k = 0; k < n_; ++k) {
+            pw[k] = a;
+            ipw[k] = b;
+            a = host::mulm(a, psi, q);
+            b = host::mulm(b, psi_inv, q);
+        }
+        ulonglong2* fwd = &tables[per_prime * i];
+        ulonglong2* inv = fwd + n_;
+        for (uint32_t k = 0; k < n_; ++k) {
+            const uint64_t w = pw[host::bitrev(k, logn_)];
+            const uint64_t iw = ipw[host::bitrev(k, logn_)];
+            fwd[k] = make_ulonglong2(w, shoup_companion(w, q));
+            inv[k] = make_ulonglong2(iw, shoup_companion(iw, q));
+        }
+        Modulus m;
+        m.q = q;
+        const unsigned __int128 ratio = ~static_cast<unsigned __int128>(0) / q;  // floor((2^128-1)/q)
+        m.ratio_lo = static_cast<uint64_t>(ratio);
+        m.ratio_hi = static_cast<uint64_t>(ratio >> 64);
+        mods_.push_back(m);
+        PrimeDev& d = devs[i];
+        d.q = q;
+        d.ratio_lo = m.ratio_lo;
+        d.ratio_hi = m.ratio_hi;
+        d.fwd = d_tab + per_prime * i;
+        d.inv = d_tab + per_prime * i + n_;
+        const uint64_t ninv = host::invm(n_, q);
+        d.ninv = ninv;
+        d.ninv_shoup = shoup_companion(ninv, q);
+        d.inv1n = host::mulm(inv[1].x, ninv, q);
+        d.inv1n_shoup = shoup_companion(d.inv1n, q);
+    }
+    LB_CUDA(cudaMemcpyAsync(d_tab, tables.data(), tables.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice,
+                            stream_));
+    d_primes_ = DeviceBuffer(devs.size() * sizeof(PrimeDev), stream_);
+    LB_CUDA(cudaMemcpyAsync(d_primes_.get(), devs.data(), devs.size() * sizeof(PrimeDev), cudaMemcpyHostToDevice,
+                            stream_));
+    LB_CUDA(cudaStreamSynchronize(stream_));
+    bfv_setup(*this);
+}
+
+Context::~Context() {
+    bfv_.reset();
+    d_primes_ = DeviceBuffer();
+    d_tables_ = DeviceBuffer();
+    if (stream_) {
+        cudaStreamSynchronize(stream_);
+        cudaStreamDestroy(stream_);
+    }
+}
+
+namespace {
+
+template <int LOGN>
+void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+    using S = NttShape<LOGN>;
+    const uint64_t limbs = static_cast<uint64_t>(b.polys) * b.limbs;
+    if (limbs == 0) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(limbs * S::CL));
+    cfg.blockDim = dim3(S::T);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (inverse)
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN>, b, primes));
+    else
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN>, b, primes));
+}
+
+void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+    switch (logn) {
+        case 12: launch_ntt<12>(b, primes, inverse, s); break;
+        case 13: launch_ntt<13>(b, primes, inverse, s); break;
+        case 14: launch_ntt<14>(b, primes, inverse, s); break;
+        case 15: launch_ntt<15>(b, primes, inverse, s); break;
+        default: throw std::invalid_argument("unsupported ring degree");
+    }
+}
+
+void check_batch(const Context& cx, const LimbBatch& b) {
+    if (b.first_prime + b.limbs > cx.prime_count()) throw std::invalid_argument("limb primes out of range");
+    if (b.poly_stride < static_cast<uint64_t>(b.limbs) * cx.n())
+        throw std::invalid_argument("poly stride smaller than limbs * n");
+}
+
+}  // namespace
+
+void Context::ntt_forward(const LimbBatch& b, cudaStream_t s) const {
+    check_batch(*this, b);
+    dispatch_ntt(logn_, b, dev_primes(), false, s);
+}
+
+void Context::ntt_inverse(const LimbBatch& b, cudaStream_t s) const {
+    check_batch(*this, b);
+    dispatch_ntt(logn_, b, dev_primes(), true, s);
+}
+
+}  // namespace lb

@@ -1,0 +1,126 @@
+// Device context: ring degree, the RNS prime table and its NTT tables, and
+// (filled in by bfv.cu) the BFV constants and key material.
+//
+// Prime table order: [q_0 .. q_{L-1}] ciphertext primes, [p_0 .. p_{K-1}]
+// special (key-switching) primes, [t_0 .. t_{T-1}] plaintext CRT primes.
+// Limb-major RNS layout everywhere: a polynomial is `limbs` contiguous
+// length-N u64 arrays, a ciphertext is 2 polynomials, a batch is contiguous.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "modarith.cuh"
+#include "ntt.cuh"
+
+namespace lb {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define LB_CUDA(expr)                                                                              \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess)                                                                     \
+            throw ::lb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)
+
+// Owning device allocation (stream-ordered pool).
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    DeviceBuffer(size_t bytes, cudaStream_t s) : bytes_(bytes), stream_(s) {
+        if (bytes) LB_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+    }
+    ~DeviceBuffer() { release(); }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept { *this = std::move(o); }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        if (this != &o) {
+            release();
+            ptr_ = o.ptr_;
+            bytes_ = o.bytes_;
+            stream_ = o.stream_;
+            o.ptr_ = nullptr;
+            o.bytes_ = 0;
+        }
+        return *this;
+    }
+    template <class T = uint64_t>
+    T* get() const { return static_cast<T*>(ptr_); }
+    size_t bytes() const { return bytes_; }
+
+private:
+    void release() {
+        if (ptr_) cudaFreeAsync(ptr_, stream_);
+        ptr_ = nullptr;
+    }
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+    cudaStream_t stream_ = nullptr;
+};
+
+struct Params {
+    uint32_t n = 0;
+    std::vector<uint64_t> q, p, t;
+    uint32_t dnum = 0;
+    uint64_t seed = 0;
+};
+
+struct BfvState;  // bfv.cu
+
+class Context {
+public:
+    explicit Context(const Params& prm);
+    ~Context();
+
+    uint32_t n() const { return n_; }
+    int logn() const { return logn_; }
+    uint32_t L() const { return static_cast<uint32_t>(prm_.q.size()); }
+    uint32_t K() const { return static_cast<uint32_t>(prm_.p.size()); }
+    uint32_t T() const { return static_cast<uint32_t>(prm_.t.size()); }
+    uint32_t dnum() const { return dnum_; }
+    uint32_t alpha() const { return (L() + dnum_ - 1) / dnum_; }
+    uint32_t prime_count() const { return static_cast<uint32_t>(all_.size()); }
+    uint64_t prime(uint32_t i) const { return all_.at(i); }
+    uint32_t t_index(uint32_t j) const { return L() + K() + j; }  // table index of t_j
+    uint64_t psi(uint32_t i) const { return psi_.at(i); }
+    const Params& params() const { return prm_; }
+    const PrimeDev* dev_primes() const { return d_primes_.get<PrimeDev>(); }
+    const Modulus& modulus(uint32_t i) const { return mods_.at(i); }
+    cudaStream_t stream() const { return stream_; }
+
+    // Batched transforms over [polys][limbs][N] with limb l using prime
+    // first_prime + l.
+    void ntt_forward(const LimbBatch& b, cudaStream_t s) const;
+    void ntt_inverse(const LimbBatch& b, cudaStream_t s) const;
+
+    BfvState* bfv() const { return bfv_.get(); }
+
+private:
+    Params prm_;
+    uint32_t n_;
+    int logn_;
+    uint32_t dnum_;
+    std::vector<uint64_t> all_;
+    std::vector<uint64_t> psi_;
+    std::vector<Modulus> mods_;
+    cudaStream_t stream_ = nullptr;
+    DeviceBuffer d_tables_;
+    DeviceBuffer d_primes_;
+    std::unique_ptr<BfvState> bfv_;
+    friend struct BfvState;
+    friend void bfv_setup(Context&);
+};
+
+void bfv_setup(Context& cx);
+
+}  // namespace lb

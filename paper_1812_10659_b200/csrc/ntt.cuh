@@ -1,0 +1,313 @@
+// Batched negacyclic NTT / INTT over RNS limbs, sm_100a.
+//
+// Replaces NttTables::forward / inverse (proj/src/ring.cpp:73-115): same
+// primitive 2N-th root psi (smallest-base search, proj/src/modular.cpp:44-56),
+// same evaluation points psi^(2k+1). The device transform leaves evaluations
+// in BIT-REVERSED order: out[bitrev(k)] = a(psi^(2k+1)); the C-ABI documents
+// the mapping and every NTT-domain permutation (slots, automorphisms) is
+// expressed in it.
+//
+// Work decomposition (one limb = N u64 = 128 KiB at N=16384):
+//   * a thread-block CLUSTER of CL = max(1, N/4096) CTAs owns one limb; each
+//     CTA keeps N/CL contiguous coefficients (32 KiB) in shared memory, so
+//     several limbs are resident per SM and loads of one overlap the
+//     butterflies of another;
+//   * every thread holds 16 coefficients in registers and runs 4 radix-2
+//     stages per shared-memory round trip (radix-16 passes);
+//   * the one pass whose butterflies span CTAs goes through distributed
+//     shared memory (st/ld.shared::cluster) — forward: stages 0-3 read
+//     straight from HBM and scatter into the owners' smem; inverse: stages
+//     3-0 gather from the owners' smem and write straight to HBM;
+//   * shared memory is XOR-swizzled (bits 0-3 ^= bits 4-7) so every pass is
+//     bank-conflict free;
+//   * butterflies are Harvey lazy Cooley-Tukey / Gentleman-Sande with Shoup
+//     twiddles, values kept in [0, 4q) and reduced once at the end.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace lb {
+
+// Per-prime device tables. fwd[i] = (psi^bitrev(i), shoup), inv[i] =
+// (psi^-bitrev(i), shoup) with bitrev over log2 N bits; inv_last = twiddles
+// of stage 0 premultiplied by n^-1 (index 0: n^-1 itself, index 1:
+// psi^-bitrev(1) * n^-1).
+struct PrimeDev {
+    uint64_t q;
+    uint64_t ratio_lo, ratio_hi;
+    const ulonglong2* fwd;
+    const ulonglong2* inv;
+    uint64_t ninv, ninv_shoup;
+    uint64_t inv1n, inv1n_shoup;  // psi^-bitrev(1) * n^-1
+};
+
+// Descriptor of a batch of RNS polynomials laid out [poly][limb][N]:
+// limb l of every poly uses prime first_prime + l.
+struct LimbBatch {
+    uint64_t* data;
+    uint32_t polys;
+    uint32_t limbs;        // limbs per poly
+    uint32_t first_prime;  // index into the context prime table
+    uint64_t poly_stride;  // elements between consecutive polys (>= limbs*N)
+};
+
+constexpr int kLogE = 4;               // 16 coefficients per thread
+constexpr int kE = 1 << kLogE;
+constexpr int kCtaCoeffs = 4096;       // coefficients owned by one CTA
+constexpr int kThreads = kCtaCoeffs / kE;  // 256
+constexpr int kMinBlocks = 3;             // resident CTAs per SM the register budget must allow
+
+__device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
+
+// Harvey lazy CT butterfly: X, Y in [0, 4q) -> X + WY, X - WY in [0, 4q).
+__device__ __forceinline__ void ct_bfly(uint64_t& x, uint64_t& y, ulonglong2 w, uint64_t q, uint64_t two_q) {
+    uint64_t xx = x >= two_q ? x - two_q : x;
+    uint64_t t = mul_shoup_lazy(y, w.x, w.y, q);
+    x = xx + t;
+    y = xx - t + two_q;
+}
+
+// Harvey lazy GS butterfly: X, Y in [0, 2q) -> X + Y, (X - Y) W in [0, 2q).
+__device__ __forceinline__ void gs_bfly(uint64_t& x, uint64_t& y, ulonglong2 w, uint64_t q, uint64_t two_q) {
+    uint64_t s = x + y;
+    s = s >= two_q ? s - two_q : s;
+    uint64_t d = x - y + two_q;
+    x = s;
+    y = mul_shoup_lazy(d, w.x, w.y, q);
+}
+
+__device__ __forceinline__ uint64_t reduce_4q(uint64_t v, uint64_t q, uint64_t two_q) {
+    v = v >= two_q ? v - two_q : v;
+    return v >= q ? v - q : v;
+}
+
+// Forward radix-2^C pass over one group held in r[0..2^C): global stages
+// s0 .. s0+C-1, B = global block index at stage s0.
+template <int C>
+__device__ __forceinline__ void fwd_group(uint64_t* r, const ulonglong2* __restrict__ tw, uint32_t s0, uint32_t B,
+                                          uint64_t q, uint64_t two_q) {
+#pragma unroll
+    for (int l = 0; l < C; ++l) {
+        const int half = 1 << (C - 1 - l);
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) {
+            if (k & half) continue;
+            const uint32_t idx = (1u << (s0 + l)) + (B << l) + (uint32_t)(k >> (C - l));
+            ct_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
+        }
+    }
+}
+
+// Inverse pass over one group: stages s0+C-1 down to s0.
+template <int C>
+__device__ __forceinline__ void inv_group(uint64_t* r, const ulonglong2* __restrict__ tw, uint32_t s0, uint32_t B,
+                                          uint64_t q, uint64_t two_q) {
+#pragma unroll
+    for (int l = C - 1; l >= 0; --l) {
+        const int half = 1 << (C - 1 - l);
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) {
+            if (k & half) continue;
+            const uint32_t idx = (1u << (s0 + l)) + (B << l) + (uint32_t)(k >> (C - l));
+            gs_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
+        }
+    }
+}
+
+// One local radix-2^C pass over the CTA's smem chunk (global stages
+// s0..s0+C-1; every block at stage s0 lies inside one CTA).
+template <int LOGN, int C, bool INVERSE>
+__device__ __forceinline__ void local_pass(uint64_t* sm, const ulonglong2* __restrict__ tw, uint32_t s0,
+                                           uint32_t cta_base, uint64_t q, uint64_t two_q) {
+    constexpr int G = kE >> C;  // groups per thread
+    const uint32_t stride = (1u << LOGN) >> (s0 + C);
+    const uint32_t log_bs = LOGN - s0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const uint32_t g = threadIdx.x + i * kThreads;
+        const uint32_t b = g / stride, o = g % stride;
+        const uint32_t base = (b << log_bs) + o;
+        const uint32_t B = (cta_base >> log_bs) + b;
+        uint64_t r[1 << C];
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) r[k] = sm[swz(base + k * stride)];
+        if (INVERSE)
+            inv_group<C>(r, tw, s0, B, q, two_q);
+        else
+            fwd_group<C>(r, tw, s0, B, q, two_q);
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) sm[swz(base + k * stride)] = r[k];
+    }
+}
+
+template <int LOGN>
+struct NttShape {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int CL = N > kCtaCoeffs ? N / kCtaCoeffs : 1;
+    static constexpr int M = N / CL;           // coefficients per CTA
+    static constexpr int T = M / kE;           // threads per CTA
+    static constexpr int PER_CTA = kE / CL;    // first-pass outputs each CTA receives per thread group
+    static constexpr int NE = N / kE;          // stride of the cross-CTA pass
+};
+
+__device__ __forceinline__ const PrimeDev& prime_of(const PrimeDev* primes, const LimbBatch& b, uint32_t limb_id) {
+    return primes[b.first_prime + limb_id % b.limbs];
+}
+
+__device__ __forceinline__ uint64_t* limb_ptr(const LimbBatch& b, uint32_t limb_id, int logn) {
+    const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
+    return b.data + (uint64_t)poly * b.poly_stride + ((uint64_t)l << logn);
+}
+
+// grid.x = CL * (polys * limbs); cluster dims (CL, 1, 1).
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+    using S = NttShape<LOGN>;
+    namespace cg = cooperative_groups;
+    __shared__ __align__(16) uint64_t sm[S::M];
+    const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
+    const uint32_t limb_id = blockIdx.x / S::CL;
+    const PrimeDev& P = prime_of(primes, b, limb_id);
+    const uint64_t q = P.q, two_q = 2 * q;
+    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
+    const ulonglong2* __restrict__ tw = P.fwd;
+
+    // Every CTA of the cluster must be running before peers write into its
+    // shared memory: arrive now, wait just before the remote stores.
+    if constexpr (S::CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    // Cross-CTA pass: stages 0..3 on group rho, straight from HBM.
+    {
+        const uint32_t rho = rank * S::T + threadIdx.x;
+        uint64_t r[kE];
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[k] = __ldcs(&a[rho + k * S::NE]);
+        fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
+        if constexpr (S::CL > 1) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+        // output k lives in block k (size N/16) owned by CTA k / PER_CTA
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            const uint32_t dst = k / S::PER_CTA;
+            const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
+            if constexpr (S::CL > 1) {
+                uint64_t* remote = cg::this_cluster().map_shared_rank(sm, dst);
+                remote[swz(y)] = r[k];
+            } else {
+                sm[swz(y)] = r[k];
+            }
+        }
+    }
+    if constexpr (S::CL > 1)
+        cg::this_cluster().sync();
+    else
+        __syncthreads();
+
+    const uint32_t cta_base = rank * S::M;
+    // Local passes: stages 4.. LOGN-1 in chunks of 4.
+#pragma unroll
+    for (int s0 = kLogE; s0 < LOGN; s0 += kLogE) {
+        if (s0 + kLogE <= LOGN) {
+            local_pass<LOGN, kLogE, false>(sm, tw, s0, cta_base, q, two_q);
+        } else if (LOGN - s0 == 3) {
+            local_pass<LOGN, 3, false>(sm, tw, s0, cta_base, q, two_q);
+        } else if (LOGN - s0 == 2) {
+            local_pass<LOGN, 2, false>(sm, tw, s0, cta_base, q, two_q);
+        } else {
+            local_pass<LOGN, 1, false>(sm, tw, s0, cta_base, q, two_q);
+        }
+        __syncthreads();
+    }
+    // Coalesced store of the CTA's chunk, fully reduced.
+    uint64_t* out = a + cta_base;
+#pragma unroll
+    for (int j = 0; j < kE; ++j) {
+        const uint32_t y = threadIdx.x + j * S::T;
+        __stcs(&out[y], reduce_4q(sm[swz(y)], q, two_q));
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+    using S = NttShape<LOGN>;
+    namespace cg = cooperative_groups;
+    __shared__ __align__(16) uint64_t sm[S::M];
+    const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
+    const uint32_t limb_id = blockIdx.x / S::CL;
+    const PrimeDev& P = prime_of(primes, b, limb_id);
+    const uint64_t q = P.q, two_q = 2 * q;
+    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
+    const ulonglong2* __restrict__ tw = P.inv;
+    const uint32_t cta_base = rank * S::M;
+
+    {
+        const uint64_t* in = a + cta_base;
+#pragma unroll
+        for (int j = 0; j < kE; ++j) {
+            const uint32_t y = threadIdx.x + j * S::T;
+            sm[swz(y)] = __ldcs(&in[y]);
+        }
+    }
+    __syncthreads();
+    // Local passes in reverse: the last (possibly short) chunk first.
+    constexpr int kTail = (LOGN - kLogE) % kLogE;
+    if constexpr (kTail == 3) {
+        local_pass<LOGN, 3, true>(sm, tw, LOGN - 3, cta_base, q, two_q);
+        __syncthreads();
+    } else if constexpr (kTail == 2) {
+        local_pass<LOGN, 2, true>(sm, tw, LOGN - 2, cta_base, q, two_q);
+        __syncthreads();
+    } else if constexpr (kTail == 1) {
+        local_pass<LOGN, 1, true>(sm, tw, LOGN - 1, cta_base, q, two_q);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int s0 = LOGN - kTail - kLogE; s0 >= kLogE; s0 -= kLogE) {
+        local_pass<LOGN, kLogE, true>(sm, tw, s0, cta_base, q, two_q);
+        __syncthreads();
+    }
+    if constexpr (S::CL > 1) cg::this_cluster().sync();
+
+    // Cross-CTA pass: stages 3..0 gathered from the owners, n^-1 folded in.
+    {
+        const uint32_t rho = rank * S::T + threadIdx.x;
+        uint64_t r[kE];
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            const uint32_t src = k / S::PER_CTA;
+            const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
+            if constexpr (S::CL > 1) {
+                const uint64_t* remote = cg::this_cluster().map_shared_rank(sm, src);
+                r[k] = remote[swz(y)];
+            } else {
+                r[k] = sm[swz(y)];
+            }
+        }
+        // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
+#pragma unroll
+        for (int l = kLogE - 1; l >= 1; --l) {
+            const int half = 1 << (kLogE - 1 - l);
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                if (k & half) continue;
+                const uint32_t idx = (1u << l) + (uint32_t)(k >> (kLogE - l));
+                gs_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
+            }
+        }
+        constexpr int half0 = kE / 2;
+#pragma unroll
+        for (int k = 0; k < half0; ++k) {
+            uint64_t x = r[k], y = r[k + half0];
+            uint64_t s = x + y;  // < 4q
+            uint64_t d = x - y + two_q;
+            r[k] = mul_shoup(s, P.ninv, P.ninv_shoup, q);
+            r[k + half0] = mul_shoup(d, P.inv1n, P.inv1n_shoup, q);
+        }
+#pragma unroll
+        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], r[k]);
+    }
+    if constexpr (S::CL > 1) cg::this_cluster().sync();  // keep smem alive for peers
+}
+
+}  // namespace lb
