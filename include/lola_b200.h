@@ -21,7 +21,8 @@
  *     u64 arrays in [0, q_i); batches of polynomials are contiguous with a
  *     caller-given stride (in elements).
  *   - Prime table order inside a context: q_0..q_{L-1} (ciphertext),
- *     p_0..p_{K-1} (special), t_0..t_{T-1} (plaintext CRT primes).
+ *     p_0..p_{K-1} (special), b_0..b_{M-1} (auxiliary), t_0..t_{T-1}
+ *     (plaintext CRT primes).
  *   - NTT-domain ("evaluation") data is in BIT-REVERSED order:
  *     element bitrev(k) holds a(psi^(2k+1)), where psi is the reference's
  *     smallest-base primitive 2n-th root (proj/src/modular.cpp:44-56) and
@@ -43,9 +44,11 @@ typedef struct {
     uint32_t n;            /* ring degree, power of two in [4096, 32768] */
     uint32_t num_q;        /* ciphertext RNS primes (L) */
     uint32_t num_p;        /* special primes for hybrid key switching (K) */
+    uint32_t num_b;        /* auxiliary base of the exact tensor product (>= num_q + 1) */
     uint32_t num_t;        /* plaintext CRT primes (independent BFV instances) */
-    const uint64_t* q;     /* each prime < 2^62, == 1 mod 2n */
+    const uint64_t* q;     /* each prime < 2^62, == 1 mod 2n, all distinct */
     const uint64_t* p;
+    const uint64_t* b;
     const uint64_t* t;
     uint32_t dnum;         /* key-switch digits (0 = num_q) */
     uint64_t seed;         /* secret key / key material seed */
@@ -75,6 +78,60 @@ int lb_ntt_forward(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
                    uint32_t first_prime, uint64_t poly_stride, void* stream);
 int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs,
                    uint32_t first_prime, uint64_t poly_stride, void* stream);
+
+/* ---- BFV ciphertext operations ---------------------------
+ * A ciphertext is [2][L][n] u64 in the evaluation (NTT) domain. A message
+ * is T ciphertexts, one per plaintext CRT prime: [T][2][L][n]; a batch of B
+ * messages is [B][T][2][L][n]. Ops on `count` ciphertexts use plaintext prime
+ * t_{c mod T} for ciphertext c. Every pointer is device memory; outputs may
+ * alias inputs. */
+
+/* Evaluator::lift (proj/src/evaluator.cpp:67-91) + encryption: values is
+ * [B][n] int64 slot values (reduced mod each t_j, slot-encoded with the
+ * reference's generator-3 order, ring.cpp:138-144), out [B][T][2][L][n];
+ * ciphertext c gets randomness id id_base + c. */
+int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
+                     void* stream);
+/* decryption + Evaluator::lower's slot decode (evaluator.cpp:98-118, before
+ * the CRT join): out [B][T][n] slot residues mod t_j. */
+int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream);
+/* decryption to plaintext coefficients mod t_j, out [B][T][n]. */
+int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream);
+/* plaintext operand encoding (plain_limbs + slot_encode, evaluator.cpp:120-135,
+ * 166-169, 214-217): values [n] int64; pt_mul, pt_add [T][L][n] (either may
+ * be NULL). */
+int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, void* stream);
+
+int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
+              void* stream);                                            /* Evaluator::add */
+int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count,
+                     void* stream);                                     /* Evaluator::mul_scalar */
+int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt_mul, uint64_t* out, uint32_t count,
+                    void* stream);                                      /* Evaluator::mul_plain / mask */
+int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt_add, uint64_t* out, uint32_t count,
+                    void* stream);                                      /* Evaluator::add_plain */
+/* automorphism x -> x^galois + key switch (galois_apply ring.cpp:155-171 with
+ * Evaluator::rotate_columns / rotate_rows / rotate_bundle, evaluator.cpp:260-332) */
+int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count,
+                 void* stream);
+/* tensor + relinearization (Evaluator::mul, evaluator.cpp:178-202) */
+int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
+              void* stream);
+
+/* key material: key_id 0 = relinearization (s^2), odd g = Galois key x->x^g.
+ * lb_key_pointer returns the device key [dnum][2][L+K][n] (NTT domain). */
+int lb_keygen(lb_context* cx, uint64_t key_id, void* stream);
+int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out);
+/* raw pieces: NTT-domain automorphism over [polys][limbs][n] (limb l uses
+ * prime l) and key switch of [count][L][n] NTT-domain polys. */
+int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
+                    uint64_t galois, void* stream);
+int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
+                  void* stream);
+/* Galois exponents of the reference (ring.cpp:173-184): right shift of both
+ * slot rows by k columns, and the row swap. */
+uint64_t lb_galois_exponent_columns(uint32_t n, uint32_t k);
+uint64_t lb_galois_exponent_rows(uint32_t n);
 
 /* ---- measurement ------------------------------------------------------- */
 

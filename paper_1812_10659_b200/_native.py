@@ -28,8 +28,8 @@ class BudgetError(LolaError):
 
 
 class lb_params(C.Structure):
-    _fields_ = [("n", u32), ("num_q", u32), ("num_p", u32), ("num_t", u32),
-                ("q", P64), ("p", P64), ("t", P64), ("dnum", u32), ("seed", u64)]
+    _fields_ = [("n", u32), ("num_q", u32), ("num_p", u32), ("num_b", u32), ("num_t", u32),
+                ("q", P64), ("p", P64), ("b", P64), ("t", P64), ("dnum", u32), ("seed", u64)]
 
 
 # name -> argtypes; every function returns int status except lb_last_error.
@@ -42,6 +42,26 @@ _SIGS: dict[str, list] = {
     "lb_ntt_forward": [vp, vp, u32, u32, u32, u64, vp],
     "lb_ntt_inverse": [vp, vp, u32, u32, u32, u64, vp],
     "lb_bench_butterfly_peak": [u64, C.c_int, C.c_int, C.POINTER(C.c_double)],
+    "lb_encrypt_slots": [vp, vp, u32, u64, vp, vp],
+    "lb_decrypt_slots": [vp, vp, u32, vp, vp],
+    "lb_decrypt_coeffs": [vp, vp, u32, vp, vp],
+    "lb_encode_plain": [vp, vp, vp, vp, vp],
+    "lb_ct_add": [vp, vp, vp, vp, u32, vp],
+    "lb_ct_mul_scalar": [vp, vp, i64, vp, u32, vp],
+    "lb_ct_mul_plain": [vp, vp, vp, vp, u32, vp],
+    "lb_ct_add_plain": [vp, vp, vp, vp, u32, vp],
+    "lb_ct_rotate": [vp, vp, u64, vp, u32, vp],
+    "lb_ct_mul": [vp, vp, vp, vp, u32, vp],
+    "lb_keygen": [vp, u64, vp],
+    "lb_key_pointer": [vp, u64, C.POINTER(vp)],
+    "lb_automorphism": [vp, vp, vp, u32, u32, u64, vp],
+    "lb_key_switch": [vp, vp, u64, vp, vp, u32, vp],
+}
+
+# functions returning a value rather than a status
+_VALUE_SIGS: dict[str, tuple] = {
+    "lb_galois_exponent_columns": (u64, [u32, u32]),
+    "lb_galois_exponent_rows": (u64, [u32]),
 }
 
 _lib: C.CDLL | None = None
@@ -59,12 +79,16 @@ def lib() -> C.CDLL:
             fn = getattr(l, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        for name, (res, args) in _VALUE_SIGS.items():
+            fn = getattr(l, name)
+            fn.argtypes = args
+            fn.restype = res
         _lib = l
     return _lib
 
 
 def declared_symbols() -> list[str]:
-    return ["lb_last_error", *_SIGS]
+    return ["lb_last_error", *_SIGS, *_VALUE_SIGS]
 
 
 def check(status: int) -> None:

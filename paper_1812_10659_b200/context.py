@@ -29,6 +29,7 @@ class Params:
     t: list[int] = field(default_factory=list)
     dnum: int = 0
     seed: int = 0
+    b: list[int] = field(default_factory=list)
 
 
 def _stream_ptr(stream) -> int | None:
@@ -41,14 +42,19 @@ def _stream_ptr(stream) -> int | None:
 
 
 class Context:
-    def __init__(self, params: Params):
+    """params: any object with n, q, p, b, t, dnum, seed (Params or
+    params.BfvParams)."""
+
+    def __init__(self, params):
         self.params = params
+        b = list(getattr(params, "b", []))
         self._q = nat.u64_array(params.q)
         self._p = nat.u64_array(params.p)
+        self._b = nat.u64_array(b)
         self._t = nat.u64_array(params.t)
-        prm = nat.lb_params(params.n, len(params.q), len(params.p), len(params.t),
-                            C.cast(self._q, nat.P64), C.cast(self._p, nat.P64), C.cast(self._t, nat.P64),
-                            params.dnum, params.seed)
+        prm = nat.lb_params(params.n, len(params.q), len(params.p), len(b), len(params.t),
+                            C.cast(self._q, nat.P64), C.cast(self._p, nat.P64), C.cast(self._b, nat.P64),
+                            C.cast(self._t, nat.P64), params.dnum, params.seed)
         h = C.c_void_p()
         nat.call("lb_context_create", C.byref(prm), C.byref(h))
         self.handle = h
@@ -70,7 +76,7 @@ class Context:
 
     @property
     def primes(self) -> list[int]:
-        return [*self.params.q, *self.params.p, *self.params.t]
+        return [*self.params.q, *self.params.p, *getattr(self.params, "b", []), *self.params.t]
 
     def prime_and_psi(self, index: int) -> tuple[int, int]:
         q, psi = C.c_uint64(), C.c_uint64()

@@ -1,7 +1,899 @@
+// BFV-RNS layer: constants, key generation and the batched ciphertext
+// operations. The reference evaluator's ring backend does the
+// same slot-level actions on plaintext polynomials (proj/src/evaluator.cpp:
+// lift_big :67-91, lower :98-118, add :137-152, add_plain :154-176, mul
+// :178-202, mul_plain :204-226, mul_scalar :242-258, rotations :260-332);
+// here every one of them runs on BFV ciphertexts.
+#include <algorithm>
+#include <cstring>
+
 #include "bfv.hpp"
+#include "bfv_kernels.cuh"
+#include "host_math.hpp"
 
 namespace lb {
 
-void bfv_setup(Context& cx) { cx.bfv_ = std::make_unique<BfvState>(); }
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(uint64_t work, int per_thread = 1) {
+    uint64_t g = (work + static_cast<uint64_t>(kBlock) * per_thread - 1) / (static_cast<uint64_t>(kBlock) * per_thread);
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 1u << 30)));
+}
+
+using host::invm;
+using host::mulm;
+
+uint64_t subm(uint64_t a, uint64_t b, uint64_t p) { return a >= b ? a - b : a + (p - b); }
+
+// product of primes[lo..hi) except index `skip`, modulo `mod`
+uint64_t prod_mod(const std::vector<uint64_t>& pr, size_t lo, size_t hi, size_t skip, uint64_t mod) {
+    uint64_t r = 1 % mod;
+    for (size_t k = lo; k < hi; ++k)
+        if (k != skip) r = mulm(r, pr[k] % mod, mod);
+    return r;
+}
+
+ulonglong2 frac128(uint64_t num, uint64_t d) {
+    unsigned __int128 x = static_cast<unsigned __int128>(num) << 64;
+    const uint64_t hi = static_cast<uint64_t>(x / d);
+    const uint64_t r = static_cast<uint64_t>(x % d);
+    x = static_cast<unsigned __int128>(r) << 64;
+    return make_ulonglong2(hi, static_cast<uint64_t>(x / d));
+}
+
+// ---- device kernels ------------------------------------------------------------
+
+// secret s (ternary, §3.2) reduced into every prime of Q, P, B
+__global__ void k_secret_coeffs(BfvDev d, uint64_t* out, uint32_t primes) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(primes) * d.n) return;
+    const uint32_t r = idx / d.n, k = idx % d.n;
+    const int64_t s = sample_ternary(prng_at(stream_key(d.seed, kStreamSecret), k));
+    out[idx] = reduce_signed(s, modulus_of(d.primes[r]));
+}
+
+// out[c][r][pos] = in[c][r][src(pos)]: x -> x^g on bit-reversed evaluations
+__global__ void k_automorph(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t total, uint32_t logn,
+                            uint64_t g) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t n = 1u << logn;
+    const uint32_t pos = idx & (n - 1);
+    const uint32_t k = __brev(pos) >> (32 - logn);
+    const uint64_t e = (g * (2ull * k + 1)) & (2ull * n - 1);
+    const uint32_t k2 = static_cast<uint32_t>((e - 1) >> 1);
+    const uint32_t src = __brev(k2) >> (32 - logn);
+    out[idx] = in[(idx & ~uint64_t(n - 1)) | src];
+}
+
+// ---- key generation (§3.5) ----
+__global__ void k_keygen_error(BfvDev d, uint64_t key_id, uint64_t* e_out /*[dnum][L+K][n]*/) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(d.dnum) * LK * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint32_t r = (idx / d.n) % LK;
+    const uint32_t j = idx / (uint64_t(d.n) * LK);
+    const int64_t e = sample_cbd21(prng_at(stream_key(d.seed, stream_ksk_e(key_id, j)), k));
+    e_out[idx] = reduce_signed(e, modulus_of(d.primes[r]));
+}
+
+// key[j][0][r] = -a s + e + [r in digit j] [P]_r s' ; key[j][1][r] = a
+__global__ void k_keygen_finish(BfvDev d, uint64_t key_id, const uint64_t* __restrict__ e_ntt,
+                                const uint64_t* __restrict__ s_target /*[L+K][n]*/, const uint64_t* __restrict__ p_mod,
+                                uint64_t* __restrict__ key) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(d.dnum) * LK * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t r = (idx / d.n) % LK;
+    const uint32_t j = idx / (uint64_t(d.n) * LK);
+    const Modulus m = modulus_of(d.primes[r]);
+    const uint64_t a = sample_uniform(m.q, prng_at(stream_key(d.seed, stream_ksk_a(key_id, j, r)), pos));
+    const uint64_t as = mul_mod(a, d.s_ntt[uint64_t(r) * d.n + pos], m);
+    uint64_t b = sub_mod(e_ntt[idx], as, m.q);
+    const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+    if (r >= lo && r < hi) b = add_mod(b, mul_mod(p_mod[r], s_target[uint64_t(r) * d.n + pos], m), m.q);
+    const uint64_t base = (uint64_t(j) * 2 * LK + r) * d.n + pos;
+    key[base] = b;
+    key[base + uint64_t(LK) * d.n] = a;
+}
+
+__global__ void k_square_limbs(const uint64_t* __restrict__ s, uint64_t* __restrict__ out, BfvDev d, uint32_t limbs) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(limbs) * d.n) return;
+    const Modulus m = modulus_of(d.primes[idx / d.n]);
+    out[idx] = mul_mod(s[idx], s[idx], m);
+}
+
+// ---- encoding / encryption (§3.3, §3.4) ----
+// dst[(b*T + j)][slot_pos[i]] = values[b][i] mod t_j
+__global__ void k_scatter_slots(BfvDev d, const int64_t* __restrict__ values, uint32_t B, uint64_t* __restrict__ dst) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(B) * d.T * d.n) return;
+    const uint32_t i = idx % d.n;
+    const uint32_t j = (idx / d.n) % d.T;
+    const uint64_t b = idx / (uint64_t(d.n) * d.T);
+    const Modulus m = modulus_of(d.primes[d.tbase + j]);
+    dst[(b * d.T + j) * d.n + d.slot_pos[i]] = reduce_signed(values[b * d.n + i], m);
+}
+
+// round(Q m / t) mod q_i = Delta m + floor(([Q]_t m + floor(t/2)) / t)
+__device__ __forceinline__ uint64_t scaled_message(const BfvDev& d, uint32_t j, uint32_t i, uint64_t mval,
+                                                   const Modulus& qm) {
+    const uint64_t t = d.primes[d.tbase + j].q;
+    const uint64_t extra = (d.q_mod_t[j] * mval + (t >> 1)) / t;
+    return add_mod(mul_mod(d.delta[j * d.L + i], mval, qm), reduce_u64(extra, qm), qm.q);
+}
+
+// c0 (coefficient domain) = e + round(Q m / t); m: [count][n] mod t_j
+__global__ void k_enc_coeffs(BfvDev d, const uint64_t* __restrict__ mcoef, uint32_t count, uint64_t id_base,
+                             uint64_t* __restrict__ ct) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.L * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    const uint32_t j = c % d.T;
+    const Modulus qm = modulus_of(d.primes[i]);
+    const int64_t e = sample_cbd21(prng_at(stream_key(d.seed, stream_enc_e(id_base + c)), k));
+    const uint64_t v = add_mod(reduce_signed(e, qm), scaled_message(d, j, i, mcoef[c * d.n + k], qm), qm.q);
+    ct[(c * 2 * d.L + i) * d.n + k] = v;
+}
+
+// c1 = a (sampled in the evaluation domain), c0 = NTT(e + round(Qm/t)) - a s
+__global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, uint64_t* __restrict__ ct) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.L * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    const Modulus qm = modulus_of(d.primes[i]);
+    const uint64_t a = sample_uniform(qm.q, prng_at(stream_key(d.seed, stream_enc_a(id_base + c, i)), pos));
+    uint64_t* c0 = ct + (c * 2 * d.L + i) * d.n;
+    uint64_t* c1 = c0 + uint64_t(d.L) * d.n;
+    c1[pos] = a;
+    c0[pos] = sub_mod(c0[pos], mul_mod(a, d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
+}
+
+// pt_mul = centered lift of m; pt_add = round(Q m / t); m: [T][n]
+__global__ void k_pt_lift(BfvDev d, const uint64_t* __restrict__ mcoef, uint64_t* __restrict__ pt_mul,
+                          uint64_t* __restrict__ pt_add) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(d.T) * d.L * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint32_t j = idx / (uint64_t(d.n) * d.L);
+    const Modulus qm = modulus_of(d.primes[i]);
+    const uint64_t t = d.primes[d.tbase + j].q;
+    const uint64_t mv = mcoef[uint64_t(j) * d.n + k];
+    const int64_t centered = mv > (t >> 1) ? static_cast<int64_t>(mv) - static_cast<int64_t>(t) : static_cast<int64_t>(mv);
+    if (pt_mul) pt_mul[idx] = reduce_signed(centered, qm);
+    if (pt_add) pt_add[idx] = scaled_message(d, j, i, mv, qm);
+}
+
+// ---- decryption (§3.7) ----
+__global__ void k_phase(BfvDev d, const uint64_t* __restrict__ ct, uint32_t count, uint64_t* __restrict__ x) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.L * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    const Modulus qm = modulus_of(d.primes[i]);
+    const uint64_t* c0 = ct + (c * 2 * d.L + i) * d.n;
+    const uint64_t* c1 = c0 + uint64_t(d.L) * d.n;
+    x[idx] = add_mod(c0[pos], mul_mod(c1[pos], d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
+}
+
+// m = round(t x / Q) mod t from coefficient residues x: [count][L][n]
+__global__ void k_dec_scale(BfvDev d, const uint64_t* __restrict__ x, uint32_t count, uint64_t* __restrict__ m) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint64_t c = idx / d.n;
+    const uint32_t j = c % d.T;
+    uint64_t H = 0, Lo = 0;
+    for (uint32_t i = 0; i < d.L; ++i) {
+        const Modulus qm = modulus_of(d.primes[i]);
+        const uint64_t y = mul_mod(x[(c * d.L + i) * d.n + k], d.qhat_inv[i], qm);
+        uint64_t ip, fp;
+        fixmul(y, d.phi[j * d.L + i], ip, fp);
+        Lo += fp;
+        H += ip + (Lo < fp ? 1 : 0);
+    }
+    const Modulus tm = modulus_of(d.primes[d.tbase + j]);
+    m[idx] = reduce_u64(H + (Lo >> 63), tm);
+}
+
+__global__ void k_gather_slots(BfvDev d, const uint64_t* __restrict__ ev, uint32_t count, uint64_t* __restrict__ out) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.n) return;
+    const uint32_t i = idx % d.n;
+    const uint64_t c = idx / d.n;
+    out[idx] = ev[c * d.n + d.slot_pos[i]];
+}
+
+// ---- elementwise (ct ops) ----
+__global__ void k_add(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
+                      uint64_t total) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t i = (idx / d.n) % d.L;
+    out[idx] = add_mod(a[idx], b[idx], d.primes[i].q);
+}
+
+struct ScalarTab {
+    ulonglong2 v[32];  // per ciphertext prime: (s mod q_i, Shoup companion)
+};
+
+__global__ void k_mul_scalar(BfvDev d, const uint64_t* __restrict__ a, ScalarTab s, uint64_t* __restrict__ out,
+                             uint64_t total) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t i = (idx / d.n) % d.L;
+    out[idx] = mul_shoup(a[idx], s.v[i].x, s.v[i].y, d.primes[i].q);
+}
+
+// out[c][comp][i] = a[c][comp][i] * pt[c mod T][i]
+__global__ void k_mul_plain(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ pt,
+                            uint64_t* __restrict__ out, uint64_t total) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L * 2);
+    const uint32_t j = c % d.T;
+    const Modulus qm = modulus_of(d.primes[i]);
+    out[idx] = mul_mod(a[idx], pt[(uint64_t(j) * d.L + i) * d.n + pos], qm);
+}
+
+__global__ void k_add_plain(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ pt,
+                            uint64_t* __restrict__ out, uint64_t total) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint32_t comp = (idx / (uint64_t(d.n) * d.L)) & 1;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L * 2);
+    const uint32_t j = c % d.T;
+    const uint64_t v = a[idx];
+    out[idx] = comp ? v : add_mod(v, pt[(uint64_t(j) * d.L + i) * d.n + pos], d.primes[i].q);
+}
+
+// ---- key switching (§3.5) ----
+// ModUp: ext[c][j][r] = sum_{i in digit j} [d_i Dhat_i^-1]_{q_i} [Dhat_i]_r for r outside digit j
+__global__ void k_modup(BfvDev d, const uint64_t* __restrict__ dc /*[count][L][n] coeff*/, uint32_t count,
+                        uint64_t* __restrict__ ext /*[count][dnum][L+K][n]*/) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.dnum * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint32_t j = (idx / d.n) % d.dnum;
+    const uint64_t c = idx / (uint64_t(d.n) * d.dnum);
+    const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+    uint64_t y[16];
+#pragma unroll 1
+    for (uint32_t i = lo; i < hi; ++i) {
+        const Modulus qm = modulus_of(d.primes[i]);
+        y[i - lo] = mul_mod(dc[(c * d.L + i) * d.n + k], d.dhat_inv[i], qm);
+    }
+    uint64_t* dst = ext + ((c * d.dnum + j) * LK) * d.n + k;
+#pragma unroll 1
+    for (uint32_t r = 0; r < LK; ++r) {
+        if (r >= lo && r < hi) continue;
+        const Modulus rm = modulus_of(d.primes[r]);
+        Acc128 acc;
+        for (uint32_t i = lo; i < hi; ++i) acc.mac(y[i - lo], d.dhat_mod[i * LK + r]);
+        dst[uint64_t(r) * d.n] = reduce_acc(acc, rm);
+    }
+}
+
+// acc_h[c][r] = sum_j X_j[r] * key[j][h][r], X_j[r] = d[r] inside digit j else ext
+__global__ void k_ks_inner(BfvDev d, const uint64_t* __restrict__ dn /*NTT input*/, uint64_t d_stride,
+                           const uint64_t* __restrict__ ext, const uint64_t* __restrict__ key, uint32_t count,
+                           uint64_t* __restrict__ acc /*[count][2][L+K][n]*/) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * LK * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t r = (idx / d.n) % LK;
+    const uint64_t c = idx / (uint64_t(d.n) * LK);
+    const Modulus rm = modulus_of(d.primes[r]);
+    Acc128 a0, a1;
+    for (uint32_t j = 0; j < d.dnum; ++j) {
+        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+        const uint64_t x = (r >= lo && r < hi) ? dn[c * d_stride + uint64_t(r) * d.n + pos]
+                                               : ext[((c * d.dnum + j) * LK + r) * d.n + pos];
+        const uint64_t kb = (uint64_t(j) * 2 * LK + r) * d.n + pos;
+        a0.mac(x, key[kb]);
+        a1.mac(x, key[kb + uint64_t(LK) * d.n]);
+    }
+    acc[(c * 2 * LK + r) * d.n + pos] = reduce_acc(a0, rm);
+    acc[(c * 2 * LK + LK + r) * d.n + pos] = reduce_acc(a1, rm);
+}
+
+// ModDown conversion: conv[c][h][r] = sum_l [accP_l Phat_l^-1]_{p_l} [Phat_l]_{q_r}
+__global__ void k_moddown_conv(BfvDev d, const uint64_t* __restrict__ acc, uint32_t count, uint64_t* __restrict__ conv) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * 2 * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint64_t ch = idx / d.n;  // c * 2 + h
+    uint64_t y[8];
+    for (uint32_t l = 0; l < d.K; ++l) {
+        const Modulus pm = modulus_of(d.primes[d.pbase + l]);
+        y[l] = mul_mod(acc[(ch * LK + d.L + l) * d.n + k], d.phat_inv[l], pm);
+    }
+    for (uint32_t r = 0; r < d.L; ++r) {
+        const Modulus qm = modulus_of(d.primes[r]);
+        Acc128 s;
+        for (uint32_t l = 0; l < d.K; ++l) s.mac(y[l], d.phat_mod_q[l * d.L + r]);
+        conv[(ch * d.L + r) * d.n + k] = reduce_acc(s, qm);
+    }
+}
+
+// u_h = (acc_h - conv_h) P^-1; out_h = add_h + u_h (add_h optional)
+__global__ void k_moddown_final(BfvDev d, const uint64_t* __restrict__ acc, const uint64_t* __restrict__ conv,
+                                uint32_t count, const uint64_t* __restrict__ add0, const uint64_t* __restrict__ add1,
+                                uint64_t add_stride, uint64_t* __restrict__ out0, uint64_t* __restrict__ out1,
+                                uint64_t out_stride) {
+    const uint32_t LK = d.L + d.K;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.L * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t r = (idx / d.n) % d.L;
+    const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    const Modulus qm = modulus_of(d.primes[r]);
+    const uint64_t off = uint64_t(r) * d.n + pos;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint64_t a = acc[(c * 2 + h) * LK * d.n + off];
+        const uint64_t v = conv[(c * 2 + h) * d.L * d.n + off];
+        uint64_t u = mul_mod(sub_mod(a, v, qm.q), d.p_inv_q[r], qm);
+        const uint64_t* add = h ? add1 : add0;
+        if (add) u = add_mod(u, add[c * add_stride + off], qm.q);
+        (h ? out1 : out0)[c * out_stride + off] = u;
+    }
+}
+
+// ---- multiplication (§3.6) ----
+// exact centered extension from `F` primes (table offset fbase) to `G`
+// primes (table offset gbase); src: [polys][F][n] coeff, dst: [polys][G][n]
+__global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint32_t polys, uint32_t F, uint32_t fbase,
+                               const uint64_t* __restrict__ hat_inv, const ulonglong2* __restrict__ frac,
+                               const uint64_t* __restrict__ hat_mod /*[F][G]*/, const uint64_t* __restrict__ prod_mod /*[G]*/,
+                               uint32_t G, uint32_t gbase, uint64_t* __restrict__ dst) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(polys) * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint64_t p = idx / d.n;
+    uint64_t y[16];
+    uint64_t S_hi = 0, S_lo = 0;
+    for (uint32_t i = 0; i < F; ++i) {
+        const Modulus fm = modulus_of(d.primes[fbase + i]);
+        y[i] = mul_mod(src[(p * F + i) * d.n + k], hat_inv[i], fm);
+        uint64_t ip, fp;
+        fixmul(y[i], frac[i], ip, fp);  // ip == 0: y_i / f_i < 1
+        S_lo += fp;
+        S_hi += ip + (S_lo < fp ? 1 : 0);
+    }
+    const uint64_t v = S_hi + (S_lo >> 63);  // round(sum y_i / f_i)
+    for (uint32_t m = 0; m < G; ++m) {
+        const Modulus gm = modulus_of(d.primes[gbase + m]);
+        Acc128 acc;
+        for (uint32_t i = 0; i < F; ++i) acc.mac(y[i], hat_mod[i * G + m]);
+        const uint64_t s = reduce_acc(acc, gm);
+        dst[(p * G + m) * d.n + k] = sub_mod(s, mul_mod(reduce_u64(v, gm), prod_mod[m], gm), gm.q);
+    }
+}
+
+// tensor over Q ∪ B in the evaluation domain: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
+__global__ void k_tensor(BfvDev d, const uint64_t* __restrict__ A, const uint64_t* __restrict__ Bc,
+                         const uint64_t* __restrict__ Y /*[count][4][M][n]*/, uint32_t count,
+                         uint64_t* __restrict__ D /*[count][3][L+M][n]*/) {
+    const uint32_t LM = d.L + d.M;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * LM * d.n) return;
+    const uint32_t pos = idx % d.n;
+    const uint32_t r = (idx / d.n) % LM;
+    const uint64_t c = idx / (uint64_t(d.n) * LM);
+    uint64_t a0, a1, b0, b1;
+    uint32_t pidx;
+    if (r < d.L) {
+        pidx = r;
+        const uint64_t o = (c * 2 * d.L + r) * d.n + pos;
+        a0 = A[o];
+        a1 = A[o + uint64_t(d.L) * d.n];
+        b0 = Bc[o];
+        b1 = Bc[o + uint64_t(d.L) * d.n];
+    } else {
+        const uint32_t m = r - d.L;
+        pidx = d.bbase + m;
+        const uint64_t o = (c * 4 * d.M + m) * d.n + pos;
+        const uint64_t st = uint64_t(d.M) * d.n;
+        a0 = Y[o];
+        a1 = Y[o + st];
+        b0 = Y[o + 2 * st];
+        b1 = Y[o + 3 * st];
+    }
+    const Modulus pm = modulus_of(d.primes[pidx]);
+    const uint64_t st = uint64_t(LM) * d.n;
+    const uint64_t o = (c * 3 * LM + r) * d.n + pos;
+    D[o] = mul_mod(a0, b0, pm);
+    Acc128 s;
+    s.mac(a0, b1);
+    s.mac(a1, b0);
+    D[o + st] = reduce_acc(s, pm);
+    D[o + 2 * st] = mul_mod(a1, b1, pm);
+}
+
+// Z = round(t D / Q) in base B; D: [polys][L+M][n] coeff, Z: [polys][M][n]
+__global__ void k_scale(BfvDev d, const uint64_t* __restrict__ D, uint32_t polys, uint32_t polys_per_ct,
+                        uint64_t* __restrict__ Z) {
+    const uint32_t LM = d.L + d.M;
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(polys) * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint64_t p = idx / d.n;
+    const uint32_t j = (p / polys_per_ct) % d.T;
+    const uint64_t* src = D + p * LM * d.n + k;
+    uint64_t H = 0, Lo = 0;
+    for (uint32_t i = 0; i < d.L; ++i) {
+        uint64_t ip, fp;
+        fixmul(src[uint64_t(i) * d.n], d.theta[j * d.L + i], ip, fp);
+        Lo += fp;
+        H += ip + (Lo < fp ? 1 : 0);
+    }
+    const uint64_t R = H + (Lo >> 63);
+    for (uint32_t m = 0; m < d.M; ++m) {
+        const Modulus bm = modulus_of(d.primes[d.bbase + m]);
+        Acc128 acc;
+        for (uint32_t i = 0; i < d.L; ++i) acc.mac(src[uint64_t(i) * d.n], d.w_mod_b[(j * d.L + i) * d.M + m]);
+        acc.mac(src[uint64_t(d.L + m) * d.n], d.tqinv_b[j * d.M + m]);
+        acc.add(R);
+        Z[(p * d.M + m) * d.n + k] = reduce_acc(acc, bm);
+    }
+}
+
+}  // namespace
+
+// ---- constants -----------------------------------------------------------------
+
+void bfv_setup(Context& cx) {
+    auto st = std::make_unique<BfvState>();
+    const auto& P = cx.params();
+    const uint32_t n = cx.n(), L = cx.L(), K = cx.K(), M = cx.M(), T = cx.T();
+    const uint32_t dnum = cx.dnum(), alpha = cx.alpha();
+    if (L > 16 || K > 8 || M > 16 || T > 16) throw std::invalid_argument("prime group too large");
+    BfvDev& d = st->dev;
+    d.n = n;
+    d.logn = cx.logn();
+    d.L = L;
+    d.K = K;
+    d.M = M;
+    d.T = T;
+    d.dnum = dnum;
+    d.alpha = alpha;
+    d.pbase = L;
+    d.bbase = L + K;
+    d.tbase = L + K + M;
+    d.seed = P.seed;
+    d.primes = cx.dev_primes();
+    const auto& q = P.q;
+    const auto& p = P.p;
+    const auto& b = P.b;
+    const auto& t = P.t;
+    const uint32_t LK = L + K;
+
+    // host staging of every table, then one upload
+    std::vector<uint8_t> blob;
+    auto put = [&](const void* src, size_t bytes) {
+        size_t off = (blob.size() + 15) & ~size_t(15);
+        blob.resize(off + bytes);
+        std::memcpy(blob.data() + off, src, bytes);
+        return off;
+    };
+    std::vector<uint32_t> slot_pos(n), pos_slot(n);
+    {
+        const uint64_t two_n = 2ull * n;
+        uint64_t g = 1;
+        for (uint32_t jj = 0; jj < n / 2; ++jj) {
+            const uint32_t e0 = static_cast<uint32_t>((g - 1) / 2);
+            const uint32_t e1 = static_cast<uint32_t>((two_n - g - 1) / 2);
+            slot_pos[jj] = host::bitrev(e0, cx.logn());
+            slot_pos[n / 2 + jj] = host::bitrev(e1, cx.logn());
+            g = g * 3 % two_n;
+        }
+        for (uint32_t i = 0; i < n; ++i) pos_slot[slot_pos[i]] = i;
+    }
+    const size_t o_slot = put(slot_pos.data(), n * 4);
+    const size_t o_pslot = put(pos_slot.data(), n * 4);
+
+    std::vector<uint64_t> delta(T * L), qmt(T);
+    for (uint32_t j = 0; j < T; ++j) {
+        qmt[j] = prod_mod(q, 0, L, SIZE_MAX, t[j]);
+        for (uint32_t i = 0; i < L; ++i) delta[j * L + i] = mulm(subm(0, qmt[j] % q[i], q[i]), invm(t[j] % q[i], q[i]), q[i]);
+    }
+    const size_t o_delta = put(delta.data(), delta.size() * 8);
+    const size_t o_qmt = put(qmt.data(), qmt.size() * 8);
+
+    std::vector<uint64_t> qhat_inv(L);
+    std::vector<ulonglong2> phi(T * L), q_frac(L);
+    for (uint32_t i = 0; i < L; ++i) {
+        qhat_inv[i] = invm(prod_mod(q, 0, L, i, q[i]), q[i]);
+        q_frac[i] = frac128(1, q[i]);
+        for (uint32_t j = 0; j < T; ++j) phi[j * L + i] = frac128(t[j], q[i]);
+    }
+    const size_t o_qhinv = put(qhat_inv.data(), L * 8);
+    const size_t o_phi = put(phi.data(), phi.size() * 16);
+    const size_t o_qfrac = put(q_frac.data(), L * 16);
+
+    std::vector<uint64_t> qhat_mod_b(L * std::max(M, 1u)), q_mod_b(std::max(M, 1u));
+    std::vector<uint64_t> bhat_inv(std::max(M, 1u)), bhat_mod_q(std::max(M, 1u) * L), b_mod_q(L);
+    std::vector<ulonglong2> b_frac(std::max(M, 1u));
+    for (uint32_t m = 0; m < M; ++m) {
+        q_mod_b[m] = prod_mod(q, 0, L, SIZE_MAX, b[m]);
+        for (uint32_t i = 0; i < L; ++i) qhat_mod_b[i * M + m] = prod_mod(q, 0, L, i, b[m]);
+        bhat_inv[m] = invm(prod_mod(b, 0, M, m, b[m]), b[m]);
+        b_frac[m] = frac128(1, b[m]);
+        for (uint32_t i = 0; i < L; ++i) bhat_mod_q[m * L + i] = prod_mod(b, 0, M, m, q[i]);
+    }
+    for (uint32_t i = 0; i < L; ++i) b_mod_q[i] = prod_mod(b, 0, M, SIZE_MAX, q[i]);
+    const size_t o_qhmb = put(qhat_mod_b.data(), qhat_mod_b.size() * 8);
+    const size_t o_qmb = put(q_mod_b.data(), q_mod_b.size() * 8);
+    const size_t o_bhinv = put(bhat_inv.data(), bhat_inv.size() * 8);
+    const size_t o_bfrac = put(b_frac.data(), b_frac.size() * 16);
+    const size_t o_bhmq = put(bhat_mod_q.data(), bhat_mod_q.size() * 8);
+    const size_t o_bmq = put(b_mod_q.data(), b_mod_q.size() * 8);
+
+    std::vector<ulonglong2> theta(T * L);
+    std::vector<uint64_t> w_mod_b(std::max<size_t>(1, size_t(T) * L * M)), tqinv_b(std::max<size_t>(1, size_t(T) * M));
+    for (uint32_t j = 0; j < T && M; ++j) {
+        for (uint32_t i = 0; i < L; ++i) {
+            const uint64_t Bm = prod_mod(b, 0, M, SIZE_MAX, q[i]);
+            const uint64_t ci = invm(mulm(prod_mod(q, 0, L, i, q[i]), Bm, q[i]), q[i]);
+            const uint64_t rem = mulm(mulm(t[j] % q[i], ci, q[i]), Bm, q[i]);
+            theta[j * L + i] = frac128(rem, q[i]);
+            for (uint32_t m = 0; m < M; ++m)
+                w_mod_b[(size_t(j) * L + i) * M + m] = mulm(subm(0, rem % b[m], b[m]), invm(q[i] % b[m], b[m]), b[m]);
+        }
+        for (uint32_t m = 0; m < M; ++m)
+            tqinv_b[j * M + m] = mulm(t[j] % b[m], invm(prod_mod(q, 0, L, SIZE_MAX, b[m]), b[m]), b[m]);
+    }
+    const size_t o_theta = put(theta.data(), theta.size() * 16);
+    const size_t o_wmb = put(w_mod_b.data(), w_mod_b.size() * 8);
+    const size_t o_tqb = put(tqinv_b.data(), tqinv_b.size() * 8);
+
+    std::vector<uint64_t> qp(q);
+    qp.insert(qp.end(), p.begin(), p.end());
+    std::vector<uint64_t> dhat_inv(L), dhat_mod(size_t(L) * LK);
+    for (uint32_t i = 0; i < L; ++i) {
+        const uint32_t j = i / alpha, lo = j * alpha, hi = std::min(L, lo + alpha);
+        dhat_inv[i] = invm(prod_mod(q, lo, hi, i, q[i]), q[i]);
+        for (uint32_t r = 0; r < LK; ++r) dhat_mod[size_t(i) * LK + r] = prod_mod(q, lo, hi, i, qp[r]);
+    }
+    std::vector<uint64_t> phat_inv(std::max(K, 1u)), phat_mod_q(std::max(K, 1u) * L), p_inv_q(L);
+    for (uint32_t l = 0; l < K; ++l) {
+        phat_inv[l] = invm(prod_mod(p, 0, K, l, p[l]), p[l]);
+        for (uint32_t i = 0; i < L; ++i) phat_mod_q[l * L + i] = prod_mod(p, 0, K, l, q[i]);
+    }
+    for (uint32_t i = 0; i < L; ++i) p_inv_q[i] = K ? invm(prod_mod(p, 0, K, SIZE_MAX, q[i]), q[i]) : 1;
+    const size_t o_dhinv = put(dhat_inv.data(), L * 8);
+    const size_t o_dhmod = put(dhat_mod.data(), dhat_mod.size() * 8);
+    const size_t o_phinv = put(phat_inv.data(), phat_inv.size() * 8);
+    const size_t o_phmq = put(phat_mod_q.data(), phat_mod_q.size() * 8);
+    const size_t o_piq = put(p_inv_q.data(), L * 8);
+    std::vector<uint64_t> p_mod_qp(LK);
+    for (uint32_t r = 0; r < LK; ++r) p_mod_qp[r] = prod_mod(p, 0, K, SIZE_MAX, qp[r]);
+    const size_t o_pmqp = put(p_mod_qp.data(), LK * 8);
+
+    std::vector<int16_t> t_map(std::max(T, 1u)), qb_map(L + M), ks_map(size_t(dnum) * LK);
+    for (uint32_t j = 0; j < T; ++j) t_map[j] = int16_t(L + K + M + j);
+    for (uint32_t r = 0; r < L + M; ++r) qb_map[r] = int16_t(r < L ? r : L + K + (r - L));
+    for (uint32_t j = 0; j < dnum; ++j) {
+        const uint32_t lo = j * alpha, hi = std::min(L, lo + alpha);
+        for (uint32_t r = 0; r < LK; ++r) ks_map[j * LK + r] = (r >= lo && r < hi) ? int16_t(-1) : int16_t(r);
+    }
+    const size_t o_tmap = put(t_map.data(), t_map.size() * 2);
+    const size_t o_qbmap = put(qb_map.data(), qb_map.size() * 2);
+    const size_t o_ksmap = put(ks_map.data(), ks_map.size() * 2);
+
+    cudaStream_t s = cx.stream();
+    st->consts = DeviceBuffer(blob.size(), s);
+    uint8_t* base = st->consts.get<uint8_t>();
+    LB_CUDA(cudaMemcpyAsync(base, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+    d.slot_pos = reinterpret_cast<const uint32_t*>(base + o_slot);
+    d.pos_slot = reinterpret_cast<const uint32_t*>(base + o_pslot);
+    d.delta = reinterpret_cast<const uint64_t*>(base + o_delta);
+    d.q_mod_t = reinterpret_cast<const uint64_t*>(base + o_qmt);
+    d.qhat_inv = reinterpret_cast<const uint64_t*>(base + o_qhinv);
+    d.phi = reinterpret_cast<const ulonglong2*>(base + o_phi);
+    d.q_frac = reinterpret_cast<const ulonglong2*>(base + o_qfrac);
+    d.qhat_mod_b = reinterpret_cast<const uint64_t*>(base + o_qhmb);
+    d.q_mod_b = reinterpret_cast<const uint64_t*>(base + o_qmb);
+    d.bhat_inv = reinterpret_cast<const uint64_t*>(base + o_bhinv);
+    d.b_frac = reinterpret_cast<const ulonglong2*>(base + o_bfrac);
+    d.bhat_mod_q = reinterpret_cast<const uint64_t*>(base + o_bhmq);
+    d.b_mod_q = reinterpret_cast<const uint64_t*>(base + o_bmq);
+    d.theta = reinterpret_cast<const ulonglong2*>(base + o_theta);
+    d.w_mod_b = reinterpret_cast<const uint64_t*>(base + o_wmb);
+    d.tqinv_b = reinterpret_cast<const uint64_t*>(base + o_tqb);
+    d.dhat_inv = reinterpret_cast<const uint64_t*>(base + o_dhinv);
+    d.dhat_mod = reinterpret_cast<const uint64_t*>(base + o_dhmod);
+    d.phat_inv = reinterpret_cast<const uint64_t*>(base + o_phinv);
+    d.phat_mod_q = reinterpret_cast<const uint64_t*>(base + o_phmq);
+    d.p_inv_q = reinterpret_cast<const uint64_t*>(base + o_piq);
+    d.p_mod_qp = reinterpret_cast<const uint64_t*>(base + o_pmqp);
+    st->t_map = reinterpret_cast<const int16_t*>(base + o_tmap);
+    st->qb_map = reinterpret_cast<const int16_t*>(base + o_qbmap);
+    st->ks_map = reinterpret_cast<const int16_t*>(base + o_ksmap);
+
+    // secret key in the evaluation domain over Q, P, B
+    const uint32_t nsec = L + K + M;
+    st->secret = DeviceBuffer(size_t(nsec) * n * 8, s);
+    k_secret_coeffs<<<grid_for(uint64_t(nsec) * n), kBlock, 0, s>>>(d, st->secret.get(), nsec);
+    LB_CUDA(cudaGetLastError());
+    d.s_ntt = st->secret.get();
+    cx.bfv_ = std::move(st);
+    cx.ntt_forward(LimbBatch{cx.bfv_->secret.get(), 1, nsec, 0, uint64_t(nsec) * n}, s);
+    LB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---- key material ----------------------------------------------------------------
+
+void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
+                      uint64_t galois, cudaStream_t s) {
+    if (galois % 2 == 0 || galois >= 2ull * cx.n()) throw std::invalid_argument("galois element must be odd in [1, 2n)");
+    const uint64_t total = uint64_t(polys) * limbs * cx.n();
+    if (!total) return;
+    k_automorph<<<grid_for(total), kBlock, 0, s>>>(in, out, total, cx.logn(), galois);
+    LB_CUDA(cudaGetLastError());
+}
+
+void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
+    BfvState& st = *cx.bfv();
+    std::lock_guard<std::mutex> lock(st.mu);
+    if (st.keys.count(key_id)) return;
+    if (key_id != kRelinKeyId && (key_id % 2 == 0 || key_id >= 2ull * cx.n()))
+        throw std::invalid_argument("galois element must be odd in [3, 2n)");
+    const BfvDev& d = st.dev;
+    const uint32_t n = cx.n(), LK = d.L + d.K;
+    const uint64_t key_elems = uint64_t(d.dnum) * 2 * LK * n;
+    KsKey key;
+    key.buf = DeviceBuffer(key_elems * 8, s);
+    DeviceBuffer target(uint64_t(LK) * n * 8, s), err(uint64_t(d.dnum) * LK * n * 8, s);
+    if (key_id == kRelinKeyId) {
+        k_square_limbs<<<grid_for(uint64_t(LK) * n), kBlock, 0, s>>>(d.s_ntt, target.get(), d, LK);
+    } else {
+        automorphism_ntt(cx, d.s_ntt, target.get(), 1, LK, key_id, s);
+    }
+    LB_CUDA(cudaGetLastError());
+    k_keygen_error<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get());
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_forward(LimbBatch{err.get(), d.dnum, LK, 0, uint64_t(LK) * n}, s);
+    k_keygen_finish<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get(), target.get(),
+                                                                             d.p_mod_qp, key.buf.get());
+    LB_CUDA(cudaGetLastError());
+    st.keys.emplace(key_id, std::move(key));
+}
+
+const uint64_t* key_ptr(Context& cx, uint64_t key_id) {
+    BfvState& st = *cx.bfv();
+    std::lock_guard<std::mutex> lock(st.mu);
+    auto it = st.keys.find(key_id);
+    if (it == st.keys.end()) throw std::invalid_argument("key not generated");
+    return it->second.buf.get();
+}
+
+// ---- key switching -------------------------------------------------------------
+
+namespace {
+
+// Key switch `count` polys d (NTT domain over Q, stride d_stride) and write
+// out_h = add_h + u_h (stride out_stride; add_h may be null).
+void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint64_t key_id, uint32_t count,
+                     const uint64_t* add0, const uint64_t* add1, uint64_t add_stride, uint64_t* out0, uint64_t* out1,
+                     uint64_t out_stride, cudaStream_t s) {
+    if (!count) return;
+    BfvState& st = *cx.bfv();
+    const BfvDev& d = st.dev;
+    if (d.K == 0) throw std::invalid_argument("key switching needs special primes");
+    ensure_key(cx, key_id, s);
+    const uint64_t* key = key_ptr(cx, key_id);
+    const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
+    // (a) coefficient-domain copy of d
+    DeviceBuffer dc(uint64_t(count) * L * n * 8, s);
+    LB_CUDA(cudaMemcpy2DAsync(dc.get(), uint64_t(L) * n * 8, d_ntt, d_stride * 8, uint64_t(L) * n * 8, count,
+                              cudaMemcpyDeviceToDevice, s));
+    cx.ntt_inverse(LimbBatch{dc.get(), count, L, 0, uint64_t(L) * n}, s);
+    // (b) ModUp
+    DeviceBuffer ext(uint64_t(count) * d.dnum * LK * n * 8, s);
+    k_modup<<<grid_for(uint64_t(count) * d.dnum * n), kBlock, 0, s>>>(d, dc.get(), count, ext.get());
+    LB_CUDA(cudaGetLastError());
+    // (c) transform the extensions, skipping each digit's own primes
+    {
+        LimbBatch lb{ext.get(), count * d.dnum, LK, 0, uint64_t(LK) * n};
+        lb.prime_map = st.ks_map;
+        lb.map_period = d.dnum * LK;
+        cx.ntt_forward(lb, s);
+    }
+    // (d) inner product with the key
+    DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
+    k_ks_inner<<<grid_for(uint64_t(count) * LK * n), kBlock, 0, s>>>(d, d_ntt, d_stride, ext.get(), key, count,
+                                                                       acc.get());
+    LB_CUDA(cudaGetLastError());
+    // (e) ModDown: P limbs to coefficients, convert, back to evaluations
+    cx.ntt_inverse(LimbBatch{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n}, s);
+    DeviceBuffer conv(uint64_t(count) * 2 * L * n * 8, s);
+    k_moddown_conv<<<grid_for(uint64_t(count) * 2 * n), kBlock, 0, s>>>(d, acc.get(), count, conv.get());
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_forward(LimbBatch{conv.get(), count * 2, L, 0, uint64_t(L) * n}, s);
+    k_moddown_final<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, acc.get(), conv.get(), count, add0, add1,
+                                                                          add_stride, out0, out1, out_stride);
+    LB_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
+                cudaStream_t s) {
+    const uint64_t LN = uint64_t(cx.L()) * cx.n();
+    key_switch_impl(cx, d, LN, key_id, count, nullptr, nullptr, 0, u0, u1, LN, s);
+}
+
+// ---- public ciphertext operations ----------------------------------------------
+
+void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!B) return;
+    const uint32_t n = d.n, T = d.T, L = d.L;
+    if (T == 0) throw std::invalid_argument("context has no plaintext primes");
+    const uint32_t count = B * T;
+    DeviceBuffer m(uint64_t(count) * n * 8, s);
+    k_scatter_slots<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, values, B, m.get());
+    LB_CUDA(cudaGetLastError());
+    LimbBatch tb{m.get(), count, 1, 0, n};
+    tb.prime_map = cx.bfv()->t_map;
+    tb.map_period = T;
+    cx.ntt_inverse(tb, s);
+    k_enc_coeffs<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, m.get(), count, id_base, out);
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_forward(LimbBatch{out, count, L, 0, 2ull * L * n}, s);
+    k_enc_finish<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, count, id_base, out);
+    LB_CUDA(cudaGetLastError());
+}
+
+void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!B) return;
+    const uint32_t n = d.n, L = d.L, count = B * d.T;
+    DeviceBuffer x(uint64_t(count) * L * n * 8, s);
+    k_phase<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, ct, count, x.get());
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_inverse(LimbBatch{x.get(), count, L, 0, uint64_t(L) * n}, s);
+    k_dec_scale<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, x.get(), count, out);
+    LB_CUDA(cudaGetLastError());
+}
+
+void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!B) return;
+    const uint32_t n = d.n, T = d.T, count = B * T;
+    DeviceBuffer m(uint64_t(count) * n * 8, s);
+    decrypt_coeffs(cx, ct, B, m.get(), s);
+    LimbBatch tb{m.get(), count, 1, 0, n};
+    tb.prime_map = cx.bfv()->t_map;
+    tb.map_period = T;
+    cx.ntt_forward(tb, s);
+    k_gather_slots<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, out);
+    LB_CUDA(cudaGetLastError());
+}
+
+void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint32_t n = d.n, T = d.T, L = d.L;
+    DeviceBuffer m(uint64_t(T) * n * 8, s);
+    k_scatter_slots<<<grid_for(uint64_t(T) * n), kBlock, 0, s>>>(d, values, 1, m.get());
+    LB_CUDA(cudaGetLastError());
+    LimbBatch tb{m.get(), T, 1, 0, n};
+    tb.prime_map = cx.bfv()->t_map;
+    tb.map_period = T;
+    cx.ntt_inverse(tb, s);
+    k_pt_lift<<<grid_for(uint64_t(T) * L * n), kBlock, 0, s>>>(d, m.get(), pt_mul, pt_add);
+    LB_CUDA(cudaGetLastError());
+    if (pt_mul) cx.ntt_forward(LimbBatch{pt_mul, T, L, 0, uint64_t(L) * n}, s);
+    if (pt_add) cx.ntt_forward(LimbBatch{pt_add, T, L, 0, uint64_t(L) * n}, s);
+}
+
+void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    k_add<<<grid_for(total), kBlock, 0, s>>>(d, a, b, out, total);
+    LB_CUDA(cudaGetLastError());
+}
+
+void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    ScalarTab tab{};
+    for (uint32_t i = 0; i < d.L; ++i) {
+        const uint64_t q = cx.prime(i);
+        int64_t r = scalar % static_cast<int64_t>(q);
+        const uint64_t v = r < 0 ? static_cast<uint64_t>(r + static_cast<int64_t>(q)) : static_cast<uint64_t>(r);
+        tab.v[i] = make_ulonglong2(v, shoup_companion(v, q));
+    }
+    k_mul_scalar<<<grid_for(total), kBlock, 0, s>>>(d, a, tab, out, total);
+    LB_CUDA(cudaGetLastError());
+}
+
+void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    k_mul_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
+    LB_CUDA(cudaGetLastError());
+}
+
+void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    k_add_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
+    LB_CUDA(cudaGetLastError());
+}
+
+void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!count) return;
+    const uint64_t LN = uint64_t(d.L) * d.n;
+    DeviceBuffer rot(uint64_t(count) * 2 * LN * 8, s);
+    automorphism_ntt(cx, a, rot.get(), count * 2, d.L, galois, s);
+    key_switch_impl(cx, rot.get() + LN, 2 * LN, galois, count, rot.get(), nullptr, 2 * LN, out, out + LN, 2 * LN, s);
+}
+
+void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!count) return;
+    if (d.M < d.L + 1) throw std::invalid_argument("multiplication needs an auxiliary base of at least L+1 primes");
+    const uint32_t n = d.n, L = d.L, M = d.M, LM = L + M;
+    const uint64_t LN = uint64_t(L) * n;
+    // (a) inputs to coefficients: X[c] = [a0 a1 b0 b1]
+    DeviceBuffer X(uint64_t(count) * 4 * LN * 8, s);
+    LB_CUDA(cudaMemcpy2DAsync(X.get(), 4 * LN * 8, a, 2 * LN * 8, 2 * LN * 8, count, cudaMemcpyDeviceToDevice, s));
+    LB_CUDA(cudaMemcpy2DAsync(X.get() + 2 * LN, 4 * LN * 8, b, 2 * LN * 8, 2 * LN * 8, count, cudaMemcpyDeviceToDevice,
+                              s));
+    cx.ntt_inverse(LimbBatch{X.get(), count * 4, L, 0, LN}, s);
+    // (b) exact Q -> B, (c) to evaluations
+    DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
+    k_exact_extend<<<grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(
+        d, X.get(), count * 4, L, 0, d.qhat_inv, d.q_frac, d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
+    // (d) tensor over Q ∪ B
+    DeviceBuffer D(uint64_t(count) * 3 * LM * n * 8, s);
+    k_tensor<<<grid_for(uint64_t(count) * LM * n), kBlock, 0, s>>>(d, a, b, Y.get(), count, D.get());
+    LB_CUDA(cudaGetLastError());
+    // (e) back to coefficients over Q ∪ B
+    LimbBatch db{D.get(), count * 3, LM, 0, uint64_t(LM) * n};
+    db.prime_map = cx.bfv()->qb_map;
+    db.map_period = LM;
+    cx.ntt_inverse(db, s);
+    // (f) scale by t/Q into B, (g) exact B -> Q, (h) to evaluations
+    DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);
+    k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
+    LB_CUDA(cudaGetLastError());
+    DeviceBuffer E(uint64_t(count) * 3 * LN * 8, s);
+    k_exact_extend<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
+        d, Z.get(), count * 3, M, d.bbase, d.bhat_inv, d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, E.get());
+    LB_CUDA(cudaGetLastError());
+    cx.ntt_forward(LimbBatch{E.get(), count * 3, L, 0, LN}, s);
+    // (i) relinearize e2 and add into (e0, e1)
+    key_switch_impl(cx, E.get() + 2 * LN, 3 * LN, kRelinKeyId, count, E.get(), E.get() + LN, 3 * LN, out, out + LN,
+                    2 * LN, s);
+}
 
 }  // namespace lb

@@ -1,12 +1,113 @@
-// BFV-RNS state attached to a Context (constants and keys); see bfv.cu.
+// BFV-RNS state attached to a Context: precomputed RNS constants, the secret
+// key and the key-switching keys, plus the batched ciphertext operations.
+//
+// Algorithm specification: DESIGN.md §3 (restated independently by the CPU
+// oracle in oracle/bfv_oracle.cpp). Device layout:
+//   ciphertext  [2][L][n]       NTT domain (bit-reversed), limb-major
+//   message     [T][2][L][n]    one ciphertext per plaintext prime t_j
+//   batch       [B][T][2][L][n] B independent messages (images)
+//   ks key      [dnum][2][L+K][n] NTT domain (b_j, a_j)
+// Ciphertext c of a batch uses plaintext prime t_{c mod T}.
 #pragma once
+
+#include <map>
+#include <mutex>
 
 #include "context.hpp"
 
 namespace lb {
 
-struct BfvState {
-    // filled by bfv_setup
+struct BfvDev {
+    uint32_t n, logn, L, K, M, T, dnum, alpha;
+    uint32_t pbase, bbase, tbase;  // prime-table offsets of P, B, T (Q starts at 0)
+    uint64_t seed;
+    const PrimeDev* primes;
+    const uint64_t* s_ntt;       // [L+K+M][n] secret, NTT domain, table order
+    const uint32_t* slot_pos;    // [n] device NTT position of slot i
+    const uint32_t* pos_slot;    // [n] inverse map
+    // encryption / plaintext addition
+    const uint64_t* delta;       // [T][L] floor(Q/t_j) mod q_i
+    const uint64_t* q_mod_t;     // [T] [Q]_{t_j}
+    // decryption
+    const uint64_t* qhat_inv;    // [L] [(Q/q_i)^-1]_{q_i}
+    const ulonglong2* phi;       // [T][L] floor(t_j 2^128 / q_i)
+    // exact extension Q -> B
+    const ulonglong2* q_frac;    // [L] floor(2^128 / q_i)
+    const uint64_t* qhat_mod_b;  // [L][M]
+    const uint64_t* q_mod_b;     // [M]
+    // exact extension B -> Q
+    const uint64_t* bhat_inv;    // [M]
+    const ulonglong2* b_frac;    // [M]
+    const uint64_t* bhat_mod_q;  // [M][L]
+    const uint64_t* b_mod_q;     // [L]
+    // scaling t/Q (per plaintext prime)
+    const ulonglong2* theta;     // [T][L]
+    const uint64_t* w_mod_b;     // [T][L][M]
+    const uint64_t* tqinv_b;     // [T][M]
+    // key switching
+    const uint64_t* dhat_inv;    // [L] [(D_j/q_i)^-1]_{q_i}, i in digit j
+    const uint64_t* dhat_mod;    // [L][L+K] [D_j/q_i]_r
+    const uint64_t* phat_inv;    // [K]
+    const uint64_t* phat_mod_q;  // [K][L]
+    const uint64_t* p_inv_q;     // [L]
+    const uint64_t* p_mod_qp;    // [L+K] [P]_r (key generation)
 };
+
+// Opaque device handle of a key-switching key.
+struct KsKey {
+    DeviceBuffer buf;  // [dnum][2][L+K][n]
+};
+
+struct BfvState {
+    BfvDev dev{};
+    DeviceBuffer consts;
+    // prime maps for LimbBatch (device int16 arrays inside `consts`)
+    const int16_t* t_map = nullptr;   // [T]          t_j
+    const int16_t* qb_map = nullptr;  // [L+M]        Q then B
+    const int16_t* ks_map = nullptr;  // [dnum][L+K]  Q∪P minus digit j's primes
+    DeviceBuffer secret;
+    std::map<uint64_t, KsKey> keys;  // key id -> key (0 = relinearization)
+    std::mutex mu;
+};
+
+// Key ids: relinearization key for s^2 is id 0, Galois key
+// for x -> x^g is id g (odd, >= 3).
+constexpr uint64_t kRelinKeyId = 0;
+
+// ---- batched ciphertext operations (bfv.cu) ----------------------------------
+// `count` = number of ciphertexts; ciphertext c uses t_{c mod T}.
+
+// values: device int64 [B][n] slot values (one vector per message, reduced
+// mod each t_j); out: [B][T][2][L][n]; ciphertext id = id_base + c.
+void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
+                   cudaStream_t s);
+// out: [B][T][n] slot residues mod t_j
+void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s);
+// out: [B][T][n] plaintext coefficients mod t_j (before slot decoding)
+void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s);
+
+// values: device int64 [n] (shared by every message); pt_mul / pt_add:
+// [T][L][n] NTT-domain plaintext operands (centered lift; round(Q m / t)).
+void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, cudaStream_t s);
+
+void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s);
+void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s);
+// pt: [T][L][n], broadcast over messages
+void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt_mul, uint64_t* out, uint32_t count,
+                  cudaStream_t s);
+void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt_add, uint64_t* out, uint32_t count,
+                  cudaStream_t s);
+void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s);
+void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s);
+
+// key material
+void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s);
+const uint64_t* key_ptr(Context& cx, uint64_t key_id);
+// raw polynomial automorphism in the NTT domain over [polys][limbs][n]
+void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
+                      uint64_t galois, cudaStream_t s);
+// raw key switch of d ([count][L][n], NTT) -> u0, u1 ([count][L][n], NTT)
+void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
+                cudaStream_t s);
 
 }  // namespace lb

@@ -68,6 +68,7 @@ int lb_context_create(const lb_params* prm, lb_context** out) {
         p.n = prm->n;
         p.q.assign(prm->q, prm->q + prm->num_q);
         if (prm->num_p) p.p.assign(prm->p, prm->p + prm->num_p);
+        if (prm->num_b) p.b.assign(prm->b, prm->b + prm->num_b);
         if (prm->num_t) p.t.assign(prm->t, prm->t + prm->num_t);
         p.dnum = prm->dnum;
         p.seed = prm->seed;
@@ -106,5 +107,126 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
         cx->cx.ntt_inverse(lb::LimbBatch{data, polys, limbs, first_prime, poly_stride}, pick(cx, stream));
     });
 }
+
+int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
+                     void* stream) {
+    return guarded([&] {
+        need(cx && values && out, "null argument");
+        lb::encrypt_slots(cx->cx, values, B, id_base, out, pick(cx, stream));
+    });
+}
+
+int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
+    return guarded([&] {
+        need(cx && ct && out, "null argument");
+        lb::decrypt_slots(cx->cx, ct, B, out, pick(cx, stream));
+    });
+}
+
+int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
+    return guarded([&] {
+        need(cx && ct && out, "null argument");
+        lb::decrypt_coeffs(cx->cx, ct, B, out, pick(cx, stream));
+    });
+}
+
+int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, void* stream) {
+    return guarded([&] {
+        need(cx && values && (pt_mul || pt_add), "null argument");
+        lb::encode_plain(cx->cx, values, pt_mul, pt_add, pick(cx, stream));
+    });
+}
+
+int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
+    return guarded([&] {
+        need(cx && a && b && out, "null argument");
+        lb::ct_add(cx->cx, a, b, out, count, pick(cx, stream));
+    });
+}
+
+int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count,
+                     void* stream) {
+    return guarded([&] {
+        need(cx && a && out, "null argument");
+        lb::ct_mul_scalar(cx->cx, a, scalar, out, count, pick(cx, stream));
+    });
+}
+
+int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
+                    void* stream) {
+    return guarded([&] {
+        need(cx && a && pt && out, "null argument");
+        lb::ct_mul_plain(cx->cx, a, pt, out, count, pick(cx, stream));
+    });
+}
+
+int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
+                    void* stream) {
+    return guarded([&] {
+        need(cx && a && pt && out, "null argument");
+        lb::ct_add_plain(cx->cx, a, pt, out, count, pick(cx, stream));
+    });
+}
+
+int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count,
+                 void* stream) {
+    return guarded([&] {
+        need(cx && a && out, "null argument");
+        lb::ct_rotate(cx->cx, a, galois, out, count, pick(cx, stream));
+    });
+}
+
+int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
+    return guarded([&] {
+        need(cx && a && b && out, "null argument");
+        lb::ct_mul(cx->cx, a, b, out, count, pick(cx, stream));
+    });
+}
+
+int lb_keygen(lb_context* cx, uint64_t key_id, void* stream) {
+    return guarded([&] {
+        need(cx != nullptr, "null context");
+        lb::ensure_key(cx->cx, key_id, pick(cx, stream));
+    });
+}
+
+int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out) {
+    return guarded([&] {
+        need(cx && out, "null argument");
+        *out = lb::key_ptr(cx->cx, key_id);
+    });
+}
+
+int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
+                    uint64_t galois, void* stream) {
+    return guarded([&] {
+        need(cx && in && out, "null argument");
+        need(limbs <= cx->cx.prime_count(), "too many limbs");
+        lb::automorphism_ntt(cx->cx, in, out, polys, limbs, galois, pick(cx, stream));
+    });
+}
+
+int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
+                  void* stream) {
+    return guarded([&] {
+        need(cx && d && u0 && u1, "null argument");
+        lb::key_switch(cx->cx, d, key_id, u0, u1, count, pick(cx, stream));
+    });
+}
+
+uint64_t lb_galois_exponent_columns(uint32_t n, uint32_t k) {
+    // right shift by k = automorphism by 3^(n/2 - k) mod 2n (ring.cpp:173-182)
+    const uint32_t half = n / 2;
+    if (n < 4 || k >= half) return 0;
+    const uint64_t two_n = 2ull * n;
+    uint64_t e = 1, base = 3;
+    for (uint64_t x = (half - k) % half; x; x >>= 1) {
+        if (x & 1) e = e * base % two_n;
+        base = base * base % two_n;
+    }
+    return e;
+}
+
+uint64_t lb_galois_exponent_rows(uint32_t n) { return 2ull * n - 1; }
 
 }  // extern "C"

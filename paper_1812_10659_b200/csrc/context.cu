@@ -13,6 +13,7 @@ Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
     if (prm.q.empty()) throw std::invalid_argument("need at least one ciphertext prime");
     all_.insert(all_.end(), prm.q.begin(), prm.q.end());
     all_.insert(all_.end(), prm.p.begin(), prm.p.end());
+    all_.insert(all_.end(), prm.b.begin(), prm.b.end());
     all_.insert(all_.end(), prm.t.begin(), prm.t.end());
     for (size_t i = 0; i < all_.size(); ++i) {
         const uint64_t q = all_[i];
@@ -25,6 +26,15 @@ Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
     if (dnum_ > L()) throw std::invalid_argument("dnum exceeds the number of ciphertext primes");
 
     LB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    {
+        // keep freed temporaries cached in the stream-ordered pool
+        int dev = 0;
+        cudaMemPool_t pool;
+        LB_CUDA(cudaGetDevice(&dev));
+        LB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t threshold = UINT64_MAX;
+        LB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    }
 
     // Twiddle tables: per prime, fwd[N] and inv[N] (value, Shoup companion).
     const size_t per_prime = 2ull * n_;  // ulonglong2 entries
@@ -126,7 +136,9 @@ void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inv
 }
 
 void check_batch(const Context& cx, const LimbBatch& b) {
-    if (b.first_prime + b.limbs > cx.prime_count()) throw std::invalid_argument("limb primes out of range");
+    if (!b.prime_map && b.first_prime + b.limbs > cx.prime_count())
+        throw std::invalid_argument("limb primes out of range");
+    if (b.prime_map && b.map_period == 0) throw std::invalid_argument("prime map without period");
     if (b.poly_stride < static_cast<uint64_t>(b.limbs) * cx.n())
         throw std::invalid_argument("poly stride smaller than limbs * n");
 }

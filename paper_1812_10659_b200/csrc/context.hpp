@@ -2,7 +2,8 @@
 // (filled in by bfv.cu) the BFV constants and key material.
 //
 // Prime table order: [q_0 .. q_{L-1}] ciphertext primes, [p_0 .. p_{K-1}]
-// special (key-switching) primes, [t_0 .. t_{T-1}] plaintext CRT primes.
+// special (key-switching) primes, [b_0 .. b_{M-1}] auxiliary base of the
+// exact tensor product, [t_0 .. t_{T-1}] plaintext CRT primes.
 // Limb-major RNS layout everywhere: a polynomial is `limbs` contiguous
 // length-N u64 arrays, a ciphertext is 2 polynomials, a batch is contiguous.
 #pragma once
@@ -70,7 +71,7 @@ private:
 
 struct Params {
     uint32_t n = 0;
-    std::vector<uint64_t> q, p, t;
+    std::vector<uint64_t> q, p, b, t;
     uint32_t dnum = 0;
     uint64_t seed = 0;
 };
@@ -86,12 +87,15 @@ public:
     int logn() const { return logn_; }
     uint32_t L() const { return static_cast<uint32_t>(prm_.q.size()); }
     uint32_t K() const { return static_cast<uint32_t>(prm_.p.size()); }
+    uint32_t M() const { return static_cast<uint32_t>(prm_.b.size()); }
     uint32_t T() const { return static_cast<uint32_t>(prm_.t.size()); }
     uint32_t dnum() const { return dnum_; }
     uint32_t alpha() const { return (L() + dnum_ - 1) / dnum_; }
     uint32_t prime_count() const { return static_cast<uint32_t>(all_.size()); }
     uint64_t prime(uint32_t i) const { return all_.at(i); }
-    uint32_t t_index(uint32_t j) const { return L() + K() + j; }  // table index of t_j
+    uint32_t p_index(uint32_t k) const { return L() + k; }
+    uint32_t b_index(uint32_t m) const { return L() + K() + m; }
+    uint32_t t_index(uint32_t j) const { return L() + K() + M() + j; }
     uint64_t psi(uint32_t i) const { return psi_.at(i); }
     const Params& params() const { return prm_; }
     const PrimeDev* dev_primes() const { return d_primes_.get<PrimeDev>(); }

@@ -46,12 +46,18 @@ struct PrimeDev {
 
 // Descriptor of a batch of RNS polynomials laid out [poly][limb][N]:
 // limb l of every poly uses prime first_prime + l.
+// Optional prime_map: limb_id -> prime index = prime_map[limb_id % map_period]
+// (negative = leave that limb untouched), for batches whose limbs do not map
+// to one contiguous prime range (Q then B, or the per-digit key-switch
+// extensions that skip the digit's own primes).
 struct LimbBatch {
     uint64_t* data;
     uint32_t polys;
     uint32_t limbs;        // limbs per poly
     uint32_t first_prime;  // index into the context prime table
     uint64_t poly_stride;  // elements between consecutive polys (>= limbs*N)
+    const int16_t* prime_map = nullptr;
+    uint32_t map_period = 0;
 };
 
 constexpr int kLogE = 4;               // 16 coefficients per thread
@@ -153,8 +159,10 @@ struct NttShape {
     static constexpr int NE = N / kE;          // stride of the cross-CTA pass
 };
 
-__device__ __forceinline__ const PrimeDev& prime_of(const PrimeDev* primes, const LimbBatch& b, uint32_t limb_id) {
-    return primes[b.first_prime + limb_id % b.limbs];
+// Prime-table index of a limb, or -1 when the limb is to be skipped.
+__device__ __forceinline__ int prime_index(const LimbBatch& b, uint32_t limb_id) {
+    if (b.prime_map) return b.prime_map[limb_id % b.map_period];
+    return static_cast<int>(b.first_prime + limb_id % b.limbs);
 }
 
 __device__ __forceinline__ uint64_t* limb_ptr(const LimbBatch& b, uint32_t limb_id, int logn) {
@@ -170,7 +178,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_ker
     __shared__ __align__(16) uint64_t sm[S::M];
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t limb_id = blockIdx.x / S::CL;
-    const PrimeDev& P = prime_of(primes, b, limb_id);
+    const int pidx = prime_index(b, limb_id);
+    if (pidx < 0) return;  // whole cluster skips together
+    const PrimeDev& P = primes[pidx];
     const uint64_t q = P.q, two_q = 2 * q;
     uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
     const ulonglong2* __restrict__ tw = P.fwd;
@@ -235,7 +245,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
     __shared__ __align__(16) uint64_t sm[S::M];
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t limb_id = blockIdx.x / S::CL;
-    const PrimeDev& P = prime_of(primes, b, limb_id);
+    const int pidx = prime_index(b, limb_id);
+    if (pidx < 0) return;  // whole cluster skips together
+    const PrimeDev& P = primes[pidx];
     const uint64_t q = P.q, two_q = 2 * q;
     uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
     const ulonglong2* __restrict__ tw = P.inv;

@@ -1,0 +1,83 @@
+"""BFV-RNS parameter sets for the LoLa configurations (BASELINE.json).
+
+The reference has no ciphertext modulus at all; its only moduli
+are the plaintext primes (proj/src/plan.cpp:574 default, and the suggestion
+list proj/src/layers.cpp:288-290). Those become our plaintext CRT primes t_j,
+each an independent BFV instance. The ciphertext chain Q, the
+special primes P (hybrid key switching) and the auxiliary base B (exact
+HPS-style multiplication) are chosen here, deterministically.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .context import find_primes
+
+# proj/src/layers.cpp:288-290 — primes == 1 mod 32768, largest first.
+SUGGESTED_PLAIN_PRIMES = [2281701377, 2149810177, 2148794369, 2148728833, 2013265921, 1004535809, 998244353]
+# proj/src/plan.cpp:574
+REFERENCE_DEFAULT_PRIMES = [2148728833, 2148794369, 2149810177]
+
+
+@dataclass
+class BfvParams:
+    n: int
+    q: list[int]
+    p: list[int]
+    b: list[int]
+    t: list[int]
+    dnum: int = 0
+    seed: int = 0
+    notes: dict = field(default_factory=dict)
+
+    @property
+    def L(self) -> int:
+        return len(self.q)
+
+    @property
+    def K(self) -> int:
+        return len(self.p)
+
+    def log_qp(self) -> float:
+        import math
+
+        return sum(math.log2(v) for v in (*self.q, *self.p))
+
+
+def plain_primes(n: int, count: int) -> list[int]:
+    """`count` plaintext primes that support degree n: the reference's
+    suggestion list first (all == 1 mod 2^15, valid up to n = 16384), then a
+    deterministic search for 31-bit primes == 1 mod 2n."""
+    ok = [t for t in SUGGESTED_PLAIN_PRIMES if (t - 1) % (2 * n) == 0]
+    if len(ok) >= count:
+        return ok[:count]
+    extra = find_primes(31, (2 * n).bit_length() - 1, count - len(ok), exclude=ok)
+    return ok + extra
+
+
+def make_params(n: int, L: int, T: int = 1, K: int = 1, dnum: int = 0, bits: int = 60, seed: int = 1,
+                plain: list[int] | None = None) -> BfvParams:
+    """Ciphertext primes: the L largest `bits`-bit primes == 1 mod 2^16 (so
+    one chain serves every n <= 32768); special primes and the auxiliary
+    base (L + 1 primes, needed for the exact tensor product) are the next
+    ones down, all distinct."""
+    log_mod = 16
+    allp = find_primes(bits, log_mod, L + K + L + 1)
+    q, p, b = allp[:L], allp[L:L + K], allp[L + K:]
+    t = plain if plain is not None else plain_primes(n, T)
+    return BfvParams(n=n, q=q, p=p, b=b, t=t, dnum=dnum or L, seed=seed)
+
+
+# BASELINE.json configs --------------------------------------------------------
+
+def lola_mnist_params(seed: int = 1) -> BfvParams:
+    """Config 0/2: n = 16384, 5 plaintext primes (the runtime
+    magnitude bound needs 5), L = 6 ciphertext primes of 60 bits, K = 1,
+    dnum = 6: log2(QP) = 420 <= 438, the HE-standard 128-bit bound for
+    n = 16384 with a ternary secret."""
+    return make_params(16384, L=6, T=5, K=1, dnum=6, seed=seed)
+
+
+def lola_small_params(seed: int = 1) -> BfvParams:
+    """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square)."""
+    return make_params(8192, L=3, T=2, K=1, dnum=3, seed=seed)

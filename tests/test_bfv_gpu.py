@@ -1,0 +1,138 @@
+"""Ciphertext-level parity: every device BFV primitive against the CPU BFV
+oracle (oracle/bfv_oracle.cpp) coefficient by coefficient, and the decrypted
+results against the reference ring semantics (oracle/_ref/libpackref.so)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import refbind as R
+from oracle.bfvbind import Oracle
+from paper_1812_10659_b200.bfv import BfvContext, galois_exponent_columns, galois_exponent_rows
+from paper_1812_10659_b200.params import make_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=[(4096, 3, 2), (8192, 4, 1)], ids=["n4096_L3_T2", "n8192_L4_T1"])
+def env(request):
+    n, L, T = request.param
+    prm = make_params(n, L=L, T=T, K=1, seed=11)
+    cx = BfvContext(prm)
+    o = Oracle.from_params(prm)
+    return prm, cx, o
+
+
+def coeffs(cx, ct: torch.Tensor) -> np.ndarray:
+    """Device ciphertexts (evaluation domain) -> coefficient numpy [count][2][L][n]."""
+    x = ct.reshape(-1, 2, cx.L, cx.n).clone()
+    cx.ntt_inverse(x, limbs=cx.L)
+    torch.cuda.synchronize()
+    return x.cpu().numpy().astype(np.uint64)
+
+
+def rand_values(prm, B, lo=-1000, hi=1000, seed=0):
+    rng = np.random.default_rng(seed)
+    return rng.integers(lo, hi, size=(B, prm.n), dtype=np.int64)
+
+
+def encrypt(cx, prm, vals, id_base=100):
+    return cx.encrypt_slots(torch.from_numpy(vals).cuda(), id_base=id_base)
+
+
+def plain_m(prm, tj, vals_row):
+    t = prm.t[tj]
+    return R.slot_encode(t, np.mod(vals_row, t).astype(np.uint64))
+
+
+def test_encrypt_matches_oracle(env):
+    prm, cx, o = env
+    vals = rand_values(prm, 2)
+    ct = encrypt(cx, prm, vals)
+    got = coeffs(cx, ct)
+    for b in range(2):
+        for tj in range(cx.T):
+            c = b * cx.T + tj
+            want = o.encrypt(tj, plain_m(prm, tj, vals[b]), 100 + c)
+            assert np.array_equal(got[c], want), f"ciphertext {c} differs"
+
+
+def test_decrypt_roundtrip(env):
+    prm, cx, o = env
+    vals = rand_values(prm, 3, seed=1)
+    ct = encrypt(cx, prm, vals)
+    slots = cx.decrypt_slots(ct).cpu().numpy()
+    m = cx.decrypt_coeffs(ct).cpu().numpy().astype(np.uint64)
+    got = coeffs(cx, ct)
+    for b in range(3):
+        for tj, t in enumerate(prm.t):
+            assert np.array_equal(slots[b, tj], np.mod(vals[b], t))
+            assert np.array_equal(m[b, tj], o.decrypt(tj, got[b * cx.T + tj]))
+
+
+def test_elementwise_ops(env):
+    prm, cx, o = env
+    vals = rand_values(prm, 2, seed=2)
+    w = rand_values(prm, 1, seed=3)[0]
+    a = encrypt(cx, prm, vals, 7)
+    b = encrypt(cx, prm, vals[::-1].copy(), 9)
+    A, Bc = coeffs(cx, a), coeffs(cx, b)
+    pm, pa = cx.encode_plain(torch.from_numpy(w).cuda())
+    s_add = coeffs(cx, cx.add(a, b))
+    s_sc = coeffs(cx, cx.mul_scalar(a, -45))
+    s_mp = coeffs(cx, cx.mul_plain(a, pm))
+    s_ap = coeffs(cx, cx.add_plain(a, pa))
+    for c in range(2 * cx.T):
+        tj = c % cx.T
+        wt = np.mod(w, prm.t[tj]).astype(np.uint64)
+        assert np.array_equal(s_add[c], o.add(A[c], Bc[c]))
+        assert np.array_equal(s_sc[c], o.mul_scalar(A[c], -45))
+        assert np.array_equal(s_mp[c], o.mul_plain(tj, A[c], wt))
+        assert np.array_equal(s_ap[c], o.add_plain(tj, A[c], wt))
+
+
+def test_galois_key_matches_oracle(env):
+    prm, cx, o = env
+    g = galois_exponent_columns(prm.n, 1)
+    cx.keygen(g)
+    k = cx.key(g)
+    kc = k.clone()
+    cx.ntt_inverse(kc, limbs=cx.L + cx.K)
+    torch.cuda.synchronize()
+    assert np.array_equal(kc.cpu().numpy().astype(np.uint64), o.galois_key(g))
+
+
+@pytest.mark.parametrize("k", [1, 2, 7, "rows"])
+def test_rotate_matches_oracle_and_reference(env, k):
+    prm, cx, o = env
+    n = prm.n
+    g = galois_exponent_rows(n) if k == "rows" else galois_exponent_columns(n, k)
+    assert g == (R.galois_exponent_rows(n) if k == "rows" else R.galois_exponent_columns(n, k))
+    vals = rand_values(prm, 1, seed=4)
+    a = encrypt(cx, prm, vals, 3)
+    A = coeffs(cx, a)
+    r = cx.rotate(a, g)
+    got = coeffs(cx, r)
+    m = cx.decrypt_coeffs(r).cpu().numpy().astype(np.uint64)
+    for tj, t in enumerate(prm.t):
+        assert np.array_equal(got[tj], o.rotate(A[tj], g))
+        assert np.array_equal(m[0, tj], R.galois_apply(t, plain_m(prm, tj, vals[0]), g))
+
+
+def test_mul_matches_oracle_and_reference(env):
+    prm, cx, o = env
+    vals = rand_values(prm, 1, seed=5)
+    vals2 = rand_values(prm, 1, seed=6)
+    a = encrypt(cx, prm, vals, 21)
+    b = encrypt(cx, prm, vals2, 23)
+    A, Bc = coeffs(cx, a), coeffs(cx, b)
+    prod = cx.mul(a, b)
+    sq = cx.mul(a, a)
+    got_p, got_s = coeffs(cx, prod), coeffs(cx, sq)
+    mp = cx.decrypt_coeffs(prod).cpu().numpy().astype(np.uint64)
+    for tj, t in enumerate(prm.t):
+        assert np.array_equal(got_p[tj], o.mul(tj, A[tj], Bc[tj]))
+        assert np.array_equal(got_s[tj], o.mul(tj, A[tj], A[tj]))
+        want = R.poly_mul(t, plain_m(prm, tj, vals[0]), plain_m(prm, tj, vals2[0]))
+        assert np.array_equal(mp[0, tj], want)
