@@ -13,7 +13,8 @@
  *   - Every function returns 0 on success; nonzero codes follow the
  *     reference CLI's exit-code map (proj/src/cli.cpp:177-192):
  *       1 internal/CUDA error, 3 invalid argument (std::invalid_argument),
- *       4 depth or magnitude budget (depth_error / magnitude_error).
+ *       4 depth or magnitude budget (depth_error / magnitude_error),
+ *       5 plan divergence (std::logic_error).
  *     lb_last_error() returns the message of the calling thread's last error.
  *   - `stream` is a cudaStream_t (NULL = the legacy default stream).
  *   - Device pointers are plain `uint64_t*` into device memory.
@@ -132,6 +133,52 @@ int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* 
  * slot rows by k columns, and the row swap. */
 uint64_t lb_galois_exponent_columns(uint32_t n, uint32_t k);
 uint64_t lb_galois_exponent_rows(uint32_t n);
+
+/* ---- LoLa layer evaluator (proj/src/representation.cpp, kernels.cpp, plan.cpp) --
+ * A network is the already-quantized integer network the reference's
+ * QuantizedNetwork holds (proj/include/packnn/layers.hpp:100-123): linear
+ * stages with a squaring after every stage but the last. */
+typedef struct {
+    int32_t is_conv;        /* window stage (1) or matrix (0) */
+    uint32_t maps;          /* conv: output maps; dense: output rows */
+    uint32_t win_h, win_w, stride_h, stride_w;
+    uint32_t pad_top, pad_left, pad_bottom, pad_right;
+    uint64_t cols;          /* conv: window volume; dense: input length */
+    const int64_t* weights; /* maps x cols, row-major (host memory) */
+    const int64_t* bias;    /* maps entries or NULL */
+} lb_stage;
+
+typedef struct {
+    uint32_t channels, in_h, in_w;
+    uint32_t num_stages;
+    const lb_stage* stages;
+    int64_t input_bound;    /* bound on |input value| (magnitude ledger) */
+} lb_network;
+
+typedef struct lb_lola_session lb_lola_session;
+
+/* build_plan (proj/src/plan.cpp:691-704) without a device: the predicted
+ * per-step counters [steps][7] = (ct.ct, ct.pt, scalar, mask, add, rot.col,
+ * rot.row). Strategies: lola-mnist, lola-dense-mnist, lola-cifar,
+ * lola-small, linear-features. */
+int lb_plan_counters(const lb_network* net, const char* strategy, uint32_t n, uint64_t* counters,
+                     uint32_t max_steps, uint32_t* steps_out, uint32_t* depth_needed, uint64_t* predicted_peak);
+
+/* A plan bound to a device context and a batch of `batch` images; plaintext
+ * weights are encoded on the device once and reused across runs. */
+int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
+                           uint32_t max_depth, void* stream, lb_lola_session** out);
+int lb_lola_session_destroy(lb_lola_session* s);
+int lb_lola_session_info(const lb_lola_session* s, uint32_t* steps, uint64_t* outputs, uint64_t* input_values);
+/* plan.encode_input -> execute -> decode (proj/src/plan.cpp:597-633,
+ * cli.cpp:68-93): images [batch][input_values] int64, scores
+ * [batch][outputs][4] two's-complement 256-bit little-endian words; each may
+ * live on the host or the device. counters: [steps][7] measured per step
+ * (NULL ok); times: encode+encrypt, HE steps, decrypt+decode seconds (NULL
+ * ok; non-NULL adds stream syncs between phases). Status 5 = a step's
+ * counters diverged from the plan's prediction (std::logic_error). */
+int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on_device, uint64_t* scores,
+                        int scores_on_device, uint64_t* counters, double* times);
 
 /* ---- measurement ------------------------------------------------------- */
 

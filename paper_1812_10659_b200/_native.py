@@ -87,6 +87,16 @@ def lib() -> C.CDLL:
     return _lib
 
 
+def register(sigs: dict) -> None:
+    """Add status-returning signatures (used by modules defining structs)."""
+    _SIGS.update(sigs)
+    if _lib is not None:
+        for name, args in sigs.items():
+            fn = getattr(_lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+
+
 def declared_symbols() -> list[str]:
     return ["lb_last_error", *_SIGS, *_VALUE_SIGS]
 

@@ -6,50 +6,30 @@
 
 #include "../../include/lola_b200.h"
 #include "bfv.hpp"
+#include "capi_internal.hpp"
 #include "context.hpp"
 #include "host_math.hpp"
 
-struct lb_context {
-    lb::Context cx;
-    explicit lb_context(const lb::Params& p) : cx(p) {}
-};
+namespace lb::capi {
+std::string& last_error() {
+    static thread_local std::string err;
+    return err;
+}
+}  // namespace lb::capi
 
 namespace {
 
-thread_local std::string g_err;
-
-template <class F>
-int guarded(F&& f) {
-    try {
-        f();
-        return 0;
-    } catch (const std::invalid_argument& e) {
-        g_err = e.what();
-        return 3;
-    } catch (const std::out_of_range& e) {
-        g_err = e.what();
-        return 3;
-    } catch (const std::bad_alloc&) {
-        g_err = "out of memory";
-        return 1;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return 1;
-    }
-}
+using lb::capi::guarded;
+using lb::capi::need;
 
 // NULL selects the legacy default stream, as everywhere in CUDA.
 cudaStream_t pick(lb_context*, void* s) { return static_cast<cudaStream_t>(s); }
-
-void need(bool ok, const char* what) {
-    if (!ok) throw std::invalid_argument(what);
-}
 
 }  // namespace
 
 extern "C" {
 
-const char* lb_last_error(void) { return g_err.c_str(); }
+const char* lb_last_error(void) { return lb::capi::last_error().c_str(); }
 
 int lb_find_primes(uint32_t bits, uint32_t log_mod, uint32_t count, const uint64_t* exclude,
                    uint32_t num_exclude, uint64_t* out) {

@@ -1,0 +1,161 @@
+// extern "C" entry points of the LoLa layer (include/lola_b200.h, §LoLa).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/lola_b200.h"
+#include "capi_internal.hpp"
+#include "lola_plan.hpp"
+
+namespace {
+
+using lb::capi::guarded;
+
+// lb_network -> quantized network (shapes chained as in layer_output_shape,
+// proj/src/layers.cpp:333-363; a squaring after every stage but the last).
+lb::lola::Network to_network(const lb_network* in) {
+    using namespace lb::lola;
+    if (!in || !in->stages || in->num_stages == 0) throw std::invalid_argument("empty network");
+    Network net;
+    net.input = {in->channels, in->in_h, in->in_w};
+    net.input_bound = in->input_bound;
+    Shape3 cur = net.input;
+    for (uint32_t k = 0; k < in->num_stages; ++k) {
+        const lb_stage& s = in->stages[k];
+        Stage st;
+        st.is_conv = s.is_conv != 0;
+        st.rows = s.maps;
+        st.cols = s.cols;
+        st.in_shape = cur;
+        if (!s.weights || s.maps == 0) throw std::invalid_argument("missing weights");
+        st.weights.assign(s.weights, s.weights + uint64_t(s.maps) * s.cols);
+        if (s.bias) st.bias.assign(s.bias, s.bias + s.maps);
+        if (st.is_conv) {
+            ConvGeometry& g = st.geom;
+            g.channels = cur.c;
+            g.in_h = cur.h;
+            g.in_w = cur.w;
+            g.win_h = s.win_h;
+            g.win_w = s.win_w;
+            g.stride_h = s.stride_h;
+            g.stride_w = s.stride_w;
+            g.pad_top = s.pad_top;
+            g.pad_left = s.pad_left;
+            g.pad_bottom = s.pad_bottom;
+            g.pad_right = s.pad_right;
+            if (s.cols != g.window_volume()) throw std::invalid_argument("weight row does not cover the window");
+            st.out_shape = {s.maps, g.out_h(), g.out_w()};
+        } else {
+            if (s.cols != cur.values()) throw std::invalid_argument("weight row does not cover the input");
+            st.out_shape = {s.maps, 1, 1};
+        }
+        cur = st.out_shape;
+        net.stages.push_back(std::move(st));
+        net.squares_after.push_back(k + 1 < in->num_stages ? 1 : 0);
+    }
+    return net;
+}
+
+void put_counters(const lb::lola::CounterDelta& d, uint64_t* out) {
+    const auto v = d.values();
+    std::memcpy(out, v.data(), 7 * sizeof(uint64_t));
+}
+
+}  // namespace
+
+struct lb_lola_session {
+    lb::lola::Network net;
+    lb::lola::Plan plan;
+    std::unique_ptr<lb::lola::EvalContext> ecx;
+    std::unique_ptr<lb::lola::Evaluator> ev;
+    uint32_t batch = 0;
+    uint64_t outputs = 0;
+    uint64_t input_values = 0;
+};
+
+extern "C" {
+
+int lb_plan_counters(const lb_network* net, const char* strategy, uint32_t n, uint64_t* counters, uint32_t max_steps,
+                     uint32_t* steps_out, uint32_t* depth_needed, uint64_t* predicted_peak) {
+    return guarded([&] {
+        auto nw = to_network(net);
+        auto plan = lb::lola::build_plan(nw, lb::lola::strategy_from_name(strategy), n);
+        if (plan.steps.size() > max_steps) throw std::invalid_argument("too many steps for buffer");
+        for (size_t i = 0; i < plan.steps.size(); ++i) put_counters(plan.steps[i].predicted, counters + 7 * i);
+        if (steps_out) *steps_out = static_cast<uint32_t>(plan.steps.size());
+        if (depth_needed) *depth_needed = plan.depth_needed;
+        if (predicted_peak) *predicted_peak = plan.predicted_peak();
+    });
+}
+
+int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
+                           uint32_t max_depth, void* stream, lb_lola_session** out) {
+    return guarded([&] {
+        if (!cx || !out) throw std::invalid_argument("null argument");
+        auto s = std::make_unique<lb_lola_session>();
+        s->net = to_network(net);
+        s->plan = lb::lola::build_plan(s->net, lb::lola::strategy_from_name(strategy), cx->cx.n());
+        s->ecx = std::make_unique<lb::lola::EvalContext>(cx->cx, batch, max_depth, static_cast<cudaStream_t>(stream));
+        s->ev = std::make_unique<lb::lola::Evaluator>(*s->ecx);
+        s->batch = batch;
+        s->outputs = s->net.stages.back().out_shape.values();
+        s->input_values = s->net.input.values();
+        *out = s.release();
+    });
+}
+
+int lb_lola_session_destroy(lb_lola_session* s) {
+    return guarded([&] { delete s; });
+}
+
+int lb_lola_session_info(const lb_lola_session* s, uint32_t* steps, uint64_t* outputs, uint64_t* input_values) {
+    return guarded([&] {
+        if (steps) *steps = static_cast<uint32_t>(s->plan.steps.size());
+        if (outputs) *outputs = s->outputs;
+        if (input_values) *input_values = s->input_values;
+    });
+}
+
+// images: [batch][input_values] int64, device (images_on_device = 1) or host;
+// scores: [batch][outputs][4] signed 256-bit words, device or host alike.
+int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on_device, uint64_t* scores,
+                        int scores_on_device, uint64_t* counters, double* times) {
+    return guarded([&] {
+        using clock = std::chrono::steady_clock;
+        cudaStream_t st = s->ecx->stream();
+        const auto t0 = clock::now();
+        lb::DeviceBuffer dimg;
+        const int64_t* img = images;
+        if (!images_on_device) {
+            dimg = lb::DeviceBuffer(uint64_t(s->batch) * s->input_values * 8, st);
+            LB_CUDA(cudaMemcpyAsync(dimg.get(), images, uint64_t(s->batch) * s->input_values * 8,
+                                    cudaMemcpyHostToDevice, st));
+            img = dimg.get<int64_t>();
+        }
+        lb::lola::Evaluator& ev = *s->ev;
+        ev.counters() = lb::lola::OpCounters{};
+        lb::lola::EncodedTensor input = s->plan.encode_input(ev, img);
+        if (times) LB_CUDA(cudaStreamSynchronize(st));
+        const auto t1 = clock::now();
+        lb::lola::ExecutionResult res = lb::lola::execute(s->plan, std::move(input), ev);
+        if (times) LB_CUDA(cudaStreamSynchronize(st));
+        const auto t2 = clock::now();
+        lb::DeviceBuffer dec = lb::lola::decode_values(ev, res.output);
+        const uint64_t bytes = uint64_t(s->batch) * s->outputs * 32;
+        if (dec.bytes() != bytes) throw std::logic_error("decoded output size mismatch");
+        LB_CUDA(cudaMemcpyAsync(scores, dec.get(), bytes,
+                                scores_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        LB_CUDA(cudaStreamSynchronize(st));
+        const auto t3 = clock::now();
+        if (counters)
+            for (size_t i = 0; i < res.per_step.size(); ++i) put_counters(res.per_step[i], counters + 7 * i);
+        if (times) {
+            times[0] = std::chrono::duration<double>(t1 - t0).count();
+            times[1] = std::chrono::duration<double>(t2 - t1).count();
+            times[2] = std::chrono::duration<double>(t3 - t2).count();
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// Host C++ mirror of the reference evaluator boundary (proj/include/packnn/
+// message.hpp:14-75, evaluator.hpp:12-91) running on device BFV ciphertexts.
+//
+// Same names, argument meaning, counting rules and exceptions as the
+// reference; two B200-first differences:
+//   * a Message is a BATCH of B independent messages (one per image) held as
+//     one device buffer [B][T][2][L][n] — every op is one set of kernels over
+//     all B*T ciphertexts, plaintext operands are broadcast;
+//   * plaintext operands are encoded on the device once and cached by value.
+// Counters, depth and magnitude budgets stay on the host and follow
+// proj/src/evaluator.cpp exactly.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "bfv.hpp"
+#include "context.hpp"
+
+namespace lb::lola {
+
+// Thrown when an operation would exceed the multiplicative depth budget
+// (proj/include/packnn/message.hpp:14-18).
+class depth_error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+// Thrown when a magnitude bound would exceed the plaintext CRT capacity
+// (message.hpp:20-24).
+class magnitude_error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+// Non-negative magnitude bound, fixed 320-bit, saturating (replaces the
+// reference's BigInt magnitude, message.hpp:74; every capacity here is below
+// 2^256 so saturation only ever means "too big").
+struct Mag {
+    std::array<uint64_t, 5> w{};
+    Mag() = default;
+    Mag(uint64_t v) { w[0] = v; }  // NOLINT
+    static Mag saturated() {
+        Mag m;
+        m.w.fill(~uint64_t{0});
+        return m;
+    }
+    friend Mag operator+(const Mag& a, const Mag& b);
+    friend Mag operator*(const Mag& a, const Mag& b);
+    friend bool operator<(const Mag& a, const Mag& b);
+    friend bool operator>(const Mag& a, const Mag& b) { return b < a; }
+    friend bool operator==(const Mag& a, const Mag& b) { return a.w == b.w; }
+    Mag half_floor() const;  // floor(x / 2)
+    Mag minus_one() const;
+    std::string str() const;  // decimal
+};
+
+struct CounterDelta {
+    uint64_t ct_ct_mul = 0, ct_plain_mul = 0, scalar_mul = 0, mask_mul = 0, add = 0, rot_cols = 0, rot_rows = 0;
+    CounterDelta& operator+=(const CounterDelta& o);
+    friend CounterDelta operator+(CounterDelta a, const CounterDelta& b) { return a += b; }
+    friend CounterDelta operator-(const CounterDelta& a, const CounterDelta& b);
+    friend bool operator==(const CounterDelta& a, const CounterDelta& b);
+    uint64_t rotations() const { return rot_cols + rot_rows; }
+    std::array<uint64_t, 7> values() const {
+        return {ct_ct_mul, ct_plain_mul, scalar_mul, mask_mul, add, rot_cols, rot_rows};
+    }
+};
+
+struct OpCounters {
+    CounterDelta ops;
+    uint64_t live_messages_peak = 0;
+    void note_live(uint64_t live) {
+        if (live > live_messages_peak) live_messages_peak = live;
+    }
+};
+
+// Device payload: [B][T][2][L][n] u64, NTT domain.
+struct Payload {
+    DeviceBuffer buf;
+};
+
+struct Message {
+    std::shared_ptr<Payload> payload;
+    uint32_t depth = 0;
+    uint32_t plain_depth = 0;
+    Mag magnitude;
+    uint64_t* data() const { return payload->buf.get(); }
+};
+
+// Shared execution parameters (evaluator.hpp:16-41): device context, batch
+// size (images per message), depth budget, the stream all ops run on.
+class EvalContext {
+public:
+    EvalContext(Context& cx, uint32_t batch, uint32_t max_depth = 8, cudaStream_t stream = nullptr);
+    Context& device() const { return *cx_; }
+    uint32_t n() const { return cx_->n(); }
+    uint32_t half() const { return cx_->n() / 2; }
+    uint32_t batch() const { return batch_; }
+    uint32_t primes() const { return cx_->T(); }  // plaintext CRT primes
+    uint32_t max_depth() const { return max_depth_; }
+    const Mag& capacity() const { return capacity_; }
+    cudaStream_t stream() const { return stream_; }
+    uint64_t cts() const { return uint64_t(batch_) * cx_->T(); }
+    size_t payload_bytes() const { return cts() * 2 * cx_->L() * cx_->n() * 8; }
+
+private:
+    Context* cx_;
+    uint32_t batch_;
+    uint32_t max_depth_;
+    cudaStream_t stream_;
+    Mag capacity_;
+};
+
+// Shared cache of device-encoded plaintext operands keyed by value.
+struct PlainCache {
+    struct Entry {
+        std::vector<int64_t> values;
+        DeviceBuffer pt;  // [T][L][n]
+    };
+    std::unordered_map<uint64_t, std::vector<std::unique_ptr<Entry>>> mul, add;
+};
+
+class Evaluator {
+public:
+    explicit Evaluator(const EvalContext& cx);
+
+    const EvalContext& context() const { return *cx_; }
+    OpCounters& counters() { return counters_; }
+    const OpCounters& counters() const { return counters_; }
+
+    // Encoding boundary (no counters). lift: the same values for every
+    // message of the batch; lift_batch: values[b] per message; lift_gather:
+    // slot s of message b = images[b * stride + map[s]] (0 where map < 0),
+    // images already on the device.
+    Message lift(const std::vector<int64_t>& values) const;
+    Message lift_batch(const std::vector<std::vector<int64_t>>& values) const;
+    Message lift_gather(const int64_t* dev_images, uint64_t stride, const std::vector<int32_t>& map,
+                        int64_t max_abs) const;
+    // Decrypt + CRT + center every slot: device [B][n] signed 256-bit
+    // (4 little-endian words, two's complement). lower_slots gathers only
+    // the listed slots: [B][slots.size()] words.
+    DeviceBuffer lower(const Message& m) const;
+    DeviceBuffer lower_slots(const Message& m, const std::vector<uint32_t>& slots) const;
+
+    Message add(const Message& a, const Message& b);
+    Message add_plain(const Message& a, const std::vector<int64_t>& values);
+    Message mul(const Message& a, const Message& b);
+    Message mul_plain(const Message& a, const std::vector<int64_t>& values);
+    Message mask(const Message& a, const std::vector<uint8_t>& bits);
+    Message mul_scalar(const Message& a, int64_t s);
+    Message rotate_columns(const Message& a, int64_t k);
+    Message rotate_rows(const Message& a);
+    Message rotate_bundle(const Message& a, uint32_t amount);
+
+    void note_live(uint64_t live) { counters_.note_live(live); }
+    Evaluator fork() const;
+    void absorb(const Evaluator& child);
+
+private:
+    const EvalContext* cx_;
+    OpCounters counters_;
+    std::shared_ptr<PlainCache> cache_;
+    std::shared_ptr<uint64_t> next_id_;
+
+    Message fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const;
+    void check_magnitude(const Mag& m, const char* op) const;
+    const uint64_t* plain(const std::vector<int64_t>& values, bool for_add);
+    Message shift_columns(const Message& a, uint32_t right_by);
+};
+
+}  // namespace lb::lola
