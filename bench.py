@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""LoLa-MNIST encrypted inference throughput on B200 (BASELINE.json config 2).
+
+One step = one pass of the HE hot path (the lola-mnist plan at n = 16384,
+5 plaintext-prime BFV instances per image) over a batch of encrypted images
+already resident in HBM. Multi-GPU: one process per GPU (torchrun), images
+sharded across ranks with no collective on the data path;
+NCCL only for the barrier and the max-over-ranks timing.
+
+`--impl reference` times the reference's own CPU implementation (packnn,
+compiled in place into oracle/_ref/libpackref.so) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LoLa-MNIST encrypted inferences/s & latency; NTT/s, rotations/s vs roofline"
+UNIT = "inferences/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
+    ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
+    ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
+    return ap.parse_args()
+
+
+# ---- distributed plumbing -----------------------------------------------------------
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, value: float) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- clocks ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- CPU baseline (reference) ---------------------------------------------------------
+
+def _ref_worker(args):
+    idx_list, = args
+    from oracle import refbind as R
+    from paper_1812_10659_b200 import nets
+    from paper_1812_10659_b200.params import lola_mnist_params
+
+    net = nets.lola_mnist_net()
+    prm = lola_mnist_params()
+    tot = 0.0
+    for i in idx_list:
+        x = nets.images(2, net, 1, start=i)[0]
+        enc, steps = R.time_plan_steps(net, "lola-mnist", prm.n, prm.t, x, ring=True, threads=1)
+        tot += enc + float(steps.sum())
+    return tot
+
+
+def cpu_reference_throughput(images: int, procs: int) -> tuple[float, float]:
+    """Reference ring backend, encode + HE steps per image (decode excluded),
+    `procs` independent single-thread processes; returns (images/s, wall s)."""
+    import multiprocessing as mp
+
+    per = [list(range(p, images, procs)) for p in range(procs)]
+    per = [p for p in per if p]
+    t0 = time.perf_counter()
+    if len(per) == 1:
+        _ref_worker((per[0],))
+    else:
+        with mp.get_context("spawn").Pool(len(per)) as pool:
+            pool.map(_ref_worker, [(p,) for p in per])
+    wall = time.perf_counter() - t0
+    return images / wall, wall
+
+
+# ---- reference arm ----------------------------------------------------------------------
+
+def run_reference(a, world, rank):
+    if rank != 0:
+        return
+    from oracle import refbind as R
+
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpackref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    for _ in range(a.warmup):
+        cpu_reference_throughput(cores, cores)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        cpu_reference_throughput(cores, cores)
+    wall = time.perf_counter() - t0
+    value = a.steps * cores / wall
+    sample = (f"{cores} images per step (one per process, {cores} single-thread processes); "
+              "lola-mnist n=16384, 5 plaintext primes, ring backend, encode + HE steps (decode excluded: "
+              "the Boost stand-in BigInt is not representative)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": wall / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "lola-mnist cfg2 batched throughput (reference packnn ring backend, CPU)",
+                   "images_per_step": cores, "n": 16384, "plain_primes": 5},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---- our arm -----------------------------------------------------------------------------
+
+def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
+    """Dominant kernel (batched 64-bit NTT at n=16384) timed alone with CUDA
+    events on its launch stream, against the measured integer-pipe roof."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1812_10659_b200 import _native as nat
+
+    n, L = cx.n, cx.L
+    polys = max(1, limbs // L)
+    data = torch.randint(0, 2**59, (polys, L, n), dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        cx.ntt_forward(data, limbs=L, stream=s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(reps):
+        cx.ntt_forward(data, limbs=L, stream=s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    logn = n.bit_length() - 1
+    bfly = polys * L * (n // 2) * logn
+    peak = C.c_double()
+    nat.call("lb_bench_butterfly_peak", cx.params.q[0], 4, 4000, C.byref(peak))
+    achieved = bfly / (ms * 1e-3) / 1e9
+    hbm_bytes = polys * L * 16 * n
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
+    return {
+        "kernel": f"ntt_forward_kernel<14> ({polys * L} limbs of n={n}, 60-bit q)",
+        "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
+        "frac": achieved / (peak.value / 1e9),
+        "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
+        "traffic": None,
+        "launch_ms": ms,
+        "limb_transforms_per_s": polys * L / (ms * 1e-3),
+        "hbm_view": {"achieved_gbs": hbm_bytes / (ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                     "frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": hbm_bytes},
+    }
+
+
+def run_ours(a, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_1812_10659_b200 import _native as nat
+    from paper_1812_10659_b200 import nets
+    from paper_1812_10659_b200.bfv import BfvContext
+    from paper_1812_10659_b200.lola import Session, plan_counters
+    from paper_1812_10659_b200.params import lola_mnist_params
+
+    torch.cuda.set_device(local)
+    prm = lola_mnist_params()
+    cx = BfvContext(prm)
+    net = nets.lola_mnist_net(config=2)
+    B = a.batch
+    sess = Session(cx, net, "lola-mnist", B)
+    # images of this rank: a disjoint contiguous range of the 4096-image set
+    imgs = nets.images(2, net, B, start=rank * B)
+    dev_imgs = torch.from_numpy(imgs).cuda()
+    counters, _, _ = plan_counters(net, "lola-mnist", prm.n)
+    rot_per_image = int(counters[:, 5:7].sum()) * len(prm.t)
+    s = torch.cuda.current_stream()
+
+    # warm-up: key generation, plaintext encoding, pool growth
+    sess.encrypt(dev_imgs, on_device=True)
+    for _ in range(a.warmup):
+        sess.execute()
+    torch.cuda.synchronize()
+
+    # ---- value: HE steps, encrypted inputs resident in HBM ----
+    launches0 = int(nat.lib().lb_launch_count())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(a.steps):
+            sess.execute()
+        e1.record(s)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = int(nat.lib().lb_launch_count()) - launches0
+    elapsed = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
+    value = world * B * a.steps / elapsed
+
+    # ---- e2e: host images -> encrypt -> HE steps -> decrypt -> host scores ----
+    host_imgs = np.ascontiguousarray(imgs)
+    scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
+    sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)  # warm
+    barrier(world)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(a.steps):
+        sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)
+    e1.record(s)
+    torch.cuda.synchronize()
+    barrier(world)
+    e2e_elapsed = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
+    e2e_value = world * B * a.steps / e2e_elapsed
+
+    extras = {}
+    if rank == 0 and not a.no_extras:
+        del sess
+        torch.cuda.empty_cache()
+        # single-image latency (server-side HE steps, and end to end)
+        one = Session(cx, net, "lola-mnist", 1)
+        one_img = torch.from_numpy(imgs[:1].copy()).cuda()
+        one.encrypt(one_img, on_device=True)
+        for _ in range(3):
+            one.execute()
+        torch.cuda.synchronize()
+        lat = []
+        for _ in range(5):
+            e0.record(s)
+            one.execute()
+            e1.record(s)
+            torch.cuda.synchronize()
+            lat.append(e0.elapsed_time(e1))
+        sc1 = np.zeros((1, one.outputs, 4), dtype=np.uint64)
+        lat_e2e = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            one.run_raw(np.ascontiguousarray(imgs[:1]), sc1, False, False, want_counters=False, want_times=False)
+            lat_e2e.append((time.perf_counter() - t0) * 1e3)
+        del one
+        torch.cuda.empty_cache()
+        extras["latency_ms"] = {"he_steps": min(lat), "e2e": min(lat_e2e), "images": 1}
+        # roofline of the dominant kernel, at the batch's key-switch limb count
+        ks_limbs = B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1)
+        extras["roofline"] = ntt_roofline(cx, ks_limbs)
+        # CPU baseline: the reference on this host, one thread, bounded sample
+        try:
+            from oracle import refbind as R
+
+            if R.available():
+                ips, wall = cpu_reference_throughput(a.cpu_sample, 1)
+                extras["cpu_baseline"] = {
+                    "value": ips, "unit": UNIT, "cores": 1, "kind": "reference",
+                    "sample": f"{a.cpu_sample} images, reference packnn ring backend (plaintext semantics, no "
+                              f"encryption), encode + HE steps, decode excluded; {wall:.1f} s"}
+        except Exception as exc:  # reported, never fatal to the GPU number
+            extras["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": elapsed / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (SplitMix64-seeded pixels and weights)",
+            "config": {"workload": "lola-mnist cfg2 batched throughput", "images_per_gpu_per_step": B,
+                       "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
+                       "q_bits": 60, "parallelism": f"images sharded over {world} GPU(s), no collective",
+                       "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes) * world,
+                    "d2h_bytes_per_step": int(scores.nbytes) * world},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "rotations_per_s": value * rot_per_image,
+            "key_switches_per_image": rot_per_image + 2 * len(prm.t),
+        }
+        line.update(extras)
+        print(json.dumps(line))
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_setup(a.gpus)
+    if a.impl == "reference":
+        run_reference(a, world, rank)
+    else:
+        run_ours(a, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -180,7 +180,18 @@ int lb_lola_session_info(const lb_lola_session* s, uint32_t* steps, uint64_t* ou
 int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on_device, uint64_t* scores,
                         int scores_on_device, uint64_t* counters, double* times);
 
+/* The same three phases separately: encrypt keeps the encrypted input in the
+ * session (images on host or device), execute runs the HE steps on it
+ * (input kept, so execute can repeat) and keeps the encrypted result,
+ * decrypt decodes that result into scores. */
+int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int images_on_device);
+int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters);
+int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device);
+
 /* ---- measurement ------------------------------------------------------- */
+
+/* kernels launched by this library since load (monotonic) */
+uint64_t lb_launch_count(void);
 
 /* Integer-pipe roof: sustained register-resident Harvey/Shoup butterflies per
  * second (the same butterfly the NTT runs), grid = SMs x blocks_per_sm. */

@@ -62,6 +62,7 @@ _SIGS: dict[str, list] = {
 _VALUE_SIGS: dict[str, tuple] = {
     "lb_galois_exponent_columns": (u64, [u32, u32]),
     "lb_galois_exponent_rows": (u64, [u32]),
+    "lb_launch_count": (u64, []),
 }
 
 _lib: C.CDLL | None = None

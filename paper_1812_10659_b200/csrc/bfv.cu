@@ -634,7 +634,7 @@ void bfv_setup(Context& cx) {
     const uint32_t nsec = L + K + M;
     st->secret = DeviceBuffer(size_t(nsec) * n * 8, s);
     k_secret_coeffs<<<grid_for(uint64_t(nsec) * n), kBlock, 0, s>>>(d, st->secret.get(), nsec);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     d.s_ntt = st->secret.get();
     cx.bfv_ = std::move(st);
     cx.ntt_forward(LimbBatch{cx.bfv_->secret.get(), 1, nsec, 0, uint64_t(nsec) * n}, s);
@@ -649,7 +649,7 @@ void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t p
     const uint64_t total = uint64_t(polys) * limbs * cx.n();
     if (!total) return;
     k_automorph<<<grid_for(total), kBlock, 0, s>>>(in, out, total, cx.logn(), galois);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
@@ -669,13 +669,13 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     } else {
         automorphism_ntt(cx, d.s_ntt, target.get(), 1, LK, key_id, s);
     }
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     k_keygen_error<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{err.get(), d.dnum, LK, 0, uint64_t(LK) * n}, s);
     k_keygen_finish<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get(), target.get(),
                                                                              d.p_mod_qp, key.buf.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     st.keys.emplace(key_id, std::move(key));
 }
 
@@ -711,7 +711,7 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     // (b) ModUp
     DeviceBuffer ext(uint64_t(count) * d.dnum * LK * n * 8, s);
     k_modup<<<grid_for(uint64_t(count) * d.dnum * n), kBlock, 0, s>>>(d, dc.get(), count, ext.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     // (c) transform the extensions, skipping each digit's own primes
     {
         LimbBatch lb{ext.get(), count * d.dnum, LK, 0, uint64_t(LK) * n};
@@ -723,16 +723,16 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
     k_ks_inner<<<grid_for(uint64_t(count) * LK * n), kBlock, 0, s>>>(d, d_ntt, d_stride, ext.get(), key, count,
                                                                        acc.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     // (e) ModDown: P limbs to coefficients, convert, back to evaluations
     cx.ntt_inverse(LimbBatch{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n}, s);
     DeviceBuffer conv(uint64_t(count) * 2 * L * n * 8, s);
     k_moddown_conv<<<grid_for(uint64_t(count) * 2 * n), kBlock, 0, s>>>(d, acc.get(), count, conv.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{conv.get(), count * 2, L, 0, uint64_t(L) * n}, s);
     k_moddown_final<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, acc.get(), conv.get(), count, add0, add1,
                                                                           add_stride, out0, out1, out_stride);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 }  // namespace
@@ -753,16 +753,16 @@ void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_b
     const uint32_t count = B * T;
     DeviceBuffer m(uint64_t(count) * n * 8, s);
     k_scatter_slots<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, values, B, m.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     LimbBatch tb{m.get(), count, 1, 0, n};
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
     k_enc_coeffs<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, m.get(), count, id_base, out);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{out, count, L, 0, 2ull * L * n}, s);
     k_enc_finish<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, count, id_base, out);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
@@ -771,10 +771,10 @@ void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, 
     const uint32_t n = d.n, L = d.L, count = B * d.T;
     DeviceBuffer x(uint64_t(count) * L * n * 8, s);
     k_phase<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, ct, count, x.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_inverse(LimbBatch{x.get(), count, L, 0, uint64_t(L) * n}, s);
     k_dec_scale<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, x.get(), count, out);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
@@ -788,7 +788,7 @@ void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, c
     tb.map_period = T;
     cx.ntt_forward(tb, s);
     k_gather_slots<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, out);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, cudaStream_t s) {
@@ -796,13 +796,13 @@ void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t
     const uint32_t n = d.n, T = d.T, L = d.L;
     DeviceBuffer m(uint64_t(T) * n * 8, s);
     k_scatter_slots<<<grid_for(uint64_t(T) * n), kBlock, 0, s>>>(d, values, 1, m.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     LimbBatch tb{m.get(), T, 1, 0, n};
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
     k_pt_lift<<<grid_for(uint64_t(T) * L * n), kBlock, 0, s>>>(d, m.get(), pt_mul, pt_add);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     if (pt_mul) cx.ntt_forward(LimbBatch{pt_mul, T, L, 0, uint64_t(L) * n}, s);
     if (pt_add) cx.ntt_forward(LimbBatch{pt_add, T, L, 0, uint64_t(L) * n}, s);
 }
@@ -812,7 +812,7 @@ void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
     if (!total) return;
     k_add<<<grid_for(total), kBlock, 0, s>>>(d, a, b, out, total);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
@@ -827,7 +827,7 @@ void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out
         tab.v[i] = make_ulonglong2(v, shoup_companion(v, q));
     }
     k_mul_scalar<<<grid_for(total), kBlock, 0, s>>>(d, a, tab, out, total);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
@@ -835,7 +835,7 @@ void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* 
     const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
     if (!total) return;
     k_mul_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
@@ -843,7 +843,7 @@ void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* 
     const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
     if (!total) return;
     k_add_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
 }
 
 void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s) {
@@ -871,12 +871,12 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
     k_exact_extend<<<grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(
         d, X.get(), count * 4, L, 0, d.qhat_inv, d.q_frac, d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
     // (d) tensor over Q ∪ B
     DeviceBuffer D(uint64_t(count) * 3 * LM * n * 8, s);
     k_tensor<<<grid_for(uint64_t(count) * LM * n), kBlock, 0, s>>>(d, a, b, Y.get(), count, D.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     // (e) back to coefficients over Q ∪ B
     LimbBatch db{D.get(), count * 3, LM, 0, uint64_t(LM) * n};
     db.prime_map = cx.bfv()->qb_map;
@@ -885,11 +885,11 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     // (f) scale by t/Q into B, (g) exact B -> Q, (h) to evaluations
     DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);
     k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     DeviceBuffer E(uint64_t(count) * 3 * LN * 8, s);
     k_exact_extend<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
         d, Z.get(), count * 3, M, d.bbase, d.bhat_inv, d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, E.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{E.get(), count * 3, L, 0, LN}, s);
     // (i) relinearize e2 and add into (e0, e1)
     key_switch_impl(cx, E.get() + 2 * LN, 3 * LN, kRelinKeyId, count, E.get(), E.get() + LN, 3 * LN, out, out + LN,

@@ -6,6 +6,11 @@
 
 namespace lb {
 
+std::atomic<uint64_t>& launch_counter() {
+    static std::atomic<uint64_t> count{0};
+    return count;
+}
+
 Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
     if (n_ < 4096 || n_ > 32768 || (n_ & (n_ - 1)))
         throw std::invalid_argument("ring degree must be a power of two in [4096, 32768]");
@@ -123,6 +128,7 @@ void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaSt
         LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN>, b, primes));
     else
         LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN>, b, primes));
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
 void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {

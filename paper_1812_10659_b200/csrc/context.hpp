@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -31,6 +32,15 @@ struct CudaError : std::runtime_error {
         cudaError_t _e = (expr);                                                                   \
         if (_e != cudaSuccess)                                                                     \
             throw ::lb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)
+
+// Kernels launched by this library (bench.py reports the count inside its
+// timed region).
+std::atomic<uint64_t>& launch_counter();
+#define LB_KERNEL_DONE()                                          \
+    do {                                                          \
+        LB_CUDA(cudaGetLastError());                              \
+        ::lb::launch_counter().fetch_add(1, std::memory_order_relaxed); \
     } while (0)
 
 // Owning device allocation (stream-ordered pool).

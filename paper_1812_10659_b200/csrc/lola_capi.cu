@@ -72,7 +72,48 @@ struct lb_lola_session {
     uint32_t batch = 0;
     uint64_t outputs = 0;
     uint64_t input_values = 0;
+    lb::lola::EncodedTensor input;   // encrypted input (kept by encrypt)
+    lb::lola::EncodedTensor output;  // encrypted scores (kept by execute)
+    std::vector<lb::lola::CounterDelta> per_step;
 };
+
+namespace {
+
+void phase_encrypt(lb_lola_session* s, const int64_t* images, int on_device) {
+    cudaStream_t st = s->ecx->stream();
+    lb::DeviceBuffer dimg;
+    const int64_t* img = images;
+    if (!on_device) {
+        dimg = lb::DeviceBuffer(uint64_t(s->batch) * s->input_values * 8, st);
+        LB_CUDA(cudaMemcpyAsync(dimg.get(), images, uint64_t(s->batch) * s->input_values * 8, cudaMemcpyHostToDevice,
+                                st));
+        img = dimg.get<int64_t>();
+    }
+    s->input = s->plan.encode_input(*s->ev, img);
+}
+
+void phase_execute(lb_lola_session* s, bool keep_input) {
+    if (s->input.messages.empty()) throw std::invalid_argument("no encrypted input: call encrypt first");
+    lb::lola::Evaluator& ev = *s->ev;
+    ev.counters() = lb::lola::OpCounters{};
+    lb::lola::EncodedTensor in = keep_input ? s->input : std::move(s->input);
+    lb::lola::ExecutionResult res = lb::lola::execute(s->plan, std::move(in), ev);
+    s->output = std::move(res.output);
+    s->per_step = std::move(res.per_step);
+}
+
+void phase_decrypt(lb_lola_session* s, uint64_t* scores, int on_device) {
+    if (s->output.messages.empty()) throw std::invalid_argument("no result: call execute first");
+    cudaStream_t st = s->ecx->stream();
+    lb::DeviceBuffer dec = lb::lola::decode_values(*s->ev, s->output);
+    const uint64_t bytes = uint64_t(s->batch) * s->outputs * 32;
+    if (dec.bytes() != bytes) throw std::logic_error("decoded output size mismatch");
+    LB_CUDA(cudaMemcpyAsync(scores, dec.get(), bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            st));
+    LB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -125,31 +166,16 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
         using clock = std::chrono::steady_clock;
         cudaStream_t st = s->ecx->stream();
         const auto t0 = clock::now();
-        lb::DeviceBuffer dimg;
-        const int64_t* img = images;
-        if (!images_on_device) {
-            dimg = lb::DeviceBuffer(uint64_t(s->batch) * s->input_values * 8, st);
-            LB_CUDA(cudaMemcpyAsync(dimg.get(), images, uint64_t(s->batch) * s->input_values * 8,
-                                    cudaMemcpyHostToDevice, st));
-            img = dimg.get<int64_t>();
-        }
-        lb::lola::Evaluator& ev = *s->ev;
-        ev.counters() = lb::lola::OpCounters{};
-        lb::lola::EncodedTensor input = s->plan.encode_input(ev, img);
+        phase_encrypt(s, images, images_on_device);
         if (times) LB_CUDA(cudaStreamSynchronize(st));
         const auto t1 = clock::now();
-        lb::lola::ExecutionResult res = lb::lola::execute(s->plan, std::move(input), ev);
+        phase_execute(s, false);
         if (times) LB_CUDA(cudaStreamSynchronize(st));
         const auto t2 = clock::now();
-        lb::DeviceBuffer dec = lb::lola::decode_values(ev, res.output);
-        const uint64_t bytes = uint64_t(s->batch) * s->outputs * 32;
-        if (dec.bytes() != bytes) throw std::logic_error("decoded output size mismatch");
-        LB_CUDA(cudaMemcpyAsync(scores, dec.get(), bytes,
-                                scores_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-        LB_CUDA(cudaStreamSynchronize(st));
+        phase_decrypt(s, scores, scores_on_device);
         const auto t3 = clock::now();
         if (counters)
-            for (size_t i = 0; i < res.per_step.size(); ++i) put_counters(res.per_step[i], counters + 7 * i);
+            for (size_t i = 0; i < s->per_step.size(); ++i) put_counters(s->per_step[i], counters + 7 * i);
         if (times) {
             times[0] = std::chrono::duration<double>(t1 - t0).count();
             times[1] = std::chrono::duration<double>(t2 - t1).count();
@@ -157,5 +183,23 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
         }
     });
 }
+
+int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int images_on_device) {
+    return guarded([&] { phase_encrypt(s, images, images_on_device); });
+}
+
+int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters) {
+    return guarded([&] {
+        phase_execute(s, true);
+        if (counters)
+            for (size_t i = 0; i < s->per_step.size(); ++i) put_counters(s->per_step[i], counters + 7 * i);
+    });
+}
+
+int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device) {
+    return guarded([&] { phase_decrypt(s, scores, scores_on_device); });
+}
+
+uint64_t lb_launch_count(void) { return lb::launch_counter().load(); }
 
 }  // extern "C"

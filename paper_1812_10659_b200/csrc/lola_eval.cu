@@ -284,7 +284,7 @@ Message Evaluator::lift_gather(const int64_t* dev_images, uint64_t stride, const
     LB_CUDA(cudaMemcpyAsync(dmap.get(), full.data(), uint64_t(n) * 4, cudaMemcpyHostToDevice, s));
     k_gather_lift<<<blocks(uint64_t(B) * n), kBlock, 0, s>>>(dev_images, stride, dmap.get<int32_t>(), n, B,
                                                              slots.get<int64_t>());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     Message m = fresh(0, 0, mag);
     const uint64_t id = *next_id_;
     *next_id_ += cx_->cts();
@@ -325,7 +325,7 @@ DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t
     DeviceBuffer out(uint64_t(B) * ns * 4 * 8, s);
     k_crt_center<<<blocks(uint64_t(B) * ns), kBlock, 0, s>>>(res.get(), n, B, slots.empty() ? nullptr : dsl.get<uint32_t>(),
                                                              ns, tab, out.get());
-    LB_CUDA(cudaGetLastError());
+    LB_KERNEL_DONE();
     LB_CUDA(cudaStreamSynchronize(s));  // `slots` may be a temporary
     return out;
 }

@@ -38,6 +38,9 @@ _SIGS = {
     "lb_lola_session_destroy": [vp],
     "lb_lola_session_info": [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "lb_lola_session_run": [vp, vp, C.c_int, vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double)],
+    "lb_lola_session_encrypt": [vp, vp, C.c_int],
+    "lb_lola_session_execute": [vp, C.POINTER(C.c_uint64)],
+    "lb_lola_session_decrypt": [vp, vp, C.c_int],
 }
 nat.register(_SIGS)
 
@@ -126,6 +129,23 @@ class Session:
                  counters, times)
         cnt = np.frombuffer(counters, dtype=np.uint64).reshape(-1, 7).astype(np.int64) if want_counters else None
         return cnt, (list(times) if want_times else None)
+
+    # separate phases (inputs resident on the device between them)
+    def encrypt(self, images, on_device: bool = False) -> None:
+        ptr = images.data_ptr() if on_device else np.ascontiguousarray(images, dtype=np.int64).ctypes.data
+        if not on_device:
+            self._host_images = images  # keep alive until the copy is issued
+        nat.call("lb_lola_session_encrypt", self.handle, ptr, int(on_device))
+
+    def execute(self, want_counters: bool = False):
+        counters = (C.c_uint64 * (7 * self.steps))() if want_counters else None
+        nat.call("lb_lola_session_execute", self.handle, counters)
+        return np.frombuffer(counters, dtype=np.uint64).reshape(-1, 7).astype(np.int64) if want_counters else None
+
+    def decrypt(self):
+        scores = np.zeros((self.batch, self.outputs, 4), dtype=np.uint64)
+        nat.call("lb_lola_session_decrypt", self.handle, scores.ctypes.data, 0)
+        return [[words_to_int(scores[b, i]) for i in range(self.outputs)] for b in range(self.batch)]
 
     def run(self, images: np.ndarray):
         """Host images [batch][input_values] -> (scores [batch][outputs] Python
