@@ -10,6 +10,7 @@
 #include "bfv.hpp"
 #include "bfv_kernels.cuh"
 #include "host_math.hpp"
+#include "ks_fused.cuh"
 
 namespace lb {
 
@@ -99,6 +100,25 @@ __global__ void k_keygen_finish(BfvDev d, uint64_t key_id, const uint64_t* __res
     const uint64_t base = (uint64_t(j) * 2 * LK + r) * d.n + pos;
     key[base] = b;
     key[base + uint64_t(LK) * d.n] = a;
+}
+
+// (k, floor(k 2^64 / q)) for every key entry; rows of n entries share a prime
+__global__ void k_shoup_pairs(BfvDev d, const uint64_t* __restrict__ key, ulonglong2* __restrict__ out, uint64_t total,
+                              uint32_t limbs) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const Modulus m = modulus_of(d.primes[(idx / d.n) % limbs]);
+    const uint64_t k = key[idx];
+    // estimate from the 128-bit ratio (never too large), then correct
+    uint64_t est = k * m.ratio_hi + mulhi64(k, m.ratio_lo);
+    uint64_t lo = 0 - est * m.q;
+    uint64_t hi = k - mulhi64(est, m.q) - (est * m.q != 0 ? 1 : 0);
+    while (hi != 0 || lo >= m.q) {
+        ++est;
+        hi -= (lo < m.q) ? 1 : 0;
+        lo -= m.q;
+    }
+    out[idx] = make_ulonglong2(k, est);
 }
 
 __global__ void k_square_limbs(const uint64_t* __restrict__ s, uint64_t* __restrict__ out, BfvDev d, uint32_t limbs) {
@@ -260,102 +280,6 @@ __global__ void k_add_plain(BfvDev d, const uint64_t* __restrict__ a, const uint
     const uint32_t j = c % d.T;
     const uint64_t v = a[idx];
     out[idx] = comp ? v : add_mod(v, pt[(uint64_t(j) * d.L + i) * d.n + pos], d.primes[i].q);
-}
-
-// ---- key switching (§3.5) ----
-// ModUp: ext[c][j][r] = sum_{i in digit j} [d_i Dhat_i^-1]_{q_i} [Dhat_i]_r for r outside digit j
-__global__ void k_modup(BfvDev d, const uint64_t* __restrict__ dc /*[count][L][n] coeff*/, uint32_t count,
-                        uint64_t* __restrict__ ext /*[count][dnum][L+K][n]*/) {
-    const uint32_t LK = d.L + d.K;
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * d.dnum * d.n) return;
-    const uint32_t k = idx % d.n;
-    const uint32_t j = (idx / d.n) % d.dnum;
-    const uint64_t c = idx / (uint64_t(d.n) * d.dnum);
-    const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
-    uint64_t y[16];
-#pragma unroll 1
-    for (uint32_t i = lo; i < hi; ++i) {
-        const Modulus qm = modulus_of(d.primes[i]);
-        y[i - lo] = mul_mod(dc[(c * d.L + i) * d.n + k], d.dhat_inv[i], qm);
-    }
-    uint64_t* dst = ext + ((c * d.dnum + j) * LK) * d.n + k;
-#pragma unroll 1
-    for (uint32_t r = 0; r < LK; ++r) {
-        if (r >= lo && r < hi) continue;
-        const Modulus rm = modulus_of(d.primes[r]);
-        Acc128 acc;
-        for (uint32_t i = lo; i < hi; ++i) acc.mac(y[i - lo], d.dhat_mod[i * LK + r]);
-        dst[uint64_t(r) * d.n] = reduce_acc(acc, rm);
-    }
-}
-
-// acc_h[c][r] = sum_j X_j[r] * key[j][h][r], X_j[r] = d[r] inside digit j else ext
-__global__ void k_ks_inner(BfvDev d, const uint64_t* __restrict__ dn /*NTT input*/, uint64_t d_stride,
-                           const uint64_t* __restrict__ ext, const uint64_t* __restrict__ key, uint32_t count,
-                           uint64_t* __restrict__ acc /*[count][2][L+K][n]*/) {
-    const uint32_t LK = d.L + d.K;
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * LK * d.n) return;
-    const uint32_t pos = idx % d.n;
-    const uint32_t r = (idx / d.n) % LK;
-    const uint64_t c = idx / (uint64_t(d.n) * LK);
-    const Modulus rm = modulus_of(d.primes[r]);
-    Acc128 a0, a1;
-    for (uint32_t j = 0; j < d.dnum; ++j) {
-        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
-        const uint64_t x = (r >= lo && r < hi) ? dn[c * d_stride + uint64_t(r) * d.n + pos]
-                                               : ext[((c * d.dnum + j) * LK + r) * d.n + pos];
-        const uint64_t kb = (uint64_t(j) * 2 * LK + r) * d.n + pos;
-        a0.mac(x, key[kb]);
-        a1.mac(x, key[kb + uint64_t(LK) * d.n]);
-    }
-    acc[(c * 2 * LK + r) * d.n + pos] = reduce_acc(a0, rm);
-    acc[(c * 2 * LK + LK + r) * d.n + pos] = reduce_acc(a1, rm);
-}
-
-// ModDown conversion: conv[c][h][r] = sum_l [accP_l Phat_l^-1]_{p_l} [Phat_l]_{q_r}
-__global__ void k_moddown_conv(BfvDev d, const uint64_t* __restrict__ acc, uint32_t count, uint64_t* __restrict__ conv) {
-    const uint32_t LK = d.L + d.K;
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * 2 * d.n) return;
-    const uint32_t k = idx % d.n;
-    const uint64_t ch = idx / d.n;  // c * 2 + h
-    uint64_t y[8];
-    for (uint32_t l = 0; l < d.K; ++l) {
-        const Modulus pm = modulus_of(d.primes[d.pbase + l]);
-        y[l] = mul_mod(acc[(ch * LK + d.L + l) * d.n + k], d.phat_inv[l], pm);
-    }
-    for (uint32_t r = 0; r < d.L; ++r) {
-        const Modulus qm = modulus_of(d.primes[r]);
-        Acc128 s;
-        for (uint32_t l = 0; l < d.K; ++l) s.mac(y[l], d.phat_mod_q[l * d.L + r]);
-        conv[(ch * d.L + r) * d.n + k] = reduce_acc(s, qm);
-    }
-}
-
-// u_h = (acc_h - conv_h) P^-1; out_h = add_h + u_h (add_h optional)
-__global__ void k_moddown_final(BfvDev d, const uint64_t* __restrict__ acc, const uint64_t* __restrict__ conv,
-                                uint32_t count, const uint64_t* __restrict__ add0, const uint64_t* __restrict__ add1,
-                                uint64_t add_stride, uint64_t* __restrict__ out0, uint64_t* __restrict__ out1,
-                                uint64_t out_stride) {
-    const uint32_t LK = d.L + d.K;
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * d.L * d.n) return;
-    const uint32_t pos = idx % d.n;
-    const uint32_t r = (idx / d.n) % d.L;
-    const uint64_t c = idx / (uint64_t(d.n) * d.L);
-    const Modulus qm = modulus_of(d.primes[r]);
-    const uint64_t off = uint64_t(r) * d.n + pos;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint64_t a = acc[(c * 2 + h) * LK * d.n + off];
-        const uint64_t v = conv[(c * 2 + h) * d.L * d.n + off];
-        uint64_t u = mul_mod(sub_mod(a, v, qm.q), d.p_inv_q[r], qm);
-        const uint64_t* add = h ? add1 : add0;
-        if (add) u = add_mod(u, add[c * add_stride + off], qm.q);
-        (h ? out1 : out0)[c * out_stride + off] = u;
-    }
 }
 
 // ---- multiplication (§3.6) ----
@@ -585,6 +509,19 @@ void bfv_setup(Context& cx) {
     const size_t o_phinv = put(phat_inv.data(), phat_inv.size() * 8);
     const size_t o_phmq = put(phat_mod_q.data(), phat_mod_q.size() * 8);
     const size_t o_piq = put(p_inv_q.data(), L * 8);
+    std::vector<ulonglong2> p_inv_shoup(L);
+    for (uint32_t i = 0; i < L; ++i) p_inv_shoup[i] = make_ulonglong2(p_inv_q[i], shoup_companion(p_inv_q[i], q[i]));
+    const size_t o_pish = put(p_inv_shoup.data(), L * 16);
+    {
+        // the fused key switch feeds single-prime digits and [acc]_P into the
+        // lazy transform unreduced: every prime of Q and P must be < 4x any other
+        uint64_t lo = ~uint64_t{0}, hi = 0;
+        for (uint32_t r = 0; r < LK; ++r) {
+            lo = std::min(lo, qp[r]);
+            hi = std::max(hi, qp[r]);
+        }
+        if (hi / 4 >= lo) throw std::invalid_argument("ciphertext and special primes must be within a factor 4");
+    }
     std::vector<uint64_t> p_mod_qp(LK);
     for (uint32_t r = 0; r < LK; ++r) p_mod_qp[r] = prod_mod(p, 0, K, SIZE_MAX, qp[r]);
     const size_t o_pmqp = put(p_mod_qp.data(), LK * 8);
@@ -626,6 +563,7 @@ void bfv_setup(Context& cx) {
     d.phat_mod_q = reinterpret_cast<const uint64_t*>(base + o_phmq);
     d.p_inv_q = reinterpret_cast<const uint64_t*>(base + o_piq);
     d.p_mod_qp = reinterpret_cast<const uint64_t*>(base + o_pmqp);
+    d.p_inv_shoup = reinterpret_cast<const ulonglong2*>(base + o_pish);
     st->t_map = reinterpret_cast<const int16_t*>(base + o_tmap);
     st->qb_map = reinterpret_cast<const int16_t*>(base + o_qbmap);
     st->ks_map = reinterpret_cast<const int16_t*>(base + o_ksmap);
@@ -676,7 +614,18 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     k_keygen_finish<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get(), target.get(),
                                                                              d.p_mod_qp, key.buf.get());
     LB_KERNEL_DONE();
+    key.shoup = DeviceBuffer(key_elems * 16, s);
+    k_shoup_pairs<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<ulonglong2>(), key_elems, LK);
+    LB_KERNEL_DONE();
     st.keys.emplace(key_id, std::move(key));
+}
+
+static const ulonglong2* key_shoup_ptr(Context& cx, uint64_t key_id) {
+    BfvState& st = *cx.bfv();
+    std::lock_guard<std::mutex> lock(st.mu);
+    auto it = st.keys.find(key_id);
+    if (it == st.keys.end()) throw std::invalid_argument("key not generated");
+    return it->second.shoup.get<ulonglong2>();
 }
 
 const uint64_t* key_ptr(Context& cx, uint64_t key_id) {
@@ -691,48 +640,90 @@ const uint64_t* key_ptr(Context& cx, uint64_t key_id) {
 
 namespace {
 
-// Key switch `count` polys d (NTT domain over Q, stride d_stride) and write
-// out_h = add_h + u_h (stride out_stride; add_h may be null).
-void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint64_t key_id, uint32_t count,
-                     const uint64_t* add0, const uint64_t* add1, uint64_t add_stride, uint64_t* out0, uint64_t* out1,
-                     uint64_t out_stride, cudaStream_t s) {
+template <int LOGN>
+void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
+    using S = NttShape<LOGN>;
+    const size_t smem = 3ull * S::M * 8;
+    static bool configured = false;
+    if (!configured) {
+        LB_CUDA(cudaFuncSetAttribute(ks_inner_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * (d.L + d.K) * S::CL));
+    cfg.blockDim = dim3(S::T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_kernel<LOGN>, d, a));
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
+template <int LOGN>
+void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
+    using S = NttShape<LOGN>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * 2 * d.L * S::CL));
+    cfg.blockDim = dim3(S::T);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN>, d, a));
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
+void dispatch_ks(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDownArgs* ma, cudaStream_t s) {
+    switch (logn) {
+        case 12: ma ? launch_moddown<12>(d, *ma, s) : launch_ks_inner<12>(d, ka, s); break;
+        case 13: ma ? launch_moddown<13>(d, *ma, s) : launch_ks_inner<13>(d, ka, s); break;
+        case 14: ma ? launch_moddown<14>(d, *ma, s) : launch_ks_inner<14>(d, ka, s); break;
+        case 15: ma ? launch_moddown<15>(d, *ma, s) : launch_ks_inner<15>(d, ka, s); break;
+        default: throw std::invalid_argument("unsupported ring degree");
+    }
+}
+
+// Key switch `count` polys d (evaluations over Q, stride d_stride, read
+// through x -> x^d_galois when nonzero) and write out_h = add_h + u_h
+// (stride out_stride; add_h optional, read through add_galois).
+//   1. inverse NTT of d (automorphism folded into the load)
+//   2. fused ModUp + NTT + key inner product over Q ∪ P   (ks_inner_kernel)
+//   3. inverse NTT of the P limbs of both accumulators
+//   4. fused P->Q conversion + NTT + ModDown epilogue     (moddown_kernel)
+void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint64_t d_galois, uint64_t key_id,
+                     uint32_t count, const uint64_t* add0, const uint64_t* add1, uint64_t add_stride,
+                     uint64_t add_galois, uint64_t* out0, uint64_t* out1, uint64_t out_stride, cudaStream_t s) {
     if (!count) return;
     BfvState& st = *cx.bfv();
     const BfvDev& d = st.dev;
     if (d.K == 0) throw std::invalid_argument("key switching needs special primes");
     ensure_key(cx, key_id, s);
-    const uint64_t* key = key_ptr(cx, key_id);
+    const ulonglong2* key = key_shoup_ptr(cx, key_id);
     const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
-    // (a) coefficient-domain copy of d
     DeviceBuffer dc(uint64_t(count) * L * n * 8, s);
-    LB_CUDA(cudaMemcpy2DAsync(dc.get(), uint64_t(L) * n * 8, d_ntt, d_stride * 8, uint64_t(L) * n * 8, count,
-                              cudaMemcpyDeviceToDevice, s));
-    cx.ntt_inverse(LimbBatch{dc.get(), count, L, 0, uint64_t(L) * n}, s);
-    // (b) ModUp
-    DeviceBuffer ext(uint64_t(count) * d.dnum * LK * n * 8, s);
-    k_modup<<<grid_for(uint64_t(count) * d.dnum * n), kBlock, 0, s>>>(d, dc.get(), count, ext.get());
-    LB_KERNEL_DONE();
-    // (c) transform the extensions, skipping each digit's own primes
     {
-        LimbBatch lb{ext.get(), count * d.dnum, LK, 0, uint64_t(LK) * n};
-        lb.prime_map = st.ks_map;
-        lb.map_period = d.dnum * LK;
-        cx.ntt_forward(lb, s);
+        LimbBatch lb{dc.get(), count, L, 0, uint64_t(L) * n};
+        lb.src = d_ntt;
+        lb.src_stride = d_stride;
+        lb.galois = d_galois;
+        cx.ntt_inverse(lb, s);
     }
-    // (d) inner product with the key
     DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
-    k_ks_inner<<<grid_for(uint64_t(count) * LK * n), kBlock, 0, s>>>(d, d_ntt, d_stride, ext.get(), key, count,
-                                                                       acc.get());
-    LB_KERNEL_DONE();
-    // (e) ModDown: P limbs to coefficients, convert, back to evaluations
+    KsInnerArgs ka{dc.get(), d_ntt, d_stride, d_galois, key, acc.get(), count};
+    dispatch_ks(cx.logn(), d, ka, nullptr, s);
     cx.ntt_inverse(LimbBatch{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n}, s);
-    DeviceBuffer conv(uint64_t(count) * 2 * L * n * 8, s);
-    k_moddown_conv<<<grid_for(uint64_t(count) * 2 * n), kBlock, 0, s>>>(d, acc.get(), count, conv.get());
-    LB_KERNEL_DONE();
-    cx.ntt_forward(LimbBatch{conv.get(), count * 2, L, 0, uint64_t(L) * n}, s);
-    k_moddown_final<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, acc.get(), conv.get(), count, add0, add1,
-                                                                          add_stride, out0, out1, out_stride);
-    LB_KERNEL_DONE();
+    ModDownArgs ma{acc.get(), add0, add1, add_stride, add_galois, out0, out1, out_stride, d.p_inv_shoup, count};
+    dispatch_ks(cx.logn(), d, ka, &ma, s);
 }
 
 }  // namespace
@@ -740,7 +731,7 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
 void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
                 cudaStream_t s) {
     const uint64_t LN = uint64_t(cx.L()) * cx.n();
-    key_switch_impl(cx, d, LN, key_id, count, nullptr, nullptr, 0, u0, u1, LN, s);
+    key_switch_impl(cx, d, LN, 0, key_id, count, nullptr, nullptr, 0, 0, u0, u1, LN, s);
 }
 
 // ---- public ciphertext operations ----------------------------------------------
@@ -849,10 +840,17 @@ void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* 
 void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
+    if (galois % 2 == 0 || galois >= 2ull * d.n) throw std::invalid_argument("galois element must be odd in [1, 2n)");
     const uint64_t LN = uint64_t(d.L) * d.n;
-    DeviceBuffer rot(uint64_t(count) * 2 * LN * 8, s);
-    automorphism_ntt(cx, a, rot.get(), count * 2, d.L, galois, s);
-    key_switch_impl(cx, rot.get() + LN, 2 * LN, galois, count, rot.get(), nullptr, 2 * LN, out, out + LN, 2 * LN, s);
+    // the automorphism is folded into the key switch's loads; an in-place
+    // call needs a private copy of the input (outputs scatter by permutation)
+    DeviceBuffer copy;
+    if (out == a) {
+        copy = DeviceBuffer(uint64_t(count) * 2 * LN * 8, s);
+        LB_CUDA(cudaMemcpyAsync(copy.get(), a, uint64_t(count) * 2 * LN * 8, cudaMemcpyDeviceToDevice, s));
+        a = copy.get();
+    }
+    key_switch_impl(cx, a + LN, 2 * LN, galois, galois, count, a, nullptr, 2 * LN, galois, out, out + LN, 2 * LN, s);
 }
 
 void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
@@ -892,8 +890,8 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{E.get(), count * 3, L, 0, LN}, s);
     // (i) relinearize e2 and add into (e0, e1)
-    key_switch_impl(cx, E.get() + 2 * LN, 3 * LN, kRelinKeyId, count, E.get(), E.get() + LN, 3 * LN, out, out + LN,
-                    2 * LN, s);
+    key_switch_impl(cx, E.get() + 2 * LN, 3 * LN, 0, kRelinKeyId, count, E.get(), E.get() + LN, 3 * LN, 0, out,
+                    out + LN, 2 * LN, s);
 }
 
 }  // namespace lb

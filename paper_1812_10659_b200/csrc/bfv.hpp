@@ -51,11 +51,13 @@ struct BfvDev {
     const uint64_t* phat_mod_q;  // [K][L]
     const uint64_t* p_inv_q;     // [L]
     const uint64_t* p_mod_qp;    // [L+K] [P]_r (key generation)
+    const ulonglong2* p_inv_shoup;  // [L] (P^-1 mod q_r, Shoup companion)
 };
 
 // Opaque device handle of a key-switching key.
 struct KsKey {
-    DeviceBuffer buf;  // [dnum][2][L+K][n]
+    DeviceBuffer buf;    // [dnum][2][L+K][n]
+    DeviceBuffer shoup;  // same entries as (value, Shoup companion) pairs
 };
 
 struct BfvState {

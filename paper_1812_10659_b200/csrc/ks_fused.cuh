@@ -1,0 +1,171 @@
+// Fused hybrid key switching on top of the cluster NTT core.
+//
+//   ks_inner_kernel  one cluster per (ciphertext, target prime r of Q∪P):
+//                    for every digit j: ModUp of the digit to r computed on
+//                    the fly in the transform's first pass (digit
+//                    decomposition), forward NTT in distributed smem, then the
+//                    key inner product accumulated in smem — the extended
+//                    digits never touch HBM. Digits whose own primes contain r
+//                    skip the transform and read the input's evaluations.
+//   moddown_kernel   one cluster per (ciphertext, component, q_r): the P->q_r
+//                    conversion in the first pass, forward NTT, then
+//                    (acc - conv) * P^-1 (+ the other ciphertext component,
+//                    through the automorphism for rotations) in the epilogue.
+#pragma once
+
+#include "bfv_kernels.cuh"
+#include "ntt.cuh"
+
+namespace lb {
+
+struct KsInnerArgs {
+    const uint64_t* dc;      // [count][L][n] coefficients of the input
+    const uint64_t* dn;      // input evaluations, poly stride d_stride
+    uint64_t d_stride;
+    uint64_t d_galois;       // automorphism applied to dn reads (0 = none)
+    const ulonglong2* key;   // [dnum][2][L+K][n] (value, Shoup companion)
+    uint64_t* acc;           // [count][2][L+K][n] evaluations
+    uint32_t count;
+};
+
+// a + b for a, b in [0, 2q) -> [0, 2q)
+__device__ __forceinline__ uint64_t add_lazy2(uint64_t a, uint64_t b, uint64_t two_q) {
+    const uint64_t s = a + b;
+    return s >= two_q ? s - two_q : s;
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d, KsInnerArgs a) {
+    using S = NttShape<LOGN>;
+    extern __shared__ __align__(16) uint64_t smem[];
+    uint64_t* sm = smem;
+    uint64_t* acc0 = smem + S::M;
+    uint64_t* acc1 = smem + 2 * S::M;
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t id = blockIdx.x / S::CL;
+    const uint32_t c = id / LK, r = id % LK;
+    const PrimeDev& P = d.primes[r];
+    const uint64_t q = P.q, two_q = 2 * q;
+    const uint32_t cta_base = rank * S::M;
+    const uint64_t n = 1ull << LOGN;
+#pragma unroll
+    for (int jj = 0; jj < kE; ++jj) {
+        const uint32_t y = threadIdx.x + jj * S::T;
+        acc0[y] = 0;
+        acc1[y] = 0;
+    }
+    auto mac = [&](uint32_t y, uint32_t x, uint64_t v, uint32_t j) {
+        const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
+        const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
+        const ulonglong2 w0 = __ldg(&k0[x]), w1 = __ldg(&k1[x]);
+        acc0[y] = add_lazy2(acc0[y], mul_shoup_lazy(v, w0.x, w0.y, q), two_q);
+        acc1[y] = add_lazy2(acc1[y], mul_shoup_lazy(v, w1.x, w1.y, q), two_q);
+    };
+    for (uint32_t j = 0; j < d.dnum; ++j) {
+        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+        if (r >= lo && r < hi) {
+            // the digit already lives in this prime: use the input's evaluations
+            const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+#pragma unroll 4
+            for (int jj = 0; jj < kE; ++jj) {
+                const uint32_t y = threadIdx.x + jj * S::T;
+                const uint32_t x = cta_base + y;
+                mac(y, x, __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]), j);
+            }
+            continue;
+        }
+        const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
+        if (hi - lo == 1) {
+            // single-prime digit: the coefficient (< q_lo < 4 q_r) feeds the
+            // lazy transform unreduced
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
+        } else {
+            const Modulus rm = modulus_of(P);
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+                Acc128 s;
+                for (uint32_t i = lo; i < hi; ++i) {
+                    const Modulus qm = modulus_of(d.primes[i]);
+                    const uint64_t yi = mul_mod(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), d.dhat_inv[i], qm);
+                    s.mac(yi, d.dhat_mod[i * LK + r]);
+                }
+                return reduce_acc(s, rm);
+            });
+        }
+#pragma unroll 4
+        for (int jj = 0; jj < kE; ++jj) {
+            const uint32_t y = threadIdx.x + jj * S::T;
+            mac(y, cta_base + y, reduce_4q(sm[swz(y)], q, two_q), j);
+        }
+    }
+    uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
+    uint64_t* out1 = out0 + uint64_t(LK) * n;
+#pragma unroll
+    for (int jj = 0; jj < kE; ++jj) {
+        const uint32_t y = threadIdx.x + jj * S::T;
+        const uint64_t v0 = acc0[y], v1 = acc1[y];
+        out0[y] = v0 >= q ? v0 - q : v0;
+        out1[y] = v1 >= q ? v1 - q : v1;
+    }
+    // no trailing cluster barrier: the last remote access to this CTA's smem
+    // (a scatter) is ordered before the cluster sync inside fwd_core
+}
+
+struct ModDownArgs {
+    const uint64_t* acc;      // [count][2][L+K][n]: Q limbs evaluations, P limbs coefficients
+    const uint64_t* add0;     // optional, poly stride add_stride
+    const uint64_t* add1;
+    uint64_t add_stride;
+    uint64_t add_galois;      // automorphism applied to add reads (0 = none)
+    uint64_t* out0;
+    uint64_t* out1;
+    uint64_t out_stride;
+    const ulonglong2* p_inv;  // [L] (P^-1 mod q_r, Shoup)
+    uint32_t count;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(BfvDev d, ModDownArgs a) {
+    using S = NttShape<LOGN>;
+    __shared__ __align__(16) uint64_t sm[S::M];
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t id = blockIdx.x / S::CL;
+    const uint32_t r = id % d.L, h = (id / d.L) & 1, c = id / (2 * d.L);
+    const PrimeDev& P = d.primes[r];
+    const uint64_t q = P.q, two_q = 2 * q;
+    const uint64_t n = 1ull << LOGN;
+    const uint64_t* accp = a.acc + ((uint64_t(c) * 2 + h) * LK + d.L) * n;
+    if (d.K == 1) {
+        // [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&accp[x]); });
+    } else {
+        const Modulus rm = modulus_of(P);
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+            Acc128 s;
+            for (uint32_t l = 0; l < d.K; ++l) {
+                const Modulus pm = modulus_of(d.primes[d.pbase + l]);
+                const uint64_t yl = mul_mod(__ldg(&accp[(uint64_t(l) << LOGN) + x]), d.phat_inv[l], pm);
+                s.mac(yl, d.phat_mod_q[l * d.L + r]);
+            }
+            return reduce_acc(s, rm);
+        });
+    }
+    const uint32_t cta_base = rank * S::M;
+    const uint64_t* accq = a.acc + ((uint64_t(c) * 2 + h) * LK + r) * n;
+    const uint64_t* add = h ? a.add1 : a.add0;
+    if (add) add += c * a.add_stride + (uint64_t(r) << LOGN);
+    uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
+    const ulonglong2 pinv = a.p_inv[r];
+#pragma unroll 4
+    for (int jj = 0; jj < kE; ++jj) {
+        const uint32_t y = threadIdx.x + jj * S::T;
+        const uint32_t x = cta_base + y;
+        const uint64_t conv = reduce_4q(sm[swz(y)], q, two_q);
+        uint64_t u = mul_shoup(__ldg(&accq[x]) + q - conv, pinv.x, pinv.y, q);
+        if (add) u = add_mod(u, __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]), q);
+        out[x] = u;
+    }
+}
+
+}  // namespace lb

@@ -58,7 +58,21 @@ struct LimbBatch {
     uint64_t poly_stride;  // elements between consecutive polys (>= limbs*N)
     const int16_t* prime_map = nullptr;
     uint32_t map_period = 0;
+    // inverse transform only: read the input from `src` (same [poly][limb]
+    // shape, poly stride src_stride) instead of in place, optionally through
+    // the automorphism x -> x^galois on the evaluations (galois 0 = none).
+    const uint64_t* src = nullptr;
+    uint64_t src_stride = 0;
+    uint64_t galois = 0;
 };
+
+// Evaluation-domain source position of x under x -> x^g (bit-reversed order).
+__device__ __forceinline__ uint32_t galois_src(uint32_t x, uint64_t g, int logn) {
+    const uint32_t n = 1u << logn;
+    const uint32_t k = __brev(x) >> (32 - logn);
+    const uint64_t e = (g * (2ull * k + 1)) & (2ull * n - 1);
+    return __brev(static_cast<uint32_t>((e - 1) >> 1)) >> (32 - logn);
+}
 
 constexpr int kLogE = 4;               // 16 coefficients per thread
 constexpr int kE = 1 << kLogE;
@@ -170,33 +184,33 @@ __device__ __forceinline__ uint64_t* limb_ptr(const LimbBatch& b, uint32_t limb_
     return b.data + (uint64_t)poly * b.poly_stride + ((uint64_t)l << logn);
 }
 
-// grid.x = CL * (polys * limbs); cluster dims (CL, 1, 1).
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
+
+// Forward transform core, shared by the plain and the fused kernels. The
+// cluster's CTAs cooperatively transform one limb: `load(x)` supplies input
+// coefficient x (any value < 4q, so loaders may skip their final reduction),
+// and on return the CTA's chunk [rank*M, (rank+1)*M) of the bit-reversed
+// evaluations sits in `sm` (swizzled, values in [0, 4q)).
+// Callers looping over several transforms must cluster-sync between them
+// (peers scatter into this CTA's smem).
+template <int LOGN, class Load>
+__device__ __forceinline__ void fwd_core(uint64_t* sm, const PrimeDev& P, uint32_t rank, Load&& load) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
-    __shared__ __align__(16) uint64_t sm[S::M];
-    const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
-    const uint32_t limb_id = blockIdx.x / S::CL;
-    const int pidx = prime_index(b, limb_id);
-    if (pidx < 0) return;  // whole cluster skips together
-    const PrimeDev& P = primes[pidx];
     const uint64_t q = P.q, two_q = 2 * q;
-    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
     const ulonglong2* __restrict__ tw = P.fwd;
-
-    // Every CTA of the cluster must be running before peers write into its
-    // shared memory: arrive now, wait just before the remote stores.
-    if constexpr (S::CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-    // Cross-CTA pass: stages 0..3 on group rho, straight from HBM.
+    // Every CTA of the cluster must be running (and done reading its smem)
+    // before peers write into it: arrive now, wait before the remote stores.
+    if constexpr (S::CL > 1) cluster_arrive();
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
         uint64_t r[kE];
 #pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = __ldcs(&a[rho + k * S::NE]);
+        for (int k = 0; k < kE; ++k) r[k] = load(rho + k * S::NE);
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
-        if constexpr (S::CL > 1) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
-        // output k lives in block k (size N/16) owned by CTA k / PER_CTA
+        if constexpr (S::CL > 1) cluster_wait();
+        else __syncthreads();
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
             const uint32_t dst = k / S::PER_CTA;
@@ -213,9 +227,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_ker
         cg::this_cluster().sync();
     else
         __syncthreads();
-
     const uint32_t cta_base = rank * S::M;
-    // Local passes: stages 4.. LOGN-1 in chunks of 4.
 #pragma unroll
     for (int s0 = kLogE; s0 < LOGN; s0 += kLogE) {
         if (s0 + kLogE <= LOGN) {
@@ -229,8 +241,28 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_ker
         }
         __syncthreads();
     }
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    namespace cg = cooperative_groups;
+    return cg::this_cluster().block_rank();
+}
+
+// grid.x = CL * (polys * limbs); cluster dims (CL, 1, 1).
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+    using S = NttShape<LOGN>;
+    __shared__ __align__(16) uint64_t sm[S::M];
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t limb_id = blockIdx.x / S::CL;
+    const int pidx = prime_index(b, limb_id);
+    if (pidx < 0) return;  // whole cluster skips together
+    const PrimeDev& P = primes[pidx];
+    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
+    fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldcs(&a[x]); });
     // Coalesced store of the CTA's chunk, fully reduced.
-    uint64_t* out = a + cta_base;
+    const uint64_t q = P.q, two_q = 2 * q;
+    uint64_t* out = a + rank * S::M;
 #pragma unroll
     for (int j = 0; j < kE; ++j) {
         const uint32_t y = threadIdx.x + j * S::T;
@@ -253,7 +285,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
     const ulonglong2* __restrict__ tw = P.inv;
     const uint32_t cta_base = rank * S::M;
 
-    {
+    if (b.src) {
+        const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
+        const uint64_t* in = b.src + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
+#pragma unroll
+        for (int j = 0; j < kE; ++j) {
+            const uint32_t y = threadIdx.x + j * S::T;
+            const uint32_t x = cta_base + y;
+            sm[swz(y)] = __ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]);
+        }
+    } else {
         const uint64_t* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
