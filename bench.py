@@ -56,21 +56,15 @@ def dist_setup(n_gpus: int):
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
+    from paper_1812_10659_b200.shard import barrier as _b
 
-        dist.barrier()
+    _b(world)
 
 
 def max_over_ranks(world, value: float) -> float:
-    if world == 1:
-        return value
-    import torch
-    import torch.distributed as dist
+    from paper_1812_10659_b200.shard import max_over_ranks as _m
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _m(value, world, device="cuda")
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -265,7 +259,9 @@ def run_ours(a, world, rank, local):
     B = a.batch
     sess = Session(cx, net, "lola-mnist", B)
     # images of this rank: a disjoint contiguous range of the 4096-image set
-    imgs = nets.images(2, net, B, start=rank * B)
+    from paper_1812_10659_b200.shard import shard_range
+
+    imgs = nets.images(2, net, B, start=shard_range(world * B, world, rank).start)
     dev_imgs = torch.from_numpy(imgs).cuda()
     counters, _, _ = plan_counters(net, "lola-mnist", prm.n)
     rot_per_image = int(counters[:, 5:7].sum()) * len(prm.t)
