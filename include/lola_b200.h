@@ -134,6 +134,42 @@ int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* 
 uint64_t lb_galois_exponent_columns(uint32_t n, uint32_t k);
 uint64_t lb_galois_exponent_rows(uint32_t n);
 
+/* ---- Evaluator boundary (proj/include/packnn/evaluator.hpp:50-91) ---------
+ * The drop-in for the reference's Evaluator on a new BackendKind: every
+ * method of Evaluator has one entry point with the same meaning, counting
+ * rules (evaluator.cpp:137-332) and budget errors (status 4 for depth_error /
+ * magnitude_error, 3 for std::invalid_argument). A message handle is one
+ * BATCH of `batch` independent messages (one per image); lifted values are
+ * shared by every message unless per_message is set ([batch][count]).
+ * Every returned message must be released with lb_message_free. */
+typedef struct lb_evaluator lb_evaluator;
+typedef struct lb_message lb_message;
+
+int lb_eval_create(lb_context* cx, uint32_t batch, uint32_t max_depth, void* stream, lb_evaluator** out);
+int lb_eval_destroy(lb_evaluator* ev);
+int lb_eval_fork(const lb_evaluator* ev, lb_evaluator** out);              /* Evaluator::fork */
+int lb_eval_absorb(lb_evaluator* ev, const lb_evaluator* child);          /* Evaluator::absorb */
+/* out[8]: ct.ct, ct.pt, scalar, mask, add, rot.col, rot.row, live peak (OpCounters) */
+int lb_eval_counters(const lb_evaluator* ev, uint64_t* out);
+int lb_eval_note_live(lb_evaluator* ev, uint64_t live);
+int lb_eval_lift(lb_evaluator* ev, const int64_t* values, uint64_t count, int per_message, lb_message** out);
+/* Evaluator::lower: out [batch][n][4] signed 256-bit words (host memory) */
+int lb_eval_lower(lb_evaluator* ev, const lb_message* m, uint64_t* out);
+int lb_eval_add(lb_evaluator* ev, const lb_message* a, const lb_message* b, lb_message** out);
+int lb_eval_add_plain(lb_evaluator* ev, const lb_message* a, const int64_t* values, uint64_t count, lb_message** out);
+int lb_eval_mul(lb_evaluator* ev, const lb_message* a, const lb_message* b, lb_message** out);
+int lb_eval_mul_plain(lb_evaluator* ev, const lb_message* a, const int64_t* values, uint64_t count, lb_message** out);
+int lb_eval_mask(lb_evaluator* ev, const lb_message* a, const uint8_t* bits, uint64_t count, lb_message** out);
+int lb_eval_mul_scalar(lb_evaluator* ev, const lb_message* a, int64_t s, lb_message** out);
+int lb_eval_rotate_columns(lb_evaluator* ev, const lb_message* a, int64_t k, lb_message** out);
+int lb_eval_rotate_rows(lb_evaluator* ev, const lb_message* a, lb_message** out);
+int lb_eval_rotate_bundle(lb_evaluator* ev, const lb_message* a, uint32_t amount, lb_message** out);
+int lb_message_free(lb_message* m);
+/* depth, plain depth, magnitude bound (decimal) of a message */
+int lb_message_info(const lb_message* m, uint32_t* depth, uint32_t* plain_depth, char* magnitude, uint64_t cap);
+/* device pointer of the message's ciphertexts [batch][T][2][L][n] */
+int lb_message_data(const lb_message* m, const uint64_t** out);
+
 /* ---- LoLa layer evaluator (proj/src/representation.cpp, kernels.cpp, plan.cpp) --
  * A network is the already-quantized integer network the reference's
  * QuantizedNetwork holds (proj/include/packnn/layers.hpp:100-123): linear
