@@ -223,6 +223,9 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
 int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int images_on_device);
 int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters);
 int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device);
+/* device pointer of encrypted output message `index` ([batch][T][2][L][n])
+ * and the number of output messages (either pointer may be NULL) */
+int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const uint64_t** data, uint32_t* count);
 
 /* ---- measurement ------------------------------------------------------- */
 

@@ -256,6 +256,15 @@ __global__ void k_mul_scalar(BfvDev d, const uint64_t* __restrict__ a, ScalarTab
     out[idx] = mul_shoup(a[idx], s.v[i].x, s.v[i].y, d.primes[i].q);
 }
 
+__global__ void k_mul_scalar_add(BfvDev d, const uint64_t* __restrict__ acc, const uint64_t* __restrict__ x,
+                                 ScalarTab s, uint64_t* __restrict__ out, uint64_t total) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint32_t i = (idx / d.n) % d.L;
+    const uint64_t q = d.primes[i].q;
+    out[idx] = add_mod(acc[idx], mul_shoup(x[idx], s.v[i].x, s.v[i].y, q), q);
+}
+
 // out[c][comp][i] = a[c][comp][i] * pt[c mod T][i]
 __global__ void k_mul_plain(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ pt,
                             uint64_t* __restrict__ out, uint64_t total) {
@@ -702,7 +711,8 @@ void dispatch_ks(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDown
 //   4. fused P->Q conversion + NTT + ModDown epilogue     (moddown_kernel)
 void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint64_t d_galois, uint64_t key_id,
                      uint32_t count, const uint64_t* add0, const uint64_t* add1, uint64_t add_stride,
-                     uint64_t add_galois, uint64_t* out0, uint64_t* out1, uint64_t out_stride, cudaStream_t s) {
+                     uint64_t add_galois, uint64_t* out0, uint64_t* out1, uint64_t out_stride, cudaStream_t s,
+                     const uint64_t* sum0 = nullptr, const uint64_t* sum1 = nullptr, uint64_t sum_stride = 0) {
     if (!count) return;
     BfvState& st = *cx.bfv();
     const BfvDev& d = st.dev;
@@ -722,7 +732,8 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     KsInnerArgs ka{dc.get(), d_ntt, d_stride, d_galois, key, acc.get(), count};
     dispatch_ks(cx.logn(), d, ka, nullptr, s);
     cx.ntt_inverse(LimbBatch{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n}, s);
-    ModDownArgs ma{acc.get(), add0, add1, add_stride, add_galois, out0, out1, out_stride, d.p_inv_shoup, count};
+    ModDownArgs ma{acc.get(), add0,  add1,  add_stride, add_galois, sum0,        sum1,
+                   sum_stride, out0, out1,  out_stride, d.p_inv_shoup, count};
     dispatch_ks(cx.logn(), d, ka, &ma, s);
 }
 
@@ -806,18 +817,31 @@ void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     LB_KERNEL_DONE();
 }
 
-void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
-    const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
+static ScalarTab scalar_table(Context& cx, int64_t scalar) {
     ScalarTab tab{};
-    for (uint32_t i = 0; i < d.L; ++i) {
+    for (uint32_t i = 0; i < cx.L(); ++i) {
         const uint64_t q = cx.prime(i);
         int64_t r = scalar % static_cast<int64_t>(q);
         const uint64_t v = r < 0 ? static_cast<uint64_t>(r + static_cast<int64_t>(q)) : static_cast<uint64_t>(r);
         tab.v[i] = make_ulonglong2(v, shoup_companion(v, q));
     }
-    k_mul_scalar<<<grid_for(total), kBlock, 0, s>>>(d, a, tab, out, total);
+    return tab;
+}
+
+void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    k_mul_scalar<<<grid_for(total), kBlock, 0, s>>>(d, a, scalar_table(cx, scalar), out, total);
+    LB_KERNEL_DONE();
+}
+
+void ct_mul_scalar_add(Context& cx, const uint64_t* acc, const uint64_t* x, int64_t scalar, uint64_t* out,
+                       uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
+    if (!total) return;
+    k_mul_scalar_add<<<grid_for(total), kBlock, 0, s>>>(d, acc, x, scalar_table(cx, scalar), out, total);
     LB_KERNEL_DONE();
 }
 
@@ -851,6 +875,25 @@ void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, u
         a = copy.get();
     }
     key_switch_impl(cx, a + LN, 2 * LN, galois, galois, count, a, nullptr, 2 * LN, galois, out, out + LN, 2 * LN, s);
+}
+
+void ct_rotate_add(Context& cx, const uint64_t* base, const uint64_t* x, uint64_t galois, uint64_t* out,
+                   uint32_t count, cudaStream_t s) {
+    const BfvDev& d = cx.bfv()->dev;
+    if (!count) return;
+    if (galois % 2 == 0 || galois >= 2ull * d.n) throw std::invalid_argument("galois element must be odd in [1, 2n)");
+    const uint64_t LN = uint64_t(d.L) * d.n;
+    DeviceBuffer copy;
+    if (out == x || out == base) {  // outputs are written while inputs are gathered
+        copy = DeviceBuffer(uint64_t(count) * 4 * LN * 8, s);
+        LB_CUDA(cudaMemcpyAsync(copy.get(), x, uint64_t(count) * 2 * LN * 8, cudaMemcpyDeviceToDevice, s));
+        LB_CUDA(cudaMemcpyAsync(copy.get() + uint64_t(count) * 2 * LN, base, uint64_t(count) * 2 * LN * 8,
+                                cudaMemcpyDeviceToDevice, s));
+        x = copy.get();
+        base = copy.get() + uint64_t(count) * 2 * LN;
+    }
+    key_switch_impl(cx, x + LN, 2 * LN, galois, galois, count, x, nullptr, 2 * LN, galois, out, out + LN, 2 * LN, s,
+                    base, base + LN, 2 * LN);
 }
 
 void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {

@@ -100,6 +100,13 @@ void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt_mul, uint64
 void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt_add, uint64_t* out, uint32_t count,
                   cudaStream_t s);
 void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s);
+// fused forms used by the evaluator (one counted rotation / scalar product
+// plus one counted addition, one pass over memory):
+//   out = base + rotate_g(x)          out = acc + scalar * x
+void ct_rotate_add(Context& cx, const uint64_t* base, const uint64_t* x, uint64_t galois, uint64_t* out,
+                   uint32_t count, cudaStream_t s);
+void ct_mul_scalar_add(Context& cx, const uint64_t* acc, const uint64_t* x, int64_t scalar, uint64_t* out,
+                       uint32_t count, cudaStream_t s);
 void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s);
 
 // key material

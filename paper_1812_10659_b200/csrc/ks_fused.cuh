@@ -117,6 +117,9 @@ struct ModDownArgs {
     const uint64_t* add1;
     uint64_t add_stride;
     uint64_t add_galois;      // automorphism applied to add reads (0 = none)
+    const uint64_t* sum0;     // optional second addend (no automorphism), poly stride sum_stride
+    const uint64_t* sum1;
+    uint64_t sum_stride;
     uint64_t* out0;
     uint64_t* out1;
     uint64_t out_stride;
@@ -155,6 +158,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
     const uint64_t* accq = a.acc + ((uint64_t(c) * 2 + h) * LK + r) * n;
     const uint64_t* add = h ? a.add1 : a.add0;
     if (add) add += c * a.add_stride + (uint64_t(r) << LOGN);
+    const uint64_t* sum = h ? a.sum1 : a.sum0;
+    if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const ulonglong2 pinv = a.p_inv[r];
 #pragma unroll 4
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
         const uint64_t conv = reduce_4q(sm[swz(y)], q, two_q);
         uint64_t u = mul_shoup(__ldg(&accq[x]) + q - conv, pinv.x, pinv.y, q);
         if (add) u = add_mod(u, __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]), q);
+        if (sum) u = add_mod(u, __ldg(&sum[x]), q);
         out[x] = u;
     }
 }

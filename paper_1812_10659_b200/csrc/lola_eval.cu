@@ -427,21 +427,32 @@ Message Evaluator::mul_scalar(const Message& a, int64_t sc) {  // evaluator.cpp:
 }
 
 // Right shift of both slot rows (evaluator.cpp:260-287): one automorphism
-// x -> x^(3^(half - shift)) plus a key switch.
-Message Evaluator::shift_columns(const Message& a, uint32_t right_by) {
+// x -> x^(3^(half - shift)) plus a key switch; with `base`, the sum
+// base + shifted (the caller counts both operations).
+Message Evaluator::shift_columns(const Message& a, uint32_t right_by, const Message* base) {
     const uint32_t half = cx_->half();
     const uint32_t shift = right_by % half;
-    Message r = fresh(a.depth, a.plain_depth, a.magnitude);
     const uint64_t two_n = 2ull * cx_->n();
-    uint64_t g = 1, base = 3;
+    uint64_t g = 1, b3 = 3;
     for (uint64_t e = (half - shift) % half; e; e >>= 1) {
-        if (e & 1) g = g * base % two_n;
-        base = base * base % two_n;
+        if (e & 1) g = g * b3 % two_n;
+        b3 = b3 * b3 % two_n;
     }
+    const uint32_t cts = static_cast<uint32_t>(cx_->cts());
+    if (base) {
+        Message r = fresh(std::max(a.depth, base->depth), std::max(a.plain_depth, base->plain_depth),
+                          a.magnitude + base->magnitude);
+        if (g == 1)
+            ct_add(cx_->device(), base->data(), a.data(), r.data(), cts, cx_->stream());
+        else
+            ct_rotate_add(cx_->device(), base->data(), a.data(), g, r.data(), cts, cx_->stream());
+        return r;
+    }
+    Message r = fresh(a.depth, a.plain_depth, a.magnitude);
     if (g == 1) {
         LB_CUDA(cudaMemcpyAsync(r.data(), a.data(), cx_->payload_bytes(), cudaMemcpyDeviceToDevice, cx_->stream()));
     } else {
-        ct_rotate(cx_->device(), a.data(), g, r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+        ct_rotate(cx_->device(), a.data(), g, r.data(), cts, cx_->stream());
     }
     return r;
 }
@@ -469,6 +480,56 @@ Message Evaluator::rotate_bundle(const Message& a, uint32_t amount) {  // evalua
     if (amount == 0) return a;
     counters_.ops.rot_cols += 1;
     return shift_columns(a, amount);
+}
+
+// ---- fused forms ------------------------------------------------------------------
+
+Message Evaluator::mul_scalar_add(const Message& acc, const Message& x, int64_t sc) {
+    const uint64_t as = sc < 0 ? uint64_t(-(sc + 1)) + 1 : uint64_t(sc);
+    const Mag prod = x.magnitude * Mag(as);
+    check_magnitude(prod, "mul_scalar");
+    counters_.ops.scalar_mul += 1;
+    const Mag mag = acc.magnitude + prod;
+    check_magnitude(mag, "add");
+    counters_.ops.add += 1;
+    Message r = fresh(std::max(acc.depth, x.depth), std::max(acc.plain_depth, x.plain_depth + 1), mag);
+    ct_mul_scalar_add(cx_->device(), acc.data(), x.data(), sc, r.data(), static_cast<uint32_t>(cx_->cts()),
+                      cx_->stream());
+    return r;
+}
+
+Message Evaluator::rotate_columns_add(const Message& base, const Message& x, int64_t k) {
+    const int64_t half = cx_->half();
+    if (k <= -half || k >= half) throw std::invalid_argument("rotate_columns: |k| must be below n/2");
+    if (k == 0) return add(base, x);
+    const uint64_t amount = static_cast<uint64_t>(k < 0 ? -k : k);
+    counters_.ops.rot_cols += static_cast<uint64_t>(__builtin_popcountll(amount));
+    const Mag mag = base.magnitude + x.magnitude;
+    check_magnitude(mag, "add");
+    counters_.ops.add += 1;
+    const uint32_t right_by = k > 0 ? static_cast<uint32_t>(k) : static_cast<uint32_t>(half + k);
+    return shift_columns(x, right_by, &base);
+}
+
+Message Evaluator::rotate_bundle_add(const Message& base, const Message& x, uint32_t amount) {
+    if (amount >= cx_->half()) throw std::invalid_argument("rotate_bundle: amount must be below n/2");
+    if (amount == 0) return add(base, x);
+    counters_.ops.rot_cols += 1;
+    const Mag mag = base.magnitude + x.magnitude;
+    check_magnitude(mag, "add");
+    counters_.ops.add += 1;
+    return shift_columns(x, amount, &base);
+}
+
+Message Evaluator::rotate_rows_add(const Message& base, const Message& x) {
+    counters_.ops.rot_rows += 1;
+    const Mag mag = base.magnitude + x.magnitude;
+    check_magnitude(mag, "add");
+    counters_.ops.add += 1;
+    Message r = fresh(std::max(x.depth, base.depth), std::max(x.plain_depth, base.plain_depth), mag);
+    ct_rotate_add(cx_->device(), base.data(), x.data(), 2ull * cx_->n() - 1, r.data(),
+                  static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    return r;
 }
 
 }  // namespace lb::lola

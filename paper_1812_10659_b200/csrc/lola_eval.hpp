@@ -157,6 +157,17 @@ public:
     Message rotate_rows(const Message& a);
     Message rotate_bundle(const Message& a, uint32_t amount);
 
+    // Fused forms: exactly the counters, budgets and results of the two-op
+    // sequences they replace, one kernel pass instead of two.
+    //   mul_scalar_add(acc, x, s)       == add(acc, mul_scalar(x, s))
+    //   rotate_columns_add(b, x, k)     == add(b, rotate_columns(x, k))
+    //   rotate_rows_add(b, x)           == add(b, rotate_rows(x))
+    //   rotate_bundle_add(b, x, amount) == add(b, rotate_bundle(x, amount))
+    Message mul_scalar_add(const Message& acc, const Message& x, int64_t s);
+    Message rotate_columns_add(const Message& base, const Message& x, int64_t k);
+    Message rotate_rows_add(const Message& base, const Message& x);
+    Message rotate_bundle_add(const Message& base, const Message& x, uint32_t amount);
+
     void note_live(uint64_t live) { counters_.note_live(live); }
     Evaluator fork() const;
     void absorb(const Evaluator& child);
@@ -170,7 +181,7 @@ private:
     Message fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const;
     void check_magnitude(const Mag& m, const char* op) const;
     const uint64_t* plain(const std::vector<int64_t>& values, bool for_add);
-    Message shift_columns(const Message& a, uint32_t right_by);
+    Message shift_columns(const Message& a, uint32_t right_by, const Message* base = nullptr);
 };
 
 }  // namespace lb::lola

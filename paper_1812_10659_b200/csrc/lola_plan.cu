@@ -166,10 +166,8 @@ EncodedTensor stack_copies(Evaluator& ev, const EncodedTensor& t, uint32_t copie
     out.rep.pad = pad;
     out.rep.copies = copies;
     Message m = t.messages[0];
-    for (uint64_t shift = pad; shift < pad * copies; shift <<= 1) {
-        Message moved = shift == half ? ev.rotate_rows(m) : ev.rotate_bundle(m, static_cast<uint32_t>(shift));
-        m = ev.add(m, moved);
-    }
+    for (uint64_t shift = pad; shift < pad * copies; shift <<= 1)  // m = add(m, rotated m), fused
+        m = shift == half ? ev.rotate_rows_add(m, m) : ev.rotate_bundle_add(m, m, static_cast<uint32_t>(shift));
     out.messages.push_back(std::move(m));
     return out;
 }
@@ -196,11 +194,9 @@ EncodedTensor combine_to_one(Evaluator& ev, const EncodedTensor& parts, const st
             const uint64_t idx = p * per_part + j;
             if (idx < total) slot_of[idx] = s;
         }
-    auto moved = [&](size_t p) {
-        return offsets[p] ? ev.rotate_bundle(parts.messages[p], offsets[p]) : parts.messages[p];
-    };
-    Message acc = moved(0);
-    for (size_t p = 1; p < parts.messages.size(); ++p) acc = ev.add(acc, moved(p));
+    Message acc = offsets[0] ? ev.rotate_bundle(parts.messages[0], offsets[0]) : parts.messages[0];
+    for (size_t p = 1; p < parts.messages.size(); ++p)  // acc = add(acc, rotated part), fused
+        acc = ev.rotate_bundle_add(acc, parts.messages[p], offsets[p]);
     EncodedTensor out;
     out.rep.kind = RepKind::Interleaved;
     out.rep.length = total;
@@ -431,11 +427,9 @@ CounterDelta sparse_to_dense_cost(uint64_t v) {
 // rotate-and-sum ladder of sizes 1, 2, ..., span/2 (kernels.cpp:26-36)
 Message reduce_rotate_add(Evaluator& ev, Message m, uint64_t span, bool toward_low) {
     const uint32_t half = ev.context().half();
-    for (uint64_t size = 1; size < span; size <<= 1) {
-        Message moved = size == half ? ev.rotate_rows(m)
-                                     : ev.rotate_columns(m, toward_low ? -int64_t(size) : int64_t(size));
-        m = ev.add(m, moved);
-    }
+    for (uint64_t size = 1; size < span; size <<= 1)  // m = add(m, rotated m), fused
+        m = size == half ? ev.rotate_rows_add(m, m)
+                         : ev.rotate_columns_add(m, m, toward_low ? -int64_t(size) : int64_t(size));
     return m;
 }
 
@@ -521,7 +515,8 @@ EncodedTensor conv_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weights
     }
     for (uint64_t map = 0; map < W.rows; ++map) {
         Message acc = ev.mul_scalar(x.messages[0], W.at(map, 0));
-        for (uint64_t j = 1; j < W.cols; ++j) acc = ev.add(acc, ev.mul_scalar(x.messages[j], W.at(map, j)));
+        for (uint64_t j = 1; j < W.cols; ++j)  // acc = add(acc, mul_scalar(x_j, w)), fused
+            acc = ev.mul_scalar_add(acc, x.messages[j], W.at(map, j));
         out.messages.push_back(std::move(acc));
     }
     return out;

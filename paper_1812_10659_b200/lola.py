@@ -41,6 +41,7 @@ _SIGS = {
     "lb_lola_session_encrypt": [vp, vp, C.c_int],
     "lb_lola_session_execute": [vp, C.POINTER(C.c_uint64)],
     "lb_lola_session_decrypt": [vp, vp, C.c_int],
+    "lb_lola_session_output": [vp, C.c_uint32, C.POINTER(vp), C.POINTER(C.c_uint32)],
 }
 nat.register(_SIGS)
 
@@ -146,6 +147,17 @@ class Session:
         scores = np.zeros((self.batch, self.outputs, 4), dtype=np.uint64)
         nat.call("lb_lola_session_decrypt", self.handle, scores.ctypes.data, 0)
         return [[words_to_int(scores[b, i]) for i in range(self.outputs)] for b in range(self.batch)]
+
+    def output_ciphertexts(self, index: int):
+        """Copy of encrypted output message `index`: torch [batch][T][2][L][n]."""
+        import torch
+
+        from .bfv import _DevPtr
+
+        p, cnt = vp(), C.c_uint32()
+        nat.call("lb_lola_session_output", self.handle, index, C.byref(p), C.byref(cnt))
+        shape = (self.batch, len(self.cx.params.t), 2, len(self.cx.params.q), self.cx.n)
+        return torch.as_tensor(_DevPtr(p.value, shape), device="cuda").clone()
 
     def run(self, images: np.ndarray):
         """Host images [batch][input_values] -> (scores [batch][outputs] Python
