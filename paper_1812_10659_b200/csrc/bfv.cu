@@ -534,6 +534,25 @@ void bfv_setup(Context& cx) {
     std::vector<uint64_t> p_mod_qp(LK);
     for (uint32_t r = 0; r < LK; ++r) p_mod_qp[r] = prod_mod(p, 0, K, SIZE_MAX, qp[r]);
     const size_t o_pmqp = put(p_mod_qp.data(), LK * 8);
+    auto pair = [](uint64_t v, uint64_t m) { return make_ulonglong2(v, shoup_companion(v, m)); };
+    std::vector<ulonglong2> dhat_mod_sh(size_t(L) * LK), phat_mod_sh(std::max(K, 1u) * size_t(L));
+    std::vector<ulonglong2> ks_last_q(2 * size_t(L)), ks_last_p(2 * size_t(std::max(K, 1u)));
+    for (uint32_t i = 0; i < L; ++i) {
+        for (uint32_t r = 0; r < LK; ++r) dhat_mod_sh[size_t(i) * LK + r] = pair(dhat_mod[size_t(i) * LK + r], qp[r]);
+        const PrimeDev& hp = cx.host_prime(i);
+        ks_last_q[2 * i] = pair(mulm(hp.ninv, dhat_inv[i], q[i]), q[i]);
+        ks_last_q[2 * i + 1] = pair(mulm(hp.inv1n, dhat_inv[i], q[i]), q[i]);
+    }
+    for (uint32_t l = 0; l < K; ++l) {
+        for (uint32_t r = 0; r < L; ++r) phat_mod_sh[size_t(l) * L + r] = pair(phat_mod_q[size_t(l) * L + r], q[r]);
+        const PrimeDev& hp = cx.host_prime(L + l);
+        ks_last_p[2 * l] = pair(mulm(hp.ninv, phat_inv[l], p[l]), p[l]);
+        ks_last_p[2 * l + 1] = pair(mulm(hp.inv1n, phat_inv[l], p[l]), p[l]);
+    }
+    const size_t o_dhsh = put(dhat_mod_sh.data(), dhat_mod_sh.size() * 16);
+    const size_t o_phsh = put(phat_mod_sh.data(), phat_mod_sh.size() * 16);
+    const size_t o_klq = put(ks_last_q.data(), ks_last_q.size() * 16);
+    const size_t o_klp = put(ks_last_p.data(), ks_last_p.size() * 16);
 
     std::vector<int16_t> t_map(std::max(T, 1u)), qb_map(L + M), ks_map(size_t(dnum) * LK);
     for (uint32_t j = 0; j < T; ++j) t_map[j] = int16_t(L + K + M + j);
@@ -573,6 +592,10 @@ void bfv_setup(Context& cx) {
     d.p_inv_q = reinterpret_cast<const uint64_t*>(base + o_piq);
     d.p_mod_qp = reinterpret_cast<const uint64_t*>(base + o_pmqp);
     d.p_inv_shoup = reinterpret_cast<const ulonglong2*>(base + o_pish);
+    d.dhat_mod_sh = reinterpret_cast<const ulonglong2*>(base + o_dhsh);
+    d.phat_mod_sh = reinterpret_cast<const ulonglong2*>(base + o_phsh);
+    d.ks_last_q = reinterpret_cast<const ulonglong2*>(base + o_klq);
+    d.ks_last_p = reinterpret_cast<const ulonglong2*>(base + o_klp);
     st->t_map = reinterpret_cast<const int16_t*>(base + o_tmap);
     st->qb_map = reinterpret_cast<const int16_t*>(base + o_qbmap);
     st->ks_map = reinterpret_cast<const int16_t*>(base + o_ksmap);
@@ -722,16 +745,23 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
     DeviceBuffer dc(uint64_t(count) * L * n * 8, s);
     {
+        // coefficients of d, pre-multiplied by [(D_j/q_i)^-1]_{q_i} for
+        // multi-prime digits (folded into the transform's n^-1)
         LimbBatch lb{dc.get(), count, L, 0, uint64_t(L) * n};
         lb.src = d_ntt;
         lb.src_stride = d_stride;
         lb.galois = d_galois;
+        if (d.alpha > 1) lb.last_stage = d.ks_last_q;
         cx.ntt_inverse(lb, s);
     }
     DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
     KsInnerArgs ka{dc.get(), d_ntt, d_stride, d_galois, key, acc.get(), count};
     dispatch_ks(cx.logn(), d, ka, nullptr, s);
-    cx.ntt_inverse(LimbBatch{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n}, s);
+    {
+        LimbBatch pb{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n};
+        if (K > 1) pb.last_stage = d.ks_last_p;  // times [(P/p_l)^-1]_{p_l}
+        cx.ntt_inverse(pb, s);
+    }
     ModDownArgs ma{acc.get(), add0,  add1,  add_stride, add_galois, sum0,        sum1,
                    sum_stride, out0, out1,  out_stride, d.p_inv_shoup, count};
     dispatch_ks(cx.logn(), d, ka, &ma, s);

@@ -52,6 +52,14 @@ struct BfvDev {
     const uint64_t* p_inv_q;     // [L]
     const uint64_t* p_mod_qp;    // [L+K] [P]_r (key generation)
     const ulonglong2* p_inv_shoup;  // [L] (P^-1 mod q_r, Shoup companion)
+    // fused key switch (Shoup pairs): ModUp constants [D_j/q_i]_r per
+    // (i, r in Q∪P), ModDown constants [P/p_l]_{q_r} per (l, r in Q), and the
+    // inverse-transform final-stage constants that fold [(D_j/q_i)^-1]_{q_i}
+    // (per q limb) and [(P/p_l)^-1]_{p_l} (per p limb) into n^-1
+    const ulonglong2* dhat_mod_sh;   // [L][L+K]
+    const ulonglong2* phat_mod_sh;   // [K][L]
+    const ulonglong2* ks_last_q;     // [L][2]
+    const ulonglong2* ks_last_p;     // [K][2]
 };
 
 // Opaque device handle of a key-switching key.

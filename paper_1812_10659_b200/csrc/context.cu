@@ -88,6 +88,7 @@ Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
     }
     LB_CUDA(cudaMemcpyAsync(d_tab, tables.data(), tables.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice,
                             stream_));
+    host_primes_ = devs;
     d_primes_ = DeviceBuffer(devs.size() * sizeof(PrimeDev), stream_);
     LB_CUDA(cudaMemcpyAsync(d_primes_.get(), devs.data(), devs.size() * sizeof(PrimeDev), cudaMemcpyHostToDevice,
                             stream_));

@@ -109,6 +109,7 @@ public:
     uint64_t psi(uint32_t i) const { return psi_.at(i); }
     const Params& params() const { return prm_; }
     const PrimeDev* dev_primes() const { return d_primes_.get<PrimeDev>(); }
+    const PrimeDev& host_prime(uint32_t i) const { return host_primes_.at(i); }  // constants only
     const Modulus& modulus(uint32_t i) const { return mods_.at(i); }
     cudaStream_t stream() const { return stream_; }
 
@@ -127,6 +128,7 @@ private:
     std::vector<uint64_t> all_;
     std::vector<uint64_t> psi_;
     std::vector<Modulus> mods_;
+    std::vector<PrimeDev> host_primes_;
     cudaStream_t stream_ = nullptr;
     DeviceBuffer d_tables_;
     DeviceBuffer d_primes_;

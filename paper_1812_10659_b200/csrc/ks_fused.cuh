@@ -55,24 +55,39 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
         acc0[y] = 0;
         acc1[y] = 0;
     }
-    auto mac = [&](uint32_t y, uint32_t x, uint64_t v, uint32_t j) {
+    // acc_h[y] += v_jj * key_j[h][r][x] for the thread's 16 final-pass
+    // elements; key loads (L2-resident, shared by every ciphertext of the
+    // batch) are issued a half at a time ahead of their use.
+    auto mac_all = [&](uint32_t j, auto&& value_of) {
         const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
         const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
-        const ulonglong2 w0 = __ldg(&k0[x]), w1 = __ldg(&k1[x]);
-        acc0[y] = add_lazy2(acc0[y], mul_shoup_lazy(v, w0.x, w0.y, q), two_q);
-        acc1[y] = add_lazy2(acc1[y], mul_shoup_lazy(v, w1.x, w1.y, q), two_q);
+        constexpr int kHalf = kE / 2;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            ulonglong2 w0[kHalf], w1[kHalf];
+#pragma unroll
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint32_t x = cta_base + threadIdx.x + (part * kHalf + jj) * S::T;
+                w0[jj] = __ldg(&k0[x]);
+                w1[jj] = __ldg(&k1[x]);
+            }
+#pragma unroll
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
+                const uint64_t v = value_of(y, cta_base + y);
+                acc0[y] = add_lazy2(acc0[y], mul_shoup_lazy(v, w0[jj].x, w0[jj].y, q), two_q);
+                acc1[y] = add_lazy2(acc1[y], mul_shoup_lazy(v, w1[jj].x, w1[jj].y, q), two_q);
+            }
+        }
     };
     for (uint32_t j = 0; j < d.dnum; ++j) {
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         if (r >= lo && r < hi) {
             // the digit already lives in this prime: use the input's evaluations
             const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
-#pragma unroll 4
-            for (int jj = 0; jj < kE; ++jj) {
-                const uint32_t y = threadIdx.x + jj * S::T;
-                const uint32_t x = cta_base + y;
-                mac(y, x, __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]), j);
-            }
+            mac_all(j, [&](uint32_t, uint32_t x) {
+                return __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
+            });
             continue;
         }
         const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
@@ -81,22 +96,18 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
             // lazy transform unreduced
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
         } else {
-            const Modulus rm = modulus_of(P);
+            // src limbs already hold y_i = [d_i (D_j/q_i)^-1]_{q_i}; fast base
+            // conversion sum_i y_i [D_j/q_i]_r, kept lazily in [0, 2r)
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-                Acc128 s;
+                uint64_t v = 0;
                 for (uint32_t i = lo; i < hi; ++i) {
-                    const Modulus qm = modulus_of(d.primes[i]);
-                    const uint64_t yi = mul_mod(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), d.dhat_inv[i], qm);
-                    s.mac(yi, d.dhat_mod[i * LK + r]);
+                    const ulonglong2 w = d.dhat_mod_sh[i * LK + r];
+                    v = add_lazy2(v, mul_shoup_lazy(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), w.x, w.y, q), two_q);
                 }
-                return reduce_acc(s, rm);
+                return v;
             });
         }
-#pragma unroll 4
-        for (int jj = 0; jj < kE; ++jj) {
-            const uint32_t y = threadIdx.x + jj * S::T;
-            mac(y, cta_base + y, reduce_4q(sm[swz(y)], q, two_q), j);
-        }
+        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q(sm[swz(y)], q, two_q); });
     }
     uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     uint64_t* out1 = out0 + uint64_t(LK) * n;
@@ -143,15 +154,15 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
         // [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&accp[x]); });
     } else {
-        const Modulus rm = modulus_of(P);
+        // P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded into the
+        // inverse transform); sum_l y_l [P/p_l]_{q_r}, lazily in [0, 2q)
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-            Acc128 s;
+            uint64_t v = 0;
             for (uint32_t l = 0; l < d.K; ++l) {
-                const Modulus pm = modulus_of(d.primes[d.pbase + l]);
-                const uint64_t yl = mul_mod(__ldg(&accp[(uint64_t(l) << LOGN) + x]), d.phat_inv[l], pm);
-                s.mac(yl, d.phat_mod_q[l * d.L + r]);
+                const ulonglong2 w = d.phat_mod_sh[l * d.L + r];
+                v = add_lazy2(v, mul_shoup_lazy(__ldg(&accp[(uint64_t(l) << LOGN) + x]), w.x, w.y, q), two_q);
             }
-            return reduce_acc(s, rm);
+            return v;
         });
     }
     const uint32_t cta_base = rank * S::M;
@@ -162,15 +173,29 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const ulonglong2 pinv = a.p_inv[r];
-#pragma unroll 4
-    for (int jj = 0; jj < kE; ++jj) {
-        const uint32_t y = threadIdx.x + jj * S::T;
-        const uint32_t x = cta_base + y;
-        const uint64_t conv = reduce_4q(sm[swz(y)], q, two_q);
-        uint64_t u = mul_shoup(__ldg(&accq[x]) + q - conv, pinv.x, pinv.y, q);
-        if (add) u = add_mod(u, __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]), q);
-        if (sum) u = add_mod(u, __ldg(&sum[x]), q);
-        out[x] = u;
+    // Epilogue in two halves: issue every global load of a half (including
+    // the automorphism gather, which hits scattered sectors) before using
+    // any of them, so their latencies overlap.
+    constexpr int kHalf = kE / 2;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+        uint64_t va[kHalf], vb[kHalf], vs[kHalf];
+#pragma unroll
+        for (int jj = 0; jj < kHalf; ++jj) {
+            const uint32_t x = cta_base + threadIdx.x + (part * kHalf + jj) * S::T;
+            va[jj] = __ldg(&accq[x]);
+            vb[jj] = add ? __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]) : 0;
+            vs[jj] = sum ? __ldg(&sum[x]) : 0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kHalf; ++jj) {
+            const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
+            const uint64_t conv = reduce_4q(sm[swz(y)], q, two_q);
+            uint64_t u = mul_shoup(va[jj] + q - conv, pinv.x, pinv.y, q);
+            u = add_mod(u, vb[jj], q);
+            u = add_mod(u, vs[jj], q);
+            out[cta_base + y] = u;
+        }
     }
 }
 

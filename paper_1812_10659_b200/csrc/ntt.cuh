@@ -64,6 +64,10 @@ struct LimbBatch {
     const uint64_t* src = nullptr;
     uint64_t src_stride = 0;
     uint64_t galois = 0;
+    // inverse transform only: per limb position l (< limbs), the final-stage
+    // constants {n^-1 * s_l, psi^-bitrev(1) * n^-1 * s_l} as (value, Shoup)
+    // pairs, which scale the output by s_l for free (NULL = s_l = 1).
+    const ulonglong2* last_stage = nullptr;
 };
 
 // Evaluation-domain source position of x under x -> x^g (bit-reversed order).
@@ -349,13 +353,19 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
             }
         }
         constexpr int half0 = kE / 2;
+        ulonglong2 c0 = make_ulonglong2(P.ninv, P.ninv_shoup), c1 = make_ulonglong2(P.inv1n, P.inv1n_shoup);
+        if (b.last_stage) {
+            const uint32_t l = limb_id % b.limbs;
+            c0 = b.last_stage[2 * l];
+            c1 = b.last_stage[2 * l + 1];
+        }
 #pragma unroll
         for (int k = 0; k < half0; ++k) {
             uint64_t x = r[k], y = r[k + half0];
             uint64_t s = x + y;  // < 4q
             uint64_t d = x - y + two_q;
-            r[k] = mul_shoup(s, P.ninv, P.ninv_shoup, q);
-            r[k + half0] = mul_shoup(d, P.inv1n, P.inv1n_shoup, q);
+            r[k] = mul_shoup(s, c0.x, c0.y, q);
+            r[k + half0] = mul_shoup(d, c1.x, c1.y, q);
         }
 #pragma unroll
         for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], r[k]);

@@ -15,10 +15,11 @@ from paper_1812_10659_b200.params import make_params
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[(4096, 3, 2), (8192, 4, 1)], ids=["n4096_L3_T2", "n8192_L4_T1"])
+@pytest.fixture(scope="module", params=[(4096, 3, 2, 1, 0), (8192, 4, 1, 1, 0), (4096, 5, 2, 2, 3)],
+                ids=["n4096_L3_T2", "n8192_L4_T1", "n4096_L5_K2_dnum3"])
 def env(request):
-    n, L, T = request.param
-    prm = make_params(n, L=L, T=T, K=1, seed=11)
+    n, L, T, K, dnum = request.param
+    prm = make_params(n, L=L, T=T, K=K, dnum=dnum, seed=11)
     cx = BfvContext(prm)
     o = Oracle.from_params(prm)
     return prm, cx, o
