@@ -236,59 +236,97 @@ __global__ void k_gather_slots(BfvDev d, const uint64_t* __restrict__ ev, uint32
 }
 
 // ---- elementwise (ct ops) ----
-__global__ void k_add(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
-                      uint64_t total) {
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const uint32_t i = (idx / d.n) % d.L;
-    out[idx] = add_mod(a[idx], b[idx], d.primes[i].q);
+// 2D grid: blockIdx.y walks the rows (poly-limb pairs, row = (c*2 + comp)*L
+// + i, so the prime is fixed per block), blockIdx.x * blockDim.x * 2 + ... the
+// coefficients, two per thread through 16-byte accesses. Rows beyond the
+// grid's y extent are covered by the row loop.
+constexpr int kEwThreads = 256;
+
+struct EwShape {
+    uint32_t rows;
+    uint32_t L;
+    uint32_t T;
+    uint32_t logn;
+};
+
+template <class F>
+__device__ __forceinline__ void ew_rows(const EwShape& sh, F&& f) {
+    const uint32_t n = 1u << sh.logn;
+    const uint32_t k = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
+    if (k >= n) return;
+    for (uint32_t row = blockIdx.y; row < sh.rows; row += gridDim.y) {
+        const uint32_t i = row % sh.L;
+        const uint32_t comp = (row / sh.L) & 1;
+        const uint32_t c = row / (2 * sh.L);
+        f(uint64_t(row) << sh.logn | k, i, comp, c, k);
+    }
+}
+
+inline dim3 ew_grid(const EwShape& sh) {
+    const uint32_t n = 1u << sh.logn;
+    return dim3((n / 2 + kEwThreads - 1) / kEwThreads, std::min<uint32_t>(sh.rows, 65535u));
+}
+
+__global__ void __launch_bounds__(kEwThreads) k_add(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
+                                                    const uint64_t* __restrict__ b, uint64_t* __restrict__ out) {
+    ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
+        const uint64_t q = d.primes[i].q;
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b + off);
+        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
+    });
 }
 
 struct ScalarTab {
     ulonglong2 v[32];  // per ciphertext prime: (s mod q_i, Shoup companion)
 };
 
-__global__ void k_mul_scalar(BfvDev d, const uint64_t* __restrict__ a, ScalarTab s, uint64_t* __restrict__ out,
-                             uint64_t total) {
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const uint32_t i = (idx / d.n) % d.L;
-    out[idx] = mul_shoup(a[idx], s.v[i].x, s.v[i].y, d.primes[i].q);
+__global__ void __launch_bounds__(kEwThreads) k_mul_scalar(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
+                                                           ScalarTab s, uint64_t* __restrict__ out) {
+    ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
+        const uint64_t q = d.primes[i].q;
+        const ulonglong2 w = s.v[i];
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
+        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(mul_shoup(x.x, w.x, w.y, q), mul_shoup(x.y, w.x, w.y, q));
+    });
 }
 
-__global__ void k_mul_scalar_add(BfvDev d, const uint64_t* __restrict__ acc, const uint64_t* __restrict__ x,
-                                 ScalarTab s, uint64_t* __restrict__ out, uint64_t total) {
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const uint32_t i = (idx / d.n) % d.L;
-    const uint64_t q = d.primes[i].q;
-    out[idx] = add_mod(acc[idx], mul_shoup(x[idx], s.v[i].x, s.v[i].y, q), q);
+__global__ void __launch_bounds__(kEwThreads) k_mul_scalar_add(BfvDev d, EwShape sh, const uint64_t* __restrict__ acc,
+                                                               const uint64_t* __restrict__ x, ScalarTab s,
+                                                               uint64_t* __restrict__ out) {
+    ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
+        const uint64_t q = d.primes[i].q;
+        const ulonglong2 w = s.v[i];
+        const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(acc + off);
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(x + off);
+        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(add_mod(u.x, mul_shoup(v.x, w.x, w.y, q), q),
+                                                                    add_mod(u.y, mul_shoup(v.y, w.x, w.y, q), q));
+    });
 }
 
 // out[c][comp][i] = a[c][comp][i] * pt[c mod T][i]
-__global__ void k_mul_plain(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ pt,
-                            uint64_t* __restrict__ out, uint64_t total) {
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const uint32_t pos = idx % d.n;
-    const uint32_t i = (idx / d.n) % d.L;
-    const uint64_t c = idx / (uint64_t(d.n) * d.L * 2);
-    const uint32_t j = c % d.T;
-    const Modulus qm = modulus_of(d.primes[i]);
-    out[idx] = mul_mod(a[idx], pt[(uint64_t(j) * d.L + i) * d.n + pos], qm);
+__global__ void __launch_bounds__(kEwThreads) k_mul_plain(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
+                                                          const uint64_t* __restrict__ pt, uint64_t* __restrict__ out) {
+    ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t c, uint32_t k) {
+        const Modulus qm = modulus_of(d.primes[i]);
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k));
+        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(mul_mod(x.x, w.x, qm), mul_mod(x.y, w.y, qm));
+    });
 }
 
-__global__ void k_add_plain(BfvDev d, const uint64_t* __restrict__ a, const uint64_t* __restrict__ pt,
-                            uint64_t* __restrict__ out, uint64_t total) {
-    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const uint32_t pos = idx % d.n;
-    const uint32_t i = (idx / d.n) % d.L;
-    const uint32_t comp = (idx / (uint64_t(d.n) * d.L)) & 1;
-    const uint64_t c = idx / (uint64_t(d.n) * d.L * 2);
-    const uint32_t j = c % d.T;
-    const uint64_t v = a[idx];
-    out[idx] = comp ? v : add_mod(v, pt[(uint64_t(j) * d.L + i) * d.n + pos], d.primes[i].q);
+__global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
+                                                          const uint64_t* __restrict__ pt, uint64_t* __restrict__ out) {
+    ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t comp, uint32_t c, uint32_t k) {
+        const uint64_t q = d.primes[i].q;
+        ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
+        if (!comp) {
+            const ulonglong2 w =
+                __ldg(reinterpret_cast<const ulonglong2*>(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k));
+            x = make_ulonglong2(add_mod(x.x, w.x, q), add_mod(x.y, w.y, q));
+        }
+        *reinterpret_cast<ulonglong2*>(out + off) = x;
+    });
 }
 
 // ---- multiplication (§3.6) ----
@@ -839,11 +877,13 @@ void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t
     if (pt_add) cx.ntt_forward(LimbBatch{pt_add, T, L, 0, uint64_t(L) * n}, s);
 }
 
+static EwShape ew_shape(const BfvDev& d, uint32_t count) { return EwShape{count * 2 * d.L, d.L, d.T, d.logn}; }
+
 void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
-    k_add<<<grid_for(total), kBlock, 0, s>>>(d, a, b, out, total);
+    if (!count) return;
+    const EwShape sh = ew_shape(d, count);
+    k_add<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, b, out);
     LB_KERNEL_DONE();
 }
 
@@ -860,34 +900,34 @@ static ScalarTab scalar_table(Context& cx, int64_t scalar) {
 
 void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
-    k_mul_scalar<<<grid_for(total), kBlock, 0, s>>>(d, a, scalar_table(cx, scalar), out, total);
+    if (!count) return;
+    const EwShape sh = ew_shape(d, count);
+    k_mul_scalar<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, scalar_table(cx, scalar), out);
     LB_KERNEL_DONE();
 }
 
 void ct_mul_scalar_add(Context& cx, const uint64_t* acc, const uint64_t* x, int64_t scalar, uint64_t* out,
                        uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
-    k_mul_scalar_add<<<grid_for(total), kBlock, 0, s>>>(d, acc, x, scalar_table(cx, scalar), out, total);
+    if (!count) return;
+    const EwShape sh = ew_shape(d, count);
+    k_mul_scalar_add<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, acc, x, scalar_table(cx, scalar), out);
     LB_KERNEL_DONE();
 }
 
 void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
-    k_mul_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
+    if (!count) return;
+    const EwShape sh = ew_shape(d, count);
+    k_mul_plain<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, pt, out);
     LB_KERNEL_DONE();
 }
 
 void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
-    const uint64_t total = uint64_t(count) * 2 * d.L * d.n;
-    if (!total) return;
-    k_add_plain<<<grid_for(total), kBlock, 0, s>>>(d, a, pt, out, total);
+    if (!count) return;
+    const EwShape sh = ew_shape(d, count);
+    k_add_plain<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, pt, out);
     LB_KERNEL_DONE();
 }
 
