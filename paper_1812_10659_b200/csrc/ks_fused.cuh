@@ -122,6 +122,156 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
     // (a scatter) is ordered before the cluster sync inside fwd_core
 }
 
+
+// ---- TMEM-accumulator variant ------------------------------------------------------
+// Same algorithm as ks_inner_kernel; the two accumulators of every element
+// live in Tensor Memory instead of shared memory (128 TMEM columns per CTA:
+// warp w owns lanes 32*(w%4).. of column block w/4, each thread 16 elements x
+// 2 components x 2 words). Shared memory then holds only the 32 KiB
+// transform chunk, so three CTAs fit per SM (registers allowing) instead of
+// two.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(addr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+        ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+constexpr int kTmemCols = 128;
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(BfvDev d, KsInnerArgs a) {
+    using S = NttShape<LOGN>;
+    static_assert(S::T == 256, "TMEM layout assumes 8 warps");
+    __shared__ __align__(16) uint64_t sm[S::M];
+    __shared__ uint32_t tmem_base_sh;
+    const uint32_t warp = threadIdx.x / 32;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = tmem_base_sh + ((32u * (warp & 3u)) << 16) + (warp >> 2) * 64u;
+
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t id = blockIdx.x / S::CL;
+    const uint32_t c = id / LK, r = id % LK;
+    const PrimeDev& P = d.primes[r];
+    const uint64_t q = P.q, two_q = 2 * q;
+    const uint32_t cta_base = rank * S::M;
+    const uint64_t n = 1ull << LOGN;
+
+    // acc_h[e] += v_e * key_j[h][r][x_e] for the thread's 16 elements, two
+    // at a time: columns [4e, 4e+4) of the thread's block = (acc0, acc1) words
+    auto mac_all = [&](uint32_t j, bool first, auto&& value_of) {
+        const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
+        const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
+#pragma unroll 2
+        for (int pair = 0; pair < 8; ++pair) {
+            ulonglong2 w0[2], w1[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t x = cta_base + threadIdx.x + (pair * 2 + e) * S::T;
+                w0[e] = __ldg(&k0[x]);
+                w1[e] = __ldg(&k1[x]);
+            }
+            uint32_t acc[8];
+            if (!first) tmem_ld8(tbase + pair * 8, acc);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t y = threadIdx.x + (pair * 2 + e) * S::T;
+                const uint64_t v = value_of(y, cta_base + y);
+                uint64_t t0 = mul_shoup_lazy(v, w0[e].x, w0[e].y, q);
+                uint64_t t1 = mul_shoup_lazy(v, w1[e].x, w1[e].y, q);
+                if (!first) {
+                    t0 = add_lazy2((uint64_t(acc[4 * e + 1]) << 32) | acc[4 * e], t0, two_q);
+                    t1 = add_lazy2((uint64_t(acc[4 * e + 3]) << 32) | acc[4 * e + 2], t1, two_q);
+                }
+                acc[4 * e] = static_cast<uint32_t>(t0);
+                acc[4 * e + 1] = static_cast<uint32_t>(t0 >> 32);
+                acc[4 * e + 2] = static_cast<uint32_t>(t1);
+                acc[4 * e + 3] = static_cast<uint32_t>(t1 >> 32);
+            }
+            tmem_st8(tbase + pair * 8, acc);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    };
+    for (uint32_t j = 0; j < d.dnum; ++j) {
+        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+        const bool first = j == 0;
+        if (r >= lo && r < hi) {
+            const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+            mac_all(j, first, [&](uint32_t, uint32_t x) {
+                return __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
+            });
+            continue;
+        }
+        const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
+        if (hi - lo == 1) {
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
+        } else {
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+                uint64_t v = 0;
+                for (uint32_t i = lo; i < hi; ++i) {
+                    const ulonglong2 w = d.dhat_mod_sh[i * LK + r];
+                    v = add_lazy2(v, mul_shoup_lazy(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), w.x, w.y, q), two_q);
+                }
+                return v;
+            });
+        }
+        mac_all(j, first, [&](uint32_t y, uint32_t) { return reduce_4q(sm[swz(y)], q, two_q); });
+    }
+    uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
+    uint64_t* out1 = out0 + uint64_t(LK) * n;
+#pragma unroll
+    for (int quarter = 0; quarter < 4; ++quarter) {
+        uint32_t acc[16];
+        tmem_ld16(tbase + quarter * 16, acc);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t y = threadIdx.x + (quarter * 4 + e) * S::T;
+            const uint64_t v0 = (uint64_t(acc[4 * e + 1]) << 32) | acc[4 * e];
+            const uint64_t v1 = (uint64_t(acc[4 * e + 3]) << 32) | acc[4 * e + 2];
+            out0[y] = v0 >= q ? v0 - q : v0;
+            out1[y] = v1 >= q ? v1 - q : v1;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base_sh), "n"(kTmemCols));
+}
+
 struct ModDownArgs {
     const uint64_t* acc;      // [count][2][L+K][n]: Q limbs evaluations, P limbs coefficients
     const uint64_t* add0;     // optional, poly stride add_stride

@@ -137,3 +137,29 @@ def test_mul_matches_oracle_and_reference(env):
         assert np.array_equal(got_s[tj], o.mul(tj, A[tj], A[tj]))
         want = R.poly_mul(t, plain_m(prm, tj, vals[0]), plain_m(prm, tj, vals2[0]))
         assert np.array_equal(mp[0, tj], want)
+
+
+def test_tmem_accumulator_variant_matches_oracle():
+    """The TMEM-accumulator key-switch kernel (LB_KS_TMEM=1) is bit-exact too."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, '.');"
+        "import numpy as np, torch;"
+        "from oracle.bfvbind import Oracle;"
+        "from paper_1812_10659_b200.bfv import BfvContext, galois_exponent_columns;"
+        "from paper_1812_10659_b200.params import make_params;"
+        "prm = make_params(16384, L=5, T=1, K=1, seed=4); cx = BfvContext(prm); o = Oracle.from_params(prm);"
+        "v = torch.arange(prm.n, dtype=torch.int64, device='cuda').reshape(1, -1) - 77;"
+        "ct = cx.encrypt_slots(v, id_base=9); g = galois_exponent_columns(prm.n, 5);"
+        "c = lambda t: (lambda x: (cx.ntt_inverse(x, limbs=prm.L), torch.cuda.synchronize(), x.cpu().numpy().astype(np.uint64))[2])(t.reshape(-1, 2, prm.L, prm.n).clone());"
+        "assert np.array_equal(c(cx.rotate(ct, g))[0], o.rotate(c(ct)[0], g));"
+        "print('ok')"
+    )
+    import os
+
+    env = dict(os.environ, LB_KS_TMEM="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
