@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
     auto mac_all = [&](uint32_t j, auto&& value_of) {
         const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
         const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
-        constexpr int kHalf = kE / 2;
+        constexpr int kHalf = 8;  // elements whose key loads are in flight together
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {
+        for (int part = 0; part < kE / kHalf; ++part) {
             ulonglong2 w0[kHalf], w1[kHalf];
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
@@ -169,7 +169,10 @@ constexpr int kTmemCols = 128;
 template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(BfvDev d, KsInnerArgs a) {
     using S = NttShape<LOGN>;
-    static_assert(S::T == 256, "TMEM layout assumes 8 warps");
+    static_assert(S::T == 256 || S::T == 128, "TMEM layout assumes 4 or 8 warps");
+    // 4 columns (acc0, acc1 as 32-bit word pairs) per element; warps beyond
+    // the four lane quadrants take the next column block
+    constexpr uint32_t kColsPerThread = 4 * kE;
     __shared__ __align__(16) uint64_t sm[S::M];
     __shared__ uint32_t tmem_base_sh;
     const uint32_t warp = threadIdx.x / 32;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(Bfv
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tbase = tmem_base_sh + ((32u * (warp & 3u)) << 16) + (warp >> 2) * 64u;
+    const uint32_t tbase = tmem_base_sh + ((32u * (warp & 3u)) << 16) + (warp >> 2) * kColsPerThread;
 
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(Bfv
         const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
         const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
 #pragma unroll 2
-        for (int pair = 0; pair < 8; ++pair) {
+        for (int pair = 0; pair < kE / 2; ++pair) {
             ulonglong2 w0[2], w1[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(Bfv
     uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     uint64_t* out1 = out0 + uint64_t(LK) * n;
 #pragma unroll
-    for (int quarter = 0; quarter < 4; ++quarter) {
+    for (int quarter = 0; quarter < kE / 4; ++quarter) {
         uint32_t acc[16];
         tmem_ld16(tbase + quarter * 16, acc);
 #pragma unroll
@@ -326,9 +329,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
     // any of them, so their latencies overlap.
-    constexpr int kHalf = kE / 2;
+    constexpr int kHalf = 8;
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
+    for (int part = 0; part < kE / kHalf; ++part) {
         uint64_t va[kHalf], vb[kHalf], vs[kHalf];
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {

@@ -78,11 +78,14 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t x, uint64_t g, int logn)
     return __brev(static_cast<uint32_t>((e - 1) >> 1)) >> (32 - logn);
 }
 
-constexpr int kLogE = 4;               // 16 coefficients per thread
+#ifndef LB_NTT_LOGE
+#define LB_NTT_LOGE 4  // radix 32 (LOGE 5, 128 threads) measured slower on B200: 481 vs 512 Gbfly/s
+#endif
+constexpr int kLogE = LB_NTT_LOGE;     // 2^kLogE coefficients per thread (radix of a register pass)
 constexpr int kE = 1 << kLogE;
 constexpr int kCtaCoeffs = 4096;       // coefficients owned by one CTA
-constexpr int kThreads = kCtaCoeffs / kE;  // 256
-constexpr int kMinBlocks = 3;             // resident CTAs per SM the register budget must allow
+constexpr int kThreads = kCtaCoeffs / kE;  // 128 (radix 32) or 256 (radix 16)
+constexpr int kMinBlocks = kThreads == 128 ? 4 : 3;  // resident CTAs per SM the register budget must allow
 
 __device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
 
@@ -167,6 +170,18 @@ __device__ __forceinline__ void local_pass(uint64_t* sm, const ulonglong2* __res
     }
 }
 
+// local pass of C stages, C chosen at run time among 1..kLogE
+template <int LOGN, bool INVERSE, int C = kLogE>
+__device__ __forceinline__ void local_pass_n(int c, uint64_t* sm, const ulonglong2* __restrict__ tw, uint32_t s0,
+                                             uint32_t cta_base, uint64_t q, uint64_t two_q) {
+    if constexpr (C >= 1) {
+        if (c == C)
+            local_pass<LOGN, C, INVERSE>(sm, tw, s0, cta_base, q, two_q);
+        else
+            local_pass_n<LOGN, INVERSE, C - 1>(c, sm, tw, s0, cta_base, q, two_q);
+    }
+}
+
 template <int LOGN>
 struct NttShape {
     static constexpr int N = 1 << LOGN;
@@ -234,15 +249,7 @@ __device__ __forceinline__ void fwd_core(uint64_t* sm, const PrimeDev& P, uint32
     const uint32_t cta_base = rank * S::M;
 #pragma unroll
     for (int s0 = kLogE; s0 < LOGN; s0 += kLogE) {
-        if (s0 + kLogE <= LOGN) {
-            local_pass<LOGN, kLogE, false>(sm, tw, s0, cta_base, q, two_q);
-        } else if (LOGN - s0 == 3) {
-            local_pass<LOGN, 3, false>(sm, tw, s0, cta_base, q, two_q);
-        } else if (LOGN - s0 == 2) {
-            local_pass<LOGN, 2, false>(sm, tw, s0, cta_base, q, two_q);
-        } else {
-            local_pass<LOGN, 1, false>(sm, tw, s0, cta_base, q, two_q);
-        }
+        local_pass_n<LOGN, false>(LOGN - s0 < kLogE ? LOGN - s0 : kLogE, sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
 }
@@ -309,14 +316,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
     __syncthreads();
     // Local passes in reverse: the last (possibly short) chunk first.
     constexpr int kTail = (LOGN - kLogE) % kLogE;
-    if constexpr (kTail == 3) {
-        local_pass<LOGN, 3, true>(sm, tw, LOGN - 3, cta_base, q, two_q);
-        __syncthreads();
-    } else if constexpr (kTail == 2) {
-        local_pass<LOGN, 2, true>(sm, tw, LOGN - 2, cta_base, q, two_q);
-        __syncthreads();
-    } else if constexpr (kTail == 1) {
-        local_pass<LOGN, 1, true>(sm, tw, LOGN - 1, cta_base, q, two_q);
+    if constexpr (kTail > 0) {
+        local_pass<LOGN, kTail, true>(sm, tw, LOGN - kTail, cta_base, q, two_q);
         __syncthreads();
     }
 #pragma unroll
