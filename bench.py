@@ -27,6 +27,24 @@ sys.path.insert(0, str(ROOT))
 METRIC = "LoLa-MNIST encrypted inferences/s & latency; NTT/s, rotations/s vs roofline"
 UNIT = "inferences/s"
 
+# workload -> (BASELINE config, strategy, default images per GPU per step)
+WORKLOADS = {
+    "lola-mnist": (2, "lola-mnist", 64),
+    "lola-small": (3, "lola-small", 256),
+    "lola-cifar": (4, "lola-cifar", 1),
+}
+
+
+def workload_objects(name: str):
+    from paper_1812_10659_b200 import nets, params
+
+    cfg, strategy, batch = WORKLOADS[name]
+    if name == "lola-mnist":
+        return cfg, strategy, batch, nets.lola_mnist_net(config=2), params.lola_mnist_params()
+    if name == "lola-small":
+        return cfg, strategy, batch, nets.lola_small_net(config=3), params.lola_small_params()
+    return cfg, strategy, batch, nets.lola_cifar_net(config=4), params.lola_cifar_params()
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -34,7 +52,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
+    ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (default per workload)")
+    ap.add_argument("--workload", default="lola-mnist", choices=list(WORKLOADS),
+                    help="lola-mnist = BASELINE config 2 (the headline); lola-small = config 3; lola-cifar = config 4")
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
     return ap.parse_args()
@@ -250,20 +270,17 @@ def run_ours(a, world, rank, local):
     from paper_1812_10659_b200 import nets
     from paper_1812_10659_b200.bfv import BfvContext
     from paper_1812_10659_b200.lola import Session, plan_counters
-    from paper_1812_10659_b200.params import lola_mnist_params
-
     torch.cuda.set_device(local)
-    prm = lola_mnist_params()
+    cfg, strategy, default_batch, net, prm = workload_objects(a.workload)
     cx = BfvContext(prm)
-    net = nets.lola_mnist_net(config=2)
-    B = a.batch
-    sess = Session(cx, net, "lola-mnist", B)
-    # images of this rank: a disjoint contiguous range of the 4096-image set
+    B = a.batch or default_batch
+    sess = Session(cx, net, strategy, B)
+    # images of this rank: a disjoint contiguous range of the job's image set
     from paper_1812_10659_b200.shard import shard_range
 
-    imgs = nets.images(2, net, B, start=shard_range(world * B, world, rank).start)
+    imgs = nets.images(cfg, net, B, start=shard_range(world * B, world, rank).start)
     dev_imgs = torch.from_numpy(imgs).cuda()
-    counters, _, _ = plan_counters(net, "lola-mnist", prm.n)
+    counters, _, _ = plan_counters(net, strategy, prm.n)
     rot_per_image = int(counters[:, 5:7].sum()) * len(prm.t)
     s = torch.cuda.current_stream()
 
@@ -309,7 +326,7 @@ def run_ours(a, world, rank, local):
         del sess
         torch.cuda.empty_cache()
         # single-image latency (server-side HE steps, and end to end)
-        one = Session(cx, net, "lola-mnist", 1)
+        one = Session(cx, net, strategy, 1)
         one_img = torch.from_numpy(imgs[:1].copy()).cuda()
         one.encrypt(one_img, on_device=True)
         for _ in range(3):
@@ -338,7 +355,7 @@ def run_ours(a, world, rank, local):
         try:
             from oracle import refbind as R
 
-            if R.available():
+            if R.available() and a.workload == "lola-mnist":
                 ips, wall = cpu_reference_throughput(a.cpu_sample, 1)
                 extras["cpu_baseline"] = {
                     "value": ips, "unit": UNIT, "cores": 1, "kind": "reference",
@@ -352,7 +369,7 @@ def run_ours(a, world, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": elapsed / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (SplitMix64-seeded pixels and weights)",
-            "config": {"workload": "lola-mnist cfg2 batched throughput", "images_per_gpu_per_step": B,
+            "config": {"workload": f"{strategy} cfg{cfg} batched throughput", "images_per_gpu_per_step": B,
                        "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
                        "q_bits": 60, "parallelism": f"images sharded over {world} GPU(s), no collective",
                        "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"},
@@ -361,7 +378,7 @@ def run_ours(a, world, rank, local):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "rotations_per_s": value * rot_per_image,
-            "key_switches_per_image": rot_per_image + 2 * len(prm.t),
+            "key_switches_per_image": rot_per_image + int(counters[:, 0].sum()) * len(prm.t),
         }
         line.update(extras)
         print(json.dumps(line))

@@ -688,6 +688,12 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     key.shoup = DeviceBuffer(key_elems * 16, s);
     k_shoup_pairs<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<ulonglong2>(), key_elems, LK);
     LB_KERNEL_DONE();
+    // keys are shared by every stream and outlive the (possibly side) stream
+    // they were generated on: complete them now, free them on the context's
+    // own stream later
+    LB_CUDA(cudaStreamSynchronize(s));
+    key.buf.rebind(cx.stream());
+    key.shoup.rebind(cx.stream());
     st.keys.emplace(key_id, std::move(key));
 }
 

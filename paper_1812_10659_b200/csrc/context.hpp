@@ -68,6 +68,9 @@ public:
     template <class T = uint64_t>
     T* get() const { return static_cast<T*>(ptr_); }
     size_t bytes() const { return bytes_; }
+    // Frees go to `s` from now on (the caller orders `s` after every use on
+    // the allocating stream, e.g. through an event).
+    void rebind(cudaStream_t s) { stream_ = s; }
 
 private:
     void release() {

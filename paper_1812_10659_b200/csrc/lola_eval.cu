@@ -1,6 +1,7 @@
 // Evaluator mirror on device ciphertexts; semantics follow
 // proj/src/evaluator.cpp line by line (cited per method).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "host_math.hpp"
@@ -199,6 +200,31 @@ uint64_t hash_values(const std::vector<int64_t>& v) {
 
 // ---- EvalContext ---------------------------------------------------------------------
 
+uint32_t EvalContext::fanout() const {
+    static const uint32_t n = [] {
+        const char* e = std::getenv("LB_STREAMS");
+        const int v = e ? std::atoi(e) : 8;
+        return static_cast<uint32_t>(std::max(1, std::min(v, 32)));
+    }();
+    return n;
+}
+
+cudaStream_t EvalContext::side_stream(uint32_t i) const {
+    while (side_.size() <= i) {
+        cudaStream_t s;
+        LB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        side_.push_back(s);
+    }
+    return side_[i];
+}
+
+EvalContext::~EvalContext() {
+    for (cudaStream_t s : side_) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+}
+
 EvalContext::EvalContext(Context& cx, uint32_t batch, uint32_t max_depth, cudaStream_t stream)
     : cx_(&cx), batch_(batch), max_depth_(max_depth), stream_(stream) {
     if (batch == 0) throw std::invalid_argument("batch must be positive");
@@ -211,10 +237,13 @@ EvalContext::EvalContext(Context& cx, uint32_t batch, uint32_t max_depth, cudaSt
 // ---- Evaluator -------------------------------------------------------------------------
 
 Evaluator::Evaluator(const EvalContext& cx)
-    : cx_(&cx), cache_(std::make_shared<PlainCache>()), next_id_(std::make_shared<uint64_t>(1)) {}
+    : cx_(&cx), stream_(cx.stream()), cache_(std::make_shared<PlainCache>()), next_id_(std::make_shared<uint64_t>(1)) {}
 
-Evaluator Evaluator::fork() const {
+Evaluator Evaluator::fork() const { return fork_on(stream_); }
+
+Evaluator Evaluator::fork_on(cudaStream_t s) const {
     Evaluator e(*cx_);
+    e.stream_ = s;
     e.cache_ = cache_;
     e.next_id_ = next_id_;
     return e;
@@ -228,7 +257,7 @@ void Evaluator::absorb(const Evaluator& child) {  // evaluator.cpp:334-337
 Message Evaluator::fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const {
     Message m;
     m.payload = std::make_shared<Payload>();
-    m.payload->buf = DeviceBuffer(cx_->payload_bytes(), cx_->stream());
+    m.payload->buf = DeviceBuffer(cx_->payload_bytes(), stream_);
     m.depth = depth;
     m.plain_depth = plain_depth;
     m.magnitude = mag;
@@ -260,7 +289,7 @@ Message Evaluator::lift_batch(const std::vector<std::vector<int64_t>>& values) c
         }
     }
     check_magnitude(mag, "lift");
-    cudaStream_t s = cx_->stream();
+    cudaStream_t s = stream_;
     DeviceBuffer dv(host.size() * 8, s);
     LB_CUDA(cudaMemcpyAsync(dv.get(), host.data(), host.size() * 8, cudaMemcpyHostToDevice, s));
     Message m = fresh(0, 0, mag);
@@ -279,7 +308,7 @@ Message Evaluator::lift_gather(const int64_t* dev_images, uint64_t stride, const
     std::copy(map.begin(), map.end(), full.begin());
     const Mag mag(static_cast<uint64_t>(max_abs < 0 ? -max_abs : max_abs));
     check_magnitude(mag, "lift");
-    cudaStream_t s = cx_->stream();
+    cudaStream_t s = stream_;
     DeviceBuffer dmap(uint64_t(n) * 4, s), slots(uint64_t(B) * n * 8, s);
     LB_CUDA(cudaMemcpyAsync(dmap.get(), full.data(), uint64_t(n) * 4, cudaMemcpyHostToDevice, s));
     k_gather_lift<<<blocks(uint64_t(B) * n), kBlock, 0, s>>>(dev_images, stride, dmap.get<int32_t>(), n, B,
@@ -295,7 +324,7 @@ Message Evaluator::lift_gather(const int64_t* dev_images, uint64_t stride, const
 DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t>& slots) const {
     Context& dc = cx_->device();
     const uint32_t n = cx_->n(), B = cx_->batch(), T = dc.T();
-    cudaStream_t s = cx_->stream();
+    cudaStream_t s = stream_;
     DeviceBuffer res(uint64_t(B) * T * n * 8, s);
     decrypt_slots(dc, m.data(), B, res.get(), s);
     CrtTab tab{};
@@ -337,10 +366,13 @@ const uint64_t* Evaluator::plain(const std::vector<int64_t>& values, bool for_ad
     const uint64_t h = hash_values(values);
     auto& bucket = table[h];
     for (auto& e : bucket)
-        if (e->values == values) return e->pt.get();
+        if (e->values == values) {
+            if (e->made_on != stream_) LB_CUDA(cudaStreamWaitEvent(stream_, e->ready, 0));
+            return e->pt.get();
+        }
     const uint32_t n = cx_->n();
     Context& dc = cx_->device();
-    cudaStream_t s = cx_->stream();
+    cudaStream_t s = stream_;
     std::vector<int64_t> full(n, 0);
     std::copy(values.begin(), values.end(), full.begin());
     DeviceBuffer dv(uint64_t(n) * 8, s);
@@ -349,7 +381,9 @@ const uint64_t* Evaluator::plain(const std::vector<int64_t>& values, bool for_ad
     e->values = values;
     e->pt = DeviceBuffer(uint64_t(dc.T()) * dc.L() * n * 8, s);
     encode_plain(dc, dv.get<int64_t>(), for_add ? nullptr : e->pt.get(), for_add ? e->pt.get() : nullptr, s);
-    LB_CUDA(cudaStreamSynchronize(s));  // `full` is pageable and local
+    e->made_on = s;
+    LB_CUDA(cudaEventCreateWithFlags(&e->ready, cudaEventDisableTiming));
+    LB_CUDA(cudaEventRecord(e->ready, s));
     const uint64_t* p = e->pt.get();
     bucket.push_back(std::move(e));
     return p;
@@ -360,7 +394,7 @@ Message Evaluator::add(const Message& a, const Message& b) {  // evaluator.cpp:1
     check_magnitude(mag, "add");
     counters_.ops.add += 1;
     Message r = fresh(std::max(a.depth, b.depth), std::max(a.plain_depth, b.plain_depth), mag);
-    ct_add(cx_->device(), a.data(), b.data(), r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    ct_add(cx_->device(), a.data(), b.data(), r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 
@@ -377,7 +411,7 @@ Message Evaluator::add_plain(const Message& a, const std::vector<int64_t>& value
     if (values.size() > cx_->n()) throw std::invalid_argument("plain operand: more values than slots");
     const uint64_t* pt = plain(values, true);
     Message r = fresh(a.depth, a.plain_depth, mag);
-    ct_add_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    ct_add_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 
@@ -389,7 +423,7 @@ Message Evaluator::mul(const Message& a, const Message& b) {  // evaluator.cpp:1
     check_magnitude(mag, "mul");
     counters_.ops.ct_ct_mul += 1;
     Message r = fresh(depth, std::max(a.plain_depth, b.plain_depth), mag);
-    ct_mul(cx_->device(), a.data(), b.data(), r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    ct_mul(cx_->device(), a.data(), b.data(), r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 
@@ -400,7 +434,7 @@ Message Evaluator::mul_plain(const Message& a, const std::vector<int64_t>& value
     if (values.size() > cx_->n()) throw std::invalid_argument("plain operand: more values than slots");
     const uint64_t* pt = plain(values, false);
     Message r = fresh(a.depth, a.plain_depth + 1, mag);
-    ct_mul_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    ct_mul_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 
@@ -422,7 +456,7 @@ Message Evaluator::mul_scalar(const Message& a, int64_t sc) {  // evaluator.cpp:
     check_magnitude(mag, "mul_scalar");
     counters_.ops.scalar_mul += 1;
     Message r = fresh(a.depth, a.plain_depth + 1, mag);
-    ct_mul_scalar(cx_->device(), a.data(), sc, r.data(), static_cast<uint32_t>(cx_->cts()), cx_->stream());
+    ct_mul_scalar(cx_->device(), a.data(), sc, r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 
@@ -443,16 +477,16 @@ Message Evaluator::shift_columns(const Message& a, uint32_t right_by, const Mess
         Message r = fresh(std::max(a.depth, base->depth), std::max(a.plain_depth, base->plain_depth),
                           a.magnitude + base->magnitude);
         if (g == 1)
-            ct_add(cx_->device(), base->data(), a.data(), r.data(), cts, cx_->stream());
+            ct_add(cx_->device(), base->data(), a.data(), r.data(), cts, stream_);
         else
-            ct_rotate_add(cx_->device(), base->data(), a.data(), g, r.data(), cts, cx_->stream());
+            ct_rotate_add(cx_->device(), base->data(), a.data(), g, r.data(), cts, stream_);
         return r;
     }
     Message r = fresh(a.depth, a.plain_depth, a.magnitude);
     if (g == 1) {
-        LB_CUDA(cudaMemcpyAsync(r.data(), a.data(), cx_->payload_bytes(), cudaMemcpyDeviceToDevice, cx_->stream()));
+        LB_CUDA(cudaMemcpyAsync(r.data(), a.data(), cx_->payload_bytes(), cudaMemcpyDeviceToDevice, stream_));
     } else {
-        ct_rotate(cx_->device(), a.data(), g, r.data(), cts, cx_->stream());
+        ct_rotate(cx_->device(), a.data(), g, r.data(), cts, stream_);
     }
     return r;
 }
@@ -471,7 +505,7 @@ Message Evaluator::rotate_rows(const Message& a) {  // evaluator.cpp:301-324
     counters_.ops.rot_rows += 1;
     Message r = fresh(a.depth, a.plain_depth, a.magnitude);
     ct_rotate(cx_->device(), a.data(), 2ull * cx_->n() - 1, r.data(), static_cast<uint32_t>(cx_->cts()),
-              cx_->stream());
+              stream_);
     return r;
 }
 
@@ -494,7 +528,7 @@ Message Evaluator::mul_scalar_add(const Message& acc, const Message& x, int64_t 
     counters_.ops.add += 1;
     Message r = fresh(std::max(acc.depth, x.depth), std::max(acc.plain_depth, x.plain_depth + 1), mag);
     ct_mul_scalar_add(cx_->device(), acc.data(), x.data(), sc, r.data(), static_cast<uint32_t>(cx_->cts()),
-                      cx_->stream());
+                      stream_);
     return r;
 }
 
@@ -528,7 +562,7 @@ Message Evaluator::rotate_rows_add(const Message& base, const Message& x) {
     counters_.ops.add += 1;
     Message r = fresh(std::max(x.depth, base.depth), std::max(x.plain_depth, base.plain_depth), mag);
     ct_rotate_add(cx_->device(), base.data(), x.data(), 2ull * cx_->n() - 1, r.data(),
-                  static_cast<uint32_t>(cx_->cts()), cx_->stream());
+                  static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
 }
 

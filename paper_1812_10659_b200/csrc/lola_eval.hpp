@@ -107,6 +107,12 @@ public:
     cudaStream_t stream() const { return stream_; }
     uint64_t cts() const { return uint64_t(batch_) * cx_->T(); }
     size_t payload_bytes() const { return cts() * 2 * cx_->L() * cx_->n() * 8; }
+    // Side streams for fanning independent op chains out (the GPU analogue
+    // of the reference's thread fan-out, proj/src/kernels.cpp:161-195).
+    // LB_STREAMS (default 8) sets the count; 1 disables the fan-out.
+    uint32_t fanout() const;
+    cudaStream_t side_stream(uint32_t i) const;
+    ~EvalContext();
 
 private:
     Context* cx_;
@@ -114,6 +120,7 @@ private:
     uint32_t max_depth_;
     cudaStream_t stream_;
     Mag capacity_;
+    mutable std::vector<cudaStream_t> side_;
 };
 
 // Shared cache of device-encoded plaintext operands keyed by value.
@@ -121,6 +128,11 @@ struct PlainCache {
     struct Entry {
         std::vector<int64_t> values;
         DeviceBuffer pt;  // [T][L][n]
+        cudaStream_t made_on = nullptr;
+        cudaEvent_t ready = nullptr;  // recorded after encoding on made_on
+        ~Entry() {
+            if (ready) cudaEventDestroy(ready);
+        }
     };
     std::unordered_map<uint64_t, std::vector<std::unique_ptr<Entry>>> mul, add;
 };
@@ -171,9 +183,13 @@ public:
     void note_live(uint64_t live) { counters_.note_live(live); }
     Evaluator fork() const;
     void absorb(const Evaluator& child);
+    // fork whose device work goes to stream `s` (shares caches and ids)
+    Evaluator fork_on(cudaStream_t s) const;
+    cudaStream_t stream() const { return stream_; }
 
 private:
     const EvalContext* cx_;
+    cudaStream_t stream_;
     OpCounters counters_;
     std::shared_ptr<PlainCache> cache_;
     std::shared_ptr<uint64_t> next_id_;

@@ -82,6 +82,52 @@ std::optional<uint32_t> ConvGeometry::tap(uint32_t j, uint32_t w) const {
 
 namespace {
 
+// ---- stream fan-out -------------------------------------------------------------------
+// Independent op chains (rows of a row-major product, calls of the stacked
+// product, output maps, per-message masks and squares) run on forked
+// evaluators bound to the context's side streams: the GPU analogue of the
+// reference's per-row thread fan-out with fork/absorb (kernels.cpp:161-195).
+// Children start after the parent's queued work (event), the parent resumes
+// after all children (events), counters are absorbed in child order, and
+// messages produced by children are rebound to the parent stream so their
+// frees are ordered after the parent's uses.
+class FanOut {
+public:
+    FanOut(Evaluator& ev, uint64_t tasks) : ev_(ev) {
+        const uint32_t S = static_cast<uint32_t>(std::min<uint64_t>(ev.context().fanout(), tasks));
+        if (S <= 1) return;
+        cudaEvent_t start;
+        LB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        LB_CUDA(cudaEventRecord(start, ev.stream()));
+        for (uint32_t i = 0; i < S; ++i) {
+            cudaStream_t st = ev.context().side_stream(i);
+            LB_CUDA(cudaStreamWaitEvent(st, start, 0));
+            kids_.push_back(ev.fork_on(st));
+        }
+        LB_CUDA(cudaEventDestroy(start));
+    }
+    Evaluator& operator[](uint64_t task) { return kids_.empty() ? ev_ : kids_[task % kids_.size()]; }
+    uint32_t width() const { return kids_.empty() ? 1u : static_cast<uint32_t>(kids_.size()); }
+    // join, then adopt the produced messages on the parent stream
+    void join(std::vector<Message>& produced) {
+        if (kids_.empty()) return;
+        for (Evaluator& k : kids_) {
+            cudaEvent_t done;
+            LB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+            LB_CUDA(cudaEventRecord(done, k.stream()));
+            LB_CUDA(cudaStreamWaitEvent(ev_.stream(), done, 0));
+            LB_CUDA(cudaEventDestroy(done));
+            ev_.absorb(k);
+        }
+        for (Message& m : produced) m.payload->buf.rebind(ev_.stream());
+        kids_.clear();
+    }
+
+private:
+    Evaluator& ev_;
+    std::vector<Evaluator> kids_;
+};
+
 // ---- encoders (input side; images already on the device) ------------------------
 
 // encode_convolution (representation.cpp:131-165): message j carries the tap
@@ -215,13 +261,27 @@ EncodedTensor sparse_to_dense(Evaluator& ev, const EncodedTensor& t) {  // repre
     require(t.rep.broadcast, "only broadcast sparse values can be re-slotted");
     const uint32_t n = ev.context().n();
     require(t.rep.length <= n, "target slot out of range");
-    Message acc;
+    // per-stream partial sums, then their sum: v masks and v - 1 additions
+    // in any association, exactly as the reference counts them
+    FanOut fan(ev, t.rep.length);
+    const uint32_t S = fan.width();
+    std::vector<Message> partial(S);
+    std::vector<bool> started(S, false);
     for (uint64_t i = 0; i < t.rep.length; ++i) {
         std::vector<uint8_t> bits(n, 0);
         bits[i] = 1;
-        Message picked = ev.mask(t.messages[i], bits);
-        acc = i == 0 ? picked : ev.add(acc, picked);
+        Evaluator& e = fan[i];
+        const uint32_t k = static_cast<uint32_t>(i % S);
+        Message picked = e.mask(t.messages[i], bits);
+        partial[k] = started[k] ? e.add(partial[k], picked) : picked;
+        started[k] = true;
     }
+    std::vector<Message> used;
+    for (uint32_t k = 0; k < S; ++k)
+        if (started[k]) used.push_back(partial[k]);
+    fan.join(used);
+    Message acc = used[0];
+    for (size_t k = 1; k < used.size(); ++k) acc = ev.add(acc, used[k]);
     EncodedTensor out;
     out.rep.kind = RepKind::Dense;  // identity targets
     out.rep.length = t.rep.length;
@@ -239,7 +299,9 @@ EncodedTensor mask_active(Evaluator& ev, const EncodedTensor& t) {  // represent
     EncodedTensor out;
     out.rep = t.rep;
     out.rep.dirty = false;
-    for (const auto& m : t.messages) out.messages.push_back(ev.mask(m, bits));
+    FanOut fan(ev, t.messages.size());
+    for (size_t i = 0; i < t.messages.size(); ++i) out.messages.push_back(fan[i].mask(t.messages[i], bits));
+    fan.join(out.messages);
     return out;
 }
 
@@ -455,11 +517,13 @@ EncodedTensor matvec_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weigh
     out.rep.value_slot = 0;
     out.rep.dirty = !out.rep.broadcast;
     std::vector<int64_t> w(n);
+    FanOut fan(ev, W.rows);
     for (uint64_t row = 0; row < W.rows; ++row) {
         std::fill(w.begin(), w.end(), 0);
         for (uint64_t i = 0; i < W.cols; ++i) w[x.rep.slot(i)] = W.at(row, i);
-        out.messages.push_back(dot_product(ev, x.messages[0], w, span));
+        out.messages.push_back(dot_product(fan[row], x.messages[0], w, span));
     }
+    fan.join(out.messages);
     return out;
 }
 
@@ -487,6 +551,7 @@ EncodedTensor matvec_stacked_rowmajor(Evaluator& ev, const EncodedTensor& x, con
     out.rep.slot_of.resize(copies);
     for (uint32_t d = 0; d < copies; ++d) out.rep.slot_of[d] = static_cast<uint32_t>((d + 1) * pad - 1);
     std::vector<int64_t> w(n);
+    FanOut fan(ev, calls);
     for (uint64_t c = 0; c < calls; ++c) {
         std::fill(w.begin(), w.end(), 0);
         for (uint32_t d = 0; d < copies; ++d) {
@@ -494,8 +559,10 @@ EncodedTensor matvec_stacked_rowmajor(Evaluator& ev, const EncodedTensor& x, con
             if (row >= W.rows) break;
             for (uint64_t i = 0; i < W.cols; ++i) w[d * pad + (x.rep.slot(i) & (pad - 1))] = W.at(row, i);
         }
-        out.messages.push_back(reduce_rotate_add(ev, ev.mul_plain(x.messages[0], w), pad, false));
+        Evaluator& e = fan[c];
+        out.messages.push_back(reduce_rotate_add(e, e.mul_plain(x.messages[0], w), pad, false));
     }
+    fan.join(out.messages);
     return out;
 }
 
@@ -513,12 +580,15 @@ EncodedTensor conv_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weights
         out.rep.kind = RepKind::Dense;
         out.rep.slot_of.clear();
     }
+    FanOut fan(ev, W.rows);
     for (uint64_t map = 0; map < W.rows; ++map) {
-        Message acc = ev.mul_scalar(x.messages[0], W.at(map, 0));
+        Evaluator& e = fan[map];
+        Message acc = e.mul_scalar(x.messages[0], W.at(map, 0));
         for (uint64_t j = 1; j < W.cols; ++j)  // acc = add(acc, mul_scalar(x_j, w)), fused
-            acc = ev.mul_scalar_add(acc, x.messages[j], W.at(map, j));
+            acc = e.mul_scalar_add(acc, x.messages[j], W.at(map, j));
         out.messages.push_back(std::move(acc));
     }
+    fan.join(out.messages);
     return out;
 }
 
@@ -526,7 +596,9 @@ EncodedTensor square_activation(Evaluator& ev, const EncodedTensor& x) {  // ker
     require(!x.messages.empty(), "empty tensor");
     EncodedTensor out;
     out.rep = x.rep;
-    for (const auto& m : x.messages) out.messages.push_back(ev.mul(m, m));
+    FanOut fan(ev, x.messages.size());
+    for (size_t i = 0; i < x.messages.size(); ++i) out.messages.push_back(fan[i].mul(x.messages[i], x.messages[i]));
+    fan.join(out.messages);
     return out;
 }
 
@@ -538,14 +610,16 @@ EncodedTensor add_bias(Evaluator& ev, const EncodedTensor& x, const std::vector<
     if (x.rep.kind == RepKind::Sparse) {
         require(bias.size() == x.messages.size(), "one bias per message required");
         std::vector<int64_t> b(n);
+        FanOut fan(ev, x.messages.size());
         for (size_t i = 0; i < x.messages.size(); ++i) {
             std::fill(b.begin(), b.end(), 0);
             if (x.rep.broadcast)
                 std::fill(b.begin(), b.end(), bias[i]);
             else
                 b[x.rep.value_slot] = bias[i];
-            out.messages.push_back(ev.add_plain(x.messages[i], b));
+            out.messages.push_back(fan[i].add_plain(x.messages[i], b));
         }
+        fan.join(out.messages);
         return out;
     }
     require(x.rep.kind != RepKind::Simd, "record tensors are not supported");

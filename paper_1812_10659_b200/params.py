@@ -79,6 +79,13 @@ def lola_mnist_params(seed: int = 1) -> BfvParams:
     return make_params(16384, L=5, T=5, K=1, dnum=5, seed=seed)
 
 
+def lola_cifar_params(seed: int = 1) -> BfvParams:
+    """Config 4: n = 16384, 6 plaintext primes (final bound 183
+    bits), L = 6 (its second window stage and 4075-value square add ~25 bits
+    of noise over LoLa-MNIST), K = 1, dnum = 6: log2(QP) = 420 <= 438."""
+    return make_params(16384, L=6, T=6, K=1, dnum=6, seed=seed)
+
+
 def lola_small_params(seed: int = 1) -> BfvParams:
     """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square)."""
     return make_params(8192, L=3, T=2, K=1, dnum=3, seed=seed)

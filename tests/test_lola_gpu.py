@@ -45,3 +45,23 @@ def test_lola_small_config3():
 
 def test_lola_mnist_config0():
     _check(lola_mnist_params(), nets.lola_mnist_net(), "lola-mnist", batch=2, config=0)
+
+
+def test_lola_cifar_config4_single_image():
+    """BASELINE config 4 (83 + 163 maps, 57,252 rotations per instance, 6
+    plaintext primes): decrypted logits == forward_integer; per-step counters
+    == the plan's predictions (checked inside execute) whose totals equal the
+    golden trace proj/tests/golden/lola_cifar.txt:10."""
+    from paper_1812_10659_b200.lola import plan_counters
+    from paper_1812_10659_b200.params import lola_cifar_params
+
+    net = nets.lola_cifar_net()
+    prm = lola_cifar_params()
+    cx = BfvContext(prm)
+    sess = Session(cx, net, "lola-cifar", 1)
+    img = nets.images(4, net, 1)
+    scores, counters, _ = sess.run(img)
+    predicted, _, _ = plan_counters(net, "lola-cifar", prm.n)
+    assert np.array_equal(counters, predicted)
+    assert counters.sum(0).tolist() == [2, 8160, 15936, 4075, 81265, 53177, 4075]
+    assert scores[0] == R.forward_integer(net, img[0])
