@@ -51,8 +51,11 @@ def main():
     peak = C.c_double()
     lines = []
     for spec in a.grid.split(","):
-        n, L = (int(x) for x in spec.split(":"))
-        prm = make_params(n, L=L, T=1, K=1, seed=1)
+        parts = [int(x) for x in spec.split(":")]
+        n, L = parts[:2]
+        K = parts[2] if len(parts) > 2 else 1
+        dnum = parts[3] if len(parts) > 3 else L
+        prm = make_params(n, L=L, T=1, K=K, dnum=dnum, seed=1)
         cx = BfvContext(prm)
         nat.call("lb_bench_butterfly_peak", prm.q[0], 4, 2000, C.byref(peak))
         B = a.batch
@@ -75,7 +78,7 @@ def main():
         bfly = nlimb * (n // 2) * (n.bit_length() - 1)
         ct_bytes = 2 * L * n * 8
         rec = {
-            "n": n, "L": L, "batch": B, "K": 1, "dnum": L,
+            "n": n, "L": L, "batch": B, "K": K, "dnum": dnum,
             "ntt_fwd_limbs_per_s": nlimb / t_fwd, "ntt_inv_limbs_per_s": nlimb / t_inv,
             "ntt_fwd_gbfly_s": bfly / t_fwd / 1e9, "int_peak_gbfly_s": peak.value / 1e9,
             "ntt_fwd_frac_of_int_peak": bfly / t_fwd / peak.value,

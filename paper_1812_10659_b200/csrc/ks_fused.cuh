@@ -95,6 +95,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
             // single-prime digit: the coefficient (< q_lo < 4 q_r) feeds the
             // lazy transform unreduced
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
+        } else if (hi - lo == 2) {
+            // two-prime digit, fully unrolled so every load of the pass is in
+            // flight at once: y_0 [D/q_0]_r + y_1 [D/q_1]_r in [0, 4r)
+            const ulonglong2 w0 = d.dhat_mod_sh[lo * LK + r], w1 = d.dhat_mod_sh[(lo + 1) * LK + r];
+            const uint64_t* src1 = src + n;
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+                return mul_shoup_lazy(__ldg(&src[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&src1[x]), w1.x, w1.y, q);
+            });
         } else {
             // src limbs already hold y_i = [d_i (D_j/q_i)^-1]_{q_i}; fast base
             // conversion sum_i y_i [D_j/q_i]_r, kept lazily in [0, 2r)
@@ -165,9 +173,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]
 }
 
 constexpr int kTmemCols = 128;
+#ifndef LB_KS_TMEM_MINB
+#define LB_KS_TMEM_MINB 3
+#endif
 
 template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(BfvDev d, KsInnerArgs a) {
+__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_tmem_kernel(BfvDev d, KsInnerArgs a) {
     using S = NttShape<LOGN>;
     static_assert(S::T == 256 || S::T == 128, "TMEM layout assumes 4 or 8 warps");
     // 4 columns (acc0, acc1 as 32-bit word pairs) per element; warps beyond
@@ -243,6 +254,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 3) ks_inner_tmem_kernel(Bfv
         const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
         if (hi - lo == 1) {
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
+        } else if (hi - lo == 2) {
+            // two-prime digit, fully unrolled so every load of the pass is in
+            // flight at once: y_0 [D/q_0]_r + y_1 [D/q_1]_r in [0, 4r)
+            const ulonglong2 w0 = d.dhat_mod_sh[lo * LK + r], w1 = d.dhat_mod_sh[(lo + 1) * LK + r];
+            const uint64_t* src1 = src + n;
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+                return mul_shoup_lazy(__ldg(&src[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&src1[x]), w1.x, w1.y, q);
+            });
         } else {
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
                 uint64_t v = 0;
@@ -306,6 +325,12 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
     if (d.K == 1) {
         // [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&accp[x]); });
+    } else if (d.K == 2) {
+        const ulonglong2 w0 = d.phat_mod_sh[r], w1 = d.phat_mod_sh[d.L + r];
+        const uint64_t* accp1 = accp + n;
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+            return mul_shoup_lazy(__ldg(&accp[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&accp1[x]), w1.x, w1.y, q);
+        });
     } else {
         // P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded into the
         // inverse transform); sum_l y_l [P/p_l]_{q_r}, lazily in [0, 2q)
