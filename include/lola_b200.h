@@ -53,6 +53,8 @@ typedef struct {
     const uint64_t* t;
     uint32_t dnum;         /* key-switch digits (0 = num_q) */
     uint64_t seed;         /* secret key / key material seed */
+    int32_t device;        /* CUDA device ordinal (this library's runtime keeps its
+                              own current device: callers pass torch's LOCAL_RANK) */
 } lb_params;
 
 /* ---- errors, setup ----------------------------------------------------- */

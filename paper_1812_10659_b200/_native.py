@@ -29,7 +29,7 @@ class BudgetError(LolaError):
 
 class lb_params(C.Structure):
     _fields_ = [("n", u32), ("num_q", u32), ("num_p", u32), ("num_b", u32), ("num_t", u32),
-                ("q", P64), ("p", P64), ("b", P64), ("t", P64), ("dnum", u32), ("seed", u64)]
+                ("q", P64), ("p", P64), ("b", P64), ("t", P64), ("dnum", u32), ("seed", u64), ("device", i32)]
 
 
 # name -> argtypes; every function returns int status except lb_last_error.

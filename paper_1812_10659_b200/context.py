@@ -41,6 +41,16 @@ def _stream_ptr(stream) -> int | None:
     return int(getattr(stream, "cuda_stream", stream)) or None
 
 
+def _current_device() -> int:
+    """torch's current CUDA device (the library's runtime is told explicitly)."""
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else 0
+    except Exception:
+        return 0
+
+
 class Context:
     """params: any object with n, q, p, b, t, dnum, seed (Params or
     params.BfvParams)."""
@@ -54,7 +64,7 @@ class Context:
         self._t = nat.u64_array(params.t)
         prm = nat.lb_params(params.n, len(params.q), len(params.p), len(b), len(params.t),
                             C.cast(self._q, nat.P64), C.cast(self._p, nat.P64), C.cast(self._b, nat.P64),
-                            C.cast(self._t, nat.P64), params.dnum, params.seed)
+                            C.cast(self._t, nat.P64), params.dnum, params.seed, _current_device())
         h = C.c_void_p()
         nat.call("lb_context_create", C.byref(prm), C.byref(h))
         self.handle = h

@@ -52,6 +52,7 @@ int lb_context_create(const lb_params* prm, lb_context** out) {
         if (prm->num_t) p.t.assign(prm->t, prm->t + prm->num_t);
         p.dnum = prm->dnum;
         p.seed = prm->seed;
+        p.device = prm->device;
         *out = new lb_context(p);
     });
 }
@@ -75,6 +76,7 @@ int lb_sync(lb_context* cx, void* stream) {
 int lb_ntt_forward(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs, uint32_t first_prime,
                    uint64_t poly_stride, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && data, "null argument");
         cx->cx.ntt_forward(lb::LimbBatch{data, polys, limbs, first_prime, poly_stride}, pick(cx, stream));
     });
@@ -83,6 +85,7 @@ int lb_ntt_forward(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
 int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs, uint32_t first_prime,
                    uint64_t poly_stride, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && data, "null argument");
         cx->cx.ntt_inverse(lb::LimbBatch{data, polys, limbs, first_prime, poly_stride}, pick(cx, stream));
     });
@@ -91,6 +94,7 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
 int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
                      void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && values && out, "null argument");
         lb::encrypt_slots(cx->cx, values, B, id_base, out, pick(cx, stream));
     });
@@ -98,6 +102,7 @@ int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t
 
 int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && ct && out, "null argument");
         lb::decrypt_slots(cx->cx, ct, B, out, pick(cx, stream));
     });
@@ -105,6 +110,7 @@ int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* o
 
 int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && ct && out, "null argument");
         lb::decrypt_coeffs(cx->cx, ct, B, out, pick(cx, stream));
     });
@@ -112,6 +118,7 @@ int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* 
 
 int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && values && (pt_mul || pt_add), "null argument");
         lb::encode_plain(cx->cx, values, pt_mul, pt_add, pick(cx, stream));
     });
@@ -119,6 +126,7 @@ int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uin
 
 int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && b && out, "null argument");
         lb::ct_add(cx->cx, a, b, out, count, pick(cx, stream));
     });
@@ -127,6 +135,7 @@ int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* ou
 int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count,
                      void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && out, "null argument");
         lb::ct_mul_scalar(cx->cx, a, scalar, out, count, pick(cx, stream));
     });
@@ -135,6 +144,7 @@ int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t
 int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
                     void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && pt && out, "null argument");
         lb::ct_mul_plain(cx->cx, a, pt, out, count, pick(cx, stream));
     });
@@ -143,6 +153,7 @@ int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint6
 int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
                     void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && pt && out, "null argument");
         lb::ct_add_plain(cx->cx, a, pt, out, count, pick(cx, stream));
     });
@@ -151,6 +162,7 @@ int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint6
 int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count,
                  void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && out, "null argument");
         lb::ct_rotate(cx->cx, a, galois, out, count, pick(cx, stream));
     });
@@ -158,6 +170,7 @@ int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* o
 
 int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && a && b && out, "null argument");
         lb::ct_mul(cx->cx, a, b, out, count, pick(cx, stream));
     });
@@ -165,6 +178,7 @@ int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* ou
 
 int lb_keygen(lb_context* cx, uint64_t key_id, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx != nullptr, "null context");
         lb::ensure_key(cx->cx, key_id, pick(cx, stream));
     });
@@ -172,6 +186,7 @@ int lb_keygen(lb_context* cx, uint64_t key_id, void* stream) {
 
 int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && out, "null argument");
         *out = lb::key_ptr(cx->cx, key_id);
     });
@@ -180,6 +195,7 @@ int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out) {
 int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
                     uint64_t galois, void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && in && out, "null argument");
         need(limbs <= cx->cx.prime_count(), "too many limbs");
         lb::automorphism_ntt(cx->cx, in, out, polys, limbs, galois, pick(cx, stream));
@@ -189,6 +205,7 @@ int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t 
 int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
                   void* stream) {
     return guarded([&] {
+        if (cx) cx->cx.activate();
         need(cx && d && u0 && u1, "null argument");
         lb::key_switch(cx->cx, d, key_id, u0, u1, count, pick(cx, stream));
     });

@@ -11,7 +11,13 @@ std::atomic<uint64_t>& launch_counter() {
     return count;
 }
 
+void Context::activate() const {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != prm_.device) LB_CUDA(cudaSetDevice(prm_.device));
+}
+
 Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
+    activate();
     if (n_ < 4096 || n_ > 32768 || (n_ & (n_ - 1)))
         throw std::invalid_argument("ring degree must be a power of two in [4096, 32768]");
     logn_ = host::ilog2(n_);

@@ -87,6 +87,7 @@ struct Params {
     std::vector<uint64_t> q, p, b, t;
     uint32_t dnum = 0;
     uint64_t seed = 0;
+    int device = 0;
 };
 
 struct BfvState;  // bfv.cu
@@ -115,6 +116,9 @@ public:
     const PrimeDev& host_prime(uint32_t i) const { return host_primes_.at(i); }  // constants only
     const Modulus& modulus(uint32_t i) const { return mods_.at(i); }
     cudaStream_t stream() const { return stream_; }
+    int device() const { return prm_.device; }
+    // make this context's device current for the calling thread
+    void activate() const;
 
     // Batched transforms over [polys][limbs][N] with limb l using prime
     // first_prime + l.

@@ -35,6 +35,7 @@ extern "C" {
 int lb_eval_create(lb_context* cx, uint32_t batch, uint32_t max_depth, void* stream, lb_evaluator** out) {
     return guarded([&] {
         need(cx && out, "null argument");
+        cx->cx.activate();
         auto e = std::make_unique<lb_evaluator>();
         e->ecx = std::make_shared<lb::lola::EvalContext>(cx->cx, batch, max_depth, static_cast<cudaStream_t>(stream));
         e->ev = std::make_unique<lb::lola::Evaluator>(*e->ecx);

@@ -134,6 +134,7 @@ int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* st
                            uint32_t max_depth, void* stream, lb_lola_session** out) {
     return guarded([&] {
         if (!cx || !out) throw std::invalid_argument("null argument");
+        cx->cx.activate();
         auto s = std::make_unique<lb_lola_session>();
         s->net = to_network(net);
         s->plan = lb::lola::build_plan(s->net, lb::lola::strategy_from_name(strategy), cx->cx.n());

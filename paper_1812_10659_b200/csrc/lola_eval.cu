@@ -255,6 +255,7 @@ void Evaluator::absorb(const Evaluator& child) {  // evaluator.cpp:334-337
 }
 
 Message Evaluator::fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const {
+    cx_->device().activate();  // every counted op starts here
     Message m;
     m.payload = std::make_shared<Payload>();
     m.payload->buf = DeviceBuffer(cx_->payload_bytes(), stream_);
@@ -323,6 +324,7 @@ Message Evaluator::lift_gather(const int64_t* dev_images, uint64_t stride, const
 
 DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t>& slots) const {
     Context& dc = cx_->device();
+    dc.activate();
     const uint32_t n = cx_->n(), B = cx_->batch(), T = dc.T();
     cudaStream_t s = stream_;
     DeviceBuffer res(uint64_t(B) * T * n * 8, s);
