@@ -35,12 +35,13 @@ WORKLOADS = {
 }
 
 
-def workload_objects(name: str):
+def workload_objects(name: str, word: int = 64):
     from paper_1812_10659_b200 import nets, params
 
     cfg, strategy, batch = WORKLOADS[name]
     if name == "lola-mnist":
-        return cfg, strategy, batch, nets.lola_mnist_net(config=2), params.lola_mnist_params()
+        prm = params.lola_mnist_params_w32() if word == 32 else params.lola_mnist_params()
+        return cfg, strategy, batch, nets.lola_mnist_net(config=2), prm
     if name == "lola-small":
         return cfg, strategy, batch, nets.lola_small_net(config=3), params.lola_small_params()
     return cfg, strategy, batch, nets.lola_cifar_net(config=4), params.lola_cifar_params()
@@ -57,6 +58,8 @@ def parse():
                     help="lola-mnist = BASELINE config 2 (the headline); lola-small = config 3; lola-cifar = config 4")
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
+    ap.add_argument("--word", type=int, default=64, choices=[32, 64],
+                    help="RNS word: 64 = 60-bit primes, 32 = 30-bit primes (32-bit word kernels)")
     return ap.parse_args()
 
 
@@ -271,7 +274,7 @@ def run_ours(a, world, rank, local):
     from paper_1812_10659_b200.bfv import BfvContext
     from paper_1812_10659_b200.lola import Session, plan_counters
     torch.cuda.set_device(local)
-    cfg, strategy, default_batch, net, prm = workload_objects(a.workload)
+    cfg, strategy, default_batch, net, prm = workload_objects(a.workload, a.word)
     cx = BfvContext(prm)
     B = a.batch or default_batch
     sess = Session(cx, net, strategy, B)

@@ -471,10 +471,12 @@ int bo_decrypt(bo_ctx* c, uint32_t tj, const uint64_t* ct, uint64_t* m) {
             x[i].resize(c->n);
             for (uint32_t k = 0; k < c->n; ++k) x[i][k] = addm(c0[k], p[k], qi);
         }
-        std::vector<uint64_t> hinv(c->L), phi_hi(c->L), phi_lo(c->L);
+        std::vector<uint64_t> hinv(c->L), phi_hi(c->L), phi_lo(c->L), phi_int(c->L);
         for (uint32_t i = 0; i < c->L; ++i) {
             hinv[i] = invm(bo_ctx::prod_mod(c->q, 0, c->L, i, c->q[i]), c->q[i]);
-            frac128(t, c->q[i], phi_hi[i], phi_lo[i]);
+            // t / q_i = phi_int + (phi_hi, phi_lo) / 2^128 (t may exceed q_i)
+            frac128(t % c->q[i], c->q[i], phi_hi[i], phi_lo[i]);
+            phi_int[i] = t / c->q[i];
         }
         for (uint32_t k = 0; k < c->n; ++k) {
             uint64_t H = 0, Lo = 0;
@@ -486,7 +488,7 @@ int bo_decrypt(bo_ctx* c, uint32_t tj, const uint64_t* ct, uint64_t* m) {
                 pl += add;
                 ph += (pl < add);
                 Lo += pl;
-                H += ph + (Lo < pl);
+                H += ph + (Lo < pl) + y * phi_int[i];
             }
             m[k] = (H + (Lo >> 63)) % t;
         }

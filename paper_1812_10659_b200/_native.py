@@ -6,9 +6,12 @@ library is missing or fails to load, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "liblola_b200.so"
+if os.environ.get("LB_LIB"):  # experiment builds (build.py LB_VARIANT)
+    LIB_PATH = Path(__file__).resolve().parent / "lib" / "variants" / os.environ["LB_LIB"] / "liblola_b200.so"
 
 u32, u64, i32, i64, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_void_p
 P64 = C.POINTER(C.c_uint64)

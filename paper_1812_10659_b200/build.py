@@ -15,6 +15,13 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 OUT = HERE / "lib"
 LIB = OUT / "liblola_b200.so"
+# experiment builds: LB_VARIANT=name LB_EXTRA_FLAGS="-DX=1" writes
+# lib/variants/name/liblola_b200.so (selected at run time with LB_LIB)
+VARIANT = os.environ.get("LB_VARIANT", "")
+EXTRA = os.environ.get("LB_EXTRA_FLAGS", "").split()
+if VARIANT:
+    OUT = OUT / "variants" / VARIANT
+    LIB = OUT / "liblola_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -22,7 +29,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 
 def _compile(src: Path, obj: Path) -> None:
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
@@ -38,7 +45,7 @@ def _stale(obj: Path, src: Path) -> bool:
 
 
 def build(force: bool = False) -> Path:
-    OUT.mkdir(exist_ok=True)
+    OUT.mkdir(parents=True, exist_ok=True)
     objdir = OUT / "obj"
     objdir.mkdir(exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu"))

@@ -5,6 +5,7 @@
 // :178-202, mul_plain :204-226, mul_scalar :242-258, rotations :260-332);
 // here every one of them runs on BFV ciphertexts.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -122,6 +123,16 @@ __global__ void k_shoup_pairs(BfvDev d, const uint64_t* __restrict__ key, ulongl
     out[idx] = make_ulonglong2(k, est);
 }
 
+// (k, floor(k 2^32 / q)) for the 32-bit word key switch (every q < 2^30)
+__global__ void k_shoup_pairs32(BfvDev d, const uint64_t* __restrict__ key, uint2* __restrict__ out, uint64_t total,
+                                uint32_t limbs) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const uint64_t q = d.primes[(idx / d.n) % limbs].q;
+    const uint64_t k = key[idx];
+    out[idx] = make_uint2(static_cast<uint32_t>(k), static_cast<uint32_t>((k << 32) / q));
+}
+
 __global__ void k_square_limbs(const uint64_t* __restrict__ s, uint64_t* __restrict__ out, BfvDev d, uint32_t limbs) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(limbs) * d.n) return;
@@ -222,7 +233,7 @@ __global__ void k_dec_scale(BfvDev d, const uint64_t* __restrict__ x, uint32_t c
         uint64_t ip, fp;
         fixmul(y, d.phi[j * d.L + i], ip, fp);
         Lo += fp;
-        H += ip + (Lo < fp ? 1 : 0);
+        H += ip + (Lo < fp ? 1 : 0) + y * d.phi_int[j * d.L + i];
     }
     const Modulus tm = modulus_of(d.primes[d.tbase + j]);
     m[idx] = reduce_u64(H + (Lo >> 63), tm);
@@ -493,13 +504,19 @@ void bfv_setup(Context& cx) {
 
     std::vector<uint64_t> qhat_inv(L);
     std::vector<ulonglong2> phi(T * L), q_frac(L);
+    std::vector<uint64_t> phi_int(std::max<size_t>(1, size_t(T) * L));
     for (uint32_t i = 0; i < L; ++i) {
         qhat_inv[i] = invm(prod_mod(q, 0, L, i, q[i]), q[i]);
         q_frac[i] = frac128(1, q[i]);
-        for (uint32_t j = 0; j < T; ++j) phi[j * L + i] = frac128(t[j], q[i]);
+        for (uint32_t j = 0; j < T; ++j) {
+            // t_j / q_i = phi_int + phi / 2^128 (t_j > q_i for 30-bit q_i)
+            phi[j * L + i] = frac128(t[j] % q[i], q[i]);
+            phi_int[j * L + i] = t[j] / q[i];
+        }
     }
     const size_t o_qhinv = put(qhat_inv.data(), L * 8);
     const size_t o_phi = put(phi.data(), phi.size() * 16);
+    const size_t o_phint = put(phi_int.data(), phi_int.size() * 8);
     const size_t o_qfrac = put(q_frac.data(), L * 16);
 
     std::vector<uint64_t> qhat_mod_b(L * std::max(M, 1u)), q_mod_b(std::max(M, 1u));
@@ -588,6 +605,29 @@ void bfv_setup(Context& cx) {
         ks_last_p[2 * l] = pair(mulm(hp.ninv, phat_inv[l], p[l]), p[l]);
         ks_last_p[2 * l + 1] = pair(mulm(hp.inv1n, phat_inv[l], p[l]), p[l]);
     }
+    // 32-bit word key switch when Q and P are all below 2^30
+    d.ks32 = Context::word32_enabled() && cx.primes_small(0, LK);
+    auto to32 = [&](const std::vector<ulonglong2>& v, auto&& modulus_of_index) {
+        std::vector<uint2> o(v.size());
+        for (size_t k = 0; k < v.size(); ++k) {
+            const uint64_t m = modulus_of_index(k);
+            o[k] = make_uint2(static_cast<uint32_t>(v[k].x), m ? shoup_companion32(v[k].x, m) : 0u);
+        }
+        return o;
+    };
+    size_t o_pi32 = 0, o_dh32 = 0, o_ph32 = 0, o_klq32 = 0, o_klp32 = 0;
+    if (d.ks32) {
+        const auto pi32 = to32(p_inv_shoup, [&](size_t k) { return q[k]; });
+        const auto dh32 = to32(dhat_mod_sh, [&](size_t k) { return qp[k % LK]; });
+        const auto ph32 = to32(phat_mod_sh, [&](size_t k) { return K ? q[k % L] : 0; });
+        const auto klq32 = to32(ks_last_q, [&](size_t k) { return q[k / 2]; });
+        const auto klp32 = to32(ks_last_p, [&](size_t k) { return K ? p[k / 2] : 0; });
+        o_pi32 = put(pi32.data(), pi32.size() * 8);
+        o_dh32 = put(dh32.data(), dh32.size() * 8);
+        o_ph32 = put(ph32.data(), ph32.size() * 8);
+        o_klq32 = put(klq32.data(), klq32.size() * 8);
+        o_klp32 = put(klp32.data(), klp32.size() * 8);
+    }
     const size_t o_dhsh = put(dhat_mod_sh.data(), dhat_mod_sh.size() * 16);
     const size_t o_phsh = put(phat_mod_sh.data(), phat_mod_sh.size() * 16);
     const size_t o_klq = put(ks_last_q.data(), ks_last_q.size() * 16);
@@ -614,6 +654,7 @@ void bfv_setup(Context& cx) {
     d.q_mod_t = reinterpret_cast<const uint64_t*>(base + o_qmt);
     d.qhat_inv = reinterpret_cast<const uint64_t*>(base + o_qhinv);
     d.phi = reinterpret_cast<const ulonglong2*>(base + o_phi);
+    d.phi_int = reinterpret_cast<const uint64_t*>(base + o_phint);
     d.q_frac = reinterpret_cast<const ulonglong2*>(base + o_qfrac);
     d.qhat_mod_b = reinterpret_cast<const uint64_t*>(base + o_qhmb);
     d.q_mod_b = reinterpret_cast<const uint64_t*>(base + o_qmb);
@@ -635,6 +676,22 @@ void bfv_setup(Context& cx) {
     d.phat_mod_sh = reinterpret_cast<const ulonglong2*>(base + o_phsh);
     d.ks_last_q = reinterpret_cast<const ulonglong2*>(base + o_klq);
     d.ks_last_p = reinterpret_cast<const ulonglong2*>(base + o_klp);
+    if (d.ks32) {
+        d.p_inv32 = reinterpret_cast<const uint2*>(base + o_pi32);
+        d.dhat_mod_sh32 = reinterpret_cast<const uint2*>(base + o_dh32);
+        d.phat_mod_sh32 = reinterpret_cast<const uint2*>(base + o_ph32);
+        d.ks_last_q32 = reinterpret_cast<const uint2*>(base + o_klq32);
+        d.ks_last_p32 = reinterpret_cast<const uint2*>(base + o_klp32);
+    }
+    {
+        // HPS scaling computes round(t D / Q) in base B, |D| < n Q^2 / 4
+        double lq = 0, lb = 0, lt = 0;
+        for (uint32_t i = 0; i < L; ++i) lq += std::log2(double(q[i]));
+        for (uint32_t m = 0; m < M; ++m) lb += std::log2(double(b[m]));
+        for (uint32_t j = 0; j < T; ++j) lt = std::max(lt, std::log2(double(t[j])));
+        st->mul_base_ok = M >= L + 1 && lb >= lq + lt + std::log2(double(n)) + 2;
+    }
+    st->qb_small = Context::word32_enabled() && cx.primes_small(0, L) && cx.primes_small(L + K, M);
     st->t_map = reinterpret_cast<const int16_t*>(base + o_tmap);
     st->qb_map = reinterpret_cast<const int16_t*>(base + o_qbmap);
     st->ks_map = reinterpret_cast<const int16_t*>(base + o_ksmap);
@@ -685,8 +742,14 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     k_keygen_finish<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get(), target.get(),
                                                                              d.p_mod_qp, key.buf.get());
     LB_KERNEL_DONE();
-    key.shoup = DeviceBuffer(key_elems * 16, s);
-    k_shoup_pairs<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<ulonglong2>(), key_elems, LK);
+    if (d.ks32) {
+        key.shoup = DeviceBuffer(key_elems * 8, s);
+        k_shoup_pairs32<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<uint2>(), key_elems, LK);
+    } else {
+        key.shoup = DeviceBuffer(key_elems * 16, s);
+        k_shoup_pairs<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<ulonglong2>(), key_elems,
+                                                             LK);
+    }
     LB_KERNEL_DONE();
     // keys are shared by every stream and outlive the (possibly side) stream
     // they were generated on: complete them now, free them on the context's
@@ -697,12 +760,12 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     st.keys.emplace(key_id, std::move(key));
 }
 
-static const ulonglong2* key_shoup_ptr(Context& cx, uint64_t key_id) {
+static const void* key_shoup_ptr(Context& cx, uint64_t key_id) {
     BfvState& st = *cx.bfv();
     std::lock_guard<std::mutex> lock(st.mu);
     auto it = st.keys.find(key_id);
     if (it == st.keys.end()) throw std::invalid_argument("key not generated");
-    return it->second.shoup.get<ulonglong2>();
+    return it->second.shoup.get();
 }
 
 const uint64_t* key_ptr(Context& cx, uint64_t key_id) {
@@ -727,10 +790,10 @@ bool ks_use_tmem() {
     return on;
 }
 
-template <int LOGN>
+template <int LOGN, class W>
 void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
     using S = NttShape<LOGN>;
-    if (ks_use_tmem()) {
+    if (sizeof(W) == 8 && ks_use_tmem()) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * (d.L + d.K) * S::CL));
         cfg.blockDim = dim3(S::T);
@@ -746,10 +809,10 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         launch_counter().fetch_add(1, std::memory_order_relaxed);
         return;
     }
-    const size_t smem = 3ull * S::M * 8;
+    const size_t smem = 3ull * S::M * sizeof(W);
     static bool configured = false;
     if (!configured) {
-        LB_CUDA(cudaFuncSetAttribute(ks_inner_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        LB_CUDA(cudaFuncSetAttribute(ks_inner_kernel<LOGN, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         configured = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -764,11 +827,11 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_kernel<LOGN>, d, a));
+    LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_kernel<LOGN, W>, d, a));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
-template <int LOGN>
+template <int LOGN, class W>
 void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     using S = NttShape<LOGN>;
     cudaLaunchConfig_t cfg = {};
@@ -782,18 +845,26 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN>, d, a));
+    LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN, W>, d, a));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
-void dispatch_ks(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDownArgs* ma, cudaStream_t s) {
+template <class W>
+void dispatch_ks_w(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDownArgs* ma, cudaStream_t s) {
     switch (logn) {
-        case 12: ma ? launch_moddown<12>(d, *ma, s) : launch_ks_inner<12>(d, ka, s); break;
-        case 13: ma ? launch_moddown<13>(d, *ma, s) : launch_ks_inner<13>(d, ka, s); break;
-        case 14: ma ? launch_moddown<14>(d, *ma, s) : launch_ks_inner<14>(d, ka, s); break;
-        case 15: ma ? launch_moddown<15>(d, *ma, s) : launch_ks_inner<15>(d, ka, s); break;
+        case 12: ma ? launch_moddown<12, W>(d, *ma, s) : launch_ks_inner<12, W>(d, ka, s); break;
+        case 13: ma ? launch_moddown<13, W>(d, *ma, s) : launch_ks_inner<13, W>(d, ka, s); break;
+        case 14: ma ? launch_moddown<14, W>(d, *ma, s) : launch_ks_inner<14, W>(d, ka, s); break;
+        case 15: ma ? launch_moddown<15, W>(d, *ma, s) : launch_ks_inner<15, W>(d, ka, s); break;
         default: throw std::invalid_argument("unsupported ring degree");
     }
+}
+
+void dispatch_ks(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDownArgs* ma, cudaStream_t s) {
+    if (d.ks32)
+        dispatch_ks_w<uint32_t>(logn, d, ka, ma, s);
+    else
+        dispatch_ks_w<uint64_t>(logn, d, ka, ma, s);
 }
 
 // Key switch `count` polys d (evaluations over Q, stride d_stride, read
@@ -812,7 +883,7 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     const BfvDev& d = st.dev;
     if (d.K == 0) throw std::invalid_argument("key switching needs special primes");
     ensure_key(cx, key_id, s);
-    const ulonglong2* key = key_shoup_ptr(cx, key_id);
+    const void* key = key_shoup_ptr(cx, key_id);
     const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
     DeviceBuffer dc(uint64_t(count) * L * n * 8, s);
     {
@@ -822,7 +893,10 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
         lb.src = d_ntt;
         lb.src_stride = d_stride;
         lb.galois = d_galois;
-        if (d.alpha > 1) lb.last_stage = d.ks_last_q;
+        if (d.alpha > 1) {
+            lb.last_stage = d.ks_last_q;
+            lb.last_stage32 = d.ks_last_q32;
+        }
         cx.ntt_inverse(lb, s);
     }
     DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
@@ -830,11 +904,15 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     dispatch_ks(cx.logn(), d, ka, nullptr, s);
     {
         LimbBatch pb{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n};
-        if (K > 1) pb.last_stage = d.ks_last_p;  // times [(P/p_l)^-1]_{p_l}
+        if (K > 1) {  // times [(P/p_l)^-1]_{p_l}
+            pb.last_stage = d.ks_last_p;
+            pb.last_stage32 = d.ks_last_p32;
+        }
         cx.ntt_inverse(pb, s);
     }
     ModDownArgs ma{acc.get(), add0,  add1,  add_stride, add_galois, sum0,        sum1,
-                   sum_stride, out0, out1,  out_stride, d.p_inv_shoup, count};
+                   sum_stride, out0, out1,  out_stride,
+                   d.ks32 ? static_cast<const void*>(d.p_inv32) : static_cast<const void*>(d.p_inv_shoup), count};
     dispatch_ks(cx.logn(), d, ka, &ma, s);
 }
 
@@ -1002,7 +1080,8 @@ void ct_rotate_add(Context& cx, const uint64_t* base, const uint64_t* x, uint64_
 void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
-    if (d.M < d.L + 1) throw std::invalid_argument("multiplication needs an auxiliary base of at least L+1 primes");
+    if (!cx.bfv()->mul_base_ok)
+        throw std::invalid_argument("multiplication needs an auxiliary base B with log2 B >= log2 Q + log2 t + log2 n + 2");
     const uint32_t n = d.n, L = d.L, M = d.M, LM = L + M;
     const uint64_t LN = uint64_t(L) * n;
     // (a) inputs to coefficients: X[c] = [a0 a1 b0 b1]
@@ -1025,6 +1104,7 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     LimbBatch db{D.get(), count * 3, LM, 0, uint64_t(LM) * n};
     db.prime_map = cx.bfv()->qb_map;
     db.map_period = LM;
+    db.map_small = cx.bfv()->qb_small;
     cx.ntt_inverse(db, s);
     // (f) scale by t/Q into B, (g) exact B -> Q, (h) to evaluations
     DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);

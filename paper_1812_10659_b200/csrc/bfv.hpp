@@ -30,7 +30,8 @@ struct BfvDev {
     const uint64_t* q_mod_t;     // [T] [Q]_{t_j}
     // decryption
     const uint64_t* qhat_inv;    // [L] [(Q/q_i)^-1]_{q_i}
-    const ulonglong2* phi;       // [T][L] floor(t_j 2^128 / q_i)
+    const ulonglong2* phi;       // [T][L] floor([t_j]_{q_i} 2^128 / q_i)
+    const uint64_t* phi_int;     // [T][L] floor(t_j / q_i)
     // exact extension Q -> B
     const ulonglong2* q_frac;    // [L] floor(2^128 / q_i)
     const uint64_t* qhat_mod_b;  // [L][M]
@@ -60,12 +61,22 @@ struct BfvDev {
     const ulonglong2* phat_mod_sh;   // [K][L]
     const ulonglong2* ks_last_q;     // [L][2]
     const ulonglong2* ks_last_p;     // [K][2]
+    // 32-bit copies of the five tables above (companions floor(w 2^32 / r)),
+    // present when every prime of Q and P is below 2^30: the key switch then
+    // runs on 32-bit words (ks32) and keys are stored as uint2 pairs
+    bool ks32;
+    const uint2* p_inv32;            // [L]
+    const uint2* dhat_mod_sh32;      // [L][L+K]
+    const uint2* phat_mod_sh32;      // [K][L]
+    const uint2* ks_last_q32;        // [L][2]
+    const uint2* ks_last_p32;        // [K][2]
 };
 
 // Opaque device handle of a key-switching key.
 struct KsKey {
     DeviceBuffer buf;    // [dnum][2][L+K][n]
-    DeviceBuffer shoup;  // same entries as (value, Shoup companion) pairs
+    DeviceBuffer shoup;  // same entries as (value, Shoup companion) pairs:
+                         // ulonglong2, or uint2 with 32-bit companions (ks32)
 };
 
 struct BfvState {
@@ -74,6 +85,8 @@ struct BfvState {
     // prime maps for LimbBatch (device int16 arrays inside `consts`)
     const int16_t* t_map = nullptr;   // [T]          t_j
     const int16_t* qb_map = nullptr;  // [L+M]        Q then B
+    bool qb_small = false;            // every prime of Q and B is below 2^30
+    bool mul_base_ok = false;         // B large enough for the exact tensor product
     const int16_t* ks_map = nullptr;  // [dnum][L+K]  Q∪P minus digit j's primes
     DeviceBuffer secret;
     std::map<uint64_t, KsKey> keys;  // key id -> key (0 = relinearization)

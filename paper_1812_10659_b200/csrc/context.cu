@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cstdlib>
 
 #include "bfv.hpp"
 #include "context.hpp"
@@ -94,6 +95,30 @@ Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
     }
     LB_CUDA(cudaMemcpyAsync(d_tab, tables.data(), tables.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice,
                             stream_));
+    // 32-bit twiddles for the primes below 2^30
+    {
+        std::vector<uint32_t> small;
+        for (size_t i = 0; i < all_.size(); ++i)
+            if (all_[i] < kWord32Bound) small.push_back(static_cast<uint32_t>(i));
+        if (!small.empty()) {
+            std::vector<uint2> t32(per_prime * small.size());
+            d_tables32_ = DeviceBuffer(t32.size() * sizeof(uint2), stream_);
+            auto* d32 = d_tables32_.get<uint2>();
+            for (size_t j = 0; j < small.size(); ++j) {
+                const uint32_t i = small[j];
+                const uint64_t q = all_[i];
+                const ulonglong2* src = &tables[per_prime * i];
+                for (size_t k = 0; k < per_prime; ++k)
+                    t32[per_prime * j + k] = make_uint2(static_cast<uint32_t>(src[k].x), shoup_companion32(src[k].x, q));
+                PrimeDev& d = devs[i];
+                d.fwd32 = d32 + per_prime * j;
+                d.inv32 = d32 + per_prime * j + n_;
+                d.ninv32 = make_uint2(static_cast<uint32_t>(d.ninv), shoup_companion32(d.ninv, q));
+                d.inv1n32 = make_uint2(static_cast<uint32_t>(d.inv1n), shoup_companion32(d.inv1n, q));
+            }
+            LB_CUDA(cudaMemcpyAsync(d32, t32.data(), t32.size() * sizeof(uint2), cudaMemcpyHostToDevice, stream_));
+        }
+    }
     host_primes_ = devs;
     d_primes_ = DeviceBuffer(devs.size() * sizeof(PrimeDev), stream_);
     LB_CUDA(cudaMemcpyAsync(d_primes_.get(), devs.data(), devs.size() * sizeof(PrimeDev), cudaMemcpyHostToDevice,
@@ -106,6 +131,7 @@ Context::~Context() {
     bfv_.reset();
     d_primes_ = DeviceBuffer();
     d_tables_ = DeviceBuffer();
+    d_tables32_ = DeviceBuffer();
     if (stream_) {
         cudaStreamSynchronize(stream_);
         cudaStreamDestroy(stream_);
@@ -114,7 +140,7 @@ Context::~Context() {
 
 namespace {
 
-template <int LOGN>
+template <int LOGN, class W>
 void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
     using S = NttShape<LOGN>;
     const uint64_t limbs = static_cast<uint64_t>(b.polys) * b.limbs;
@@ -132,20 +158,28 @@ void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (inverse)
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W>, b, primes));
     else
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W>, b, primes));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
+template <class W>
 void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
     switch (logn) {
-        case 12: launch_ntt<12>(b, primes, inverse, s); break;
-        case 13: launch_ntt<13>(b, primes, inverse, s); break;
-        case 14: launch_ntt<14>(b, primes, inverse, s); break;
-        case 15: launch_ntt<15>(b, primes, inverse, s); break;
+        case 12: launch_ntt<12, W>(b, primes, inverse, s); break;
+        case 13: launch_ntt<13, W>(b, primes, inverse, s); break;
+        case 14: launch_ntt<14, W>(b, primes, inverse, s); break;
+        case 15: launch_ntt<15, W>(b, primes, inverse, s); break;
         default: throw std::invalid_argument("unsupported ring degree");
     }
+}
+
+void dispatch_ntt(bool word32, int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+    if (word32)
+        dispatch_ntt<uint32_t>(logn, b, primes, inverse, s);
+    else
+        dispatch_ntt<uint64_t>(logn, b, primes, inverse, s);
 }
 
 void check_batch(const Context& cx, const LimbBatch& b) {
@@ -158,14 +192,31 @@ void check_batch(const Context& cx, const LimbBatch& b) {
 
 }  // namespace
 
+bool Context::word32_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LB_WORD32");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool Context::batch_word32(const LimbBatch& b) const {
+    if (!word32_enabled()) return false;
+    if (b.prime_map) return b.map_small;
+    if (b.last_stage && !b.last_stage32) return false;
+    for (uint32_t l = 0; l < b.limbs; ++l)
+        if (all_[b.first_prime + l] >= kWord32Bound) return false;
+    return true;
+}
+
 void Context::ntt_forward(const LimbBatch& b, cudaStream_t s) const {
     check_batch(*this, b);
-    dispatch_ntt(logn_, b, dev_primes(), false, s);
+    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), false, s);
 }
 
 void Context::ntt_inverse(const LimbBatch& b, cudaStream_t s) const {
     check_batch(*this, b);
-    dispatch_ntt(logn_, b, dev_primes(), true, s);
+    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), true, s);
 }
 
 }  // namespace lb

@@ -122,6 +122,16 @@ public:
 
     // Batched transforms over [polys][limbs][N] with limb l using prime
     // first_prime + l.
+    // true when every prime of the batch is below 2^30 (and LB_WORD32 != 0):
+    // the transform then runs on 32-bit words
+    bool batch_word32(const LimbBatch& b) const;
+    static bool word32_enabled();
+    // every prime of [first, first + count) is below 2^30
+    bool primes_small(uint32_t first, uint32_t count) const {
+        for (uint32_t i = first; i < first + count; ++i)
+            if (all_.at(i) >= kWord32Bound) return false;
+        return true;
+    }
     void ntt_forward(const LimbBatch& b, cudaStream_t s) const;
     void ntt_inverse(const LimbBatch& b, cudaStream_t s) const;
 
@@ -136,6 +146,7 @@ private:
     std::vector<uint64_t> psi_;
     std::vector<Modulus> mods_;
     std::vector<PrimeDev> host_primes_;
+    DeviceBuffer d_tables32_;
     cudaStream_t stream_ = nullptr;
     DeviceBuffer d_tables_;
     DeviceBuffer d_primes_;

@@ -23,32 +23,111 @@ struct KsInnerArgs {
     const uint64_t* dn;      // input evaluations, poly stride d_stride
     uint64_t d_stride;
     uint64_t d_galois;       // automorphism applied to dn reads (0 = none)
-    const ulonglong2* key;   // [dnum][2][L+K][n] (value, Shoup companion)
+    const void* key;         // [dnum][2][L+K][n] (value, Shoup companion): PairT<W>
     uint64_t* acc;           // [count][2][L+K][n] evaluations
     uint32_t count;
 };
 
 // a + b for a, b in [0, 2q) -> [0, 2q)
-__device__ __forceinline__ uint64_t add_lazy2(uint64_t a, uint64_t b, uint64_t two_q) {
-    const uint64_t s = a + b;
+template <class W>
+__device__ __forceinline__ W add_lazy2(W a, W b, W two_q) {
+    const W s = a + b;
     return s >= two_q ? s - two_q : s;
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d, KsInnerArgs a) {
+// Word-specific views of the key-switch constant tables.
+template <class W> struct KsTables;
+template <> struct KsTables<uint64_t> {
+    __device__ static const ulonglong2* dhat(const BfvDev& d) { return d.dhat_mod_sh; }
+    __device__ static const ulonglong2* phat(const BfvDev& d) { return d.phat_mod_sh; }
+};
+template <> struct KsTables<uint32_t> {
+    __device__ static const uint2* dhat(const BfvDev& d) { return d.dhat_mod_sh32; }
+    __device__ static const uint2* phat(const BfvDev& d) { return d.phat_mod_sh32; }
+};
+
+// Fast base conversion of A source limbs (limb stride n) to one target
+// prime: sum_i y_i w_i with Shoup pairs w_i, in [0, 4r). A == 1 passes the
+// raw residue (< 4r: every prime of Q and P is within a factor 4 of every
+// other). A is a compile-time constant so all A loads of an element are
+// independent (a runtime loop serializes them).
+template <int A, int LOGN, class W>
+__device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const uint64_t* __restrict__ src,
+                                           const PairT<W>* w, uint32_t w_stride) {
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    constexpr uint64_t n = 1ull << LOGN;
+    if constexpr (A == 1) {
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return static_cast<W>(__ldg(&src[x])); });
+    } else {
+        PairT<W> ww[A];
+#pragma unroll
+        for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride];
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+            W v[A];
+#pragma unroll
+            for (int i = 0; i < A; ++i) v[i] = static_cast<W>(__ldg(&src[i * n + x]));
+            W acc = shoup_lazy<W>(v[0], ww[0].x, ww[0].y, q) + shoup_lazy<W>(v[1], ww[1].x, ww[1].y, q);
+#pragma unroll
+            for (int i = 2; i < A; ++i) {
+                acc = acc >= two_q ? acc - two_q : acc;
+                acc += shoup_lazy<W>(v[i], ww[i].x, ww[i].y, q);
+            }
+            return acc;
+        });
+    }
+}
+
+template <int LOGN, class W>
+__device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const uint64_t* src, uint32_t A,
+                                         const PairT<W>* w, uint32_t w_stride) {
+    switch (A) {
+        case 1: fwd_conv_n<1, LOGN, W>(sm, P, rank, src, w, w_stride); break;
+        case 2: fwd_conv_n<2, LOGN, W>(sm, P, rank, src, w, w_stride); break;
+        // (64-bit words: unrolling 3 and 4 costs registers the common
+        // K, alpha <= 2 configurations need)
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W>(sm, P, rank, src, w, w_stride); break; }
+        [[fallthrough]];
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W>(sm, P, rank, src, w, w_stride); break; } }
+        [[fallthrough]];
+        default: {
+            const W q = static_cast<W>(P.q), two_q = 2 * q;
+            constexpr uint64_t n = 1ull << LOGN;
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+                W v = 0;
+                for (uint32_t i = 0; i < A; ++i) {
+                    const PairT<W> wi = w[i * w_stride];
+                    v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&src[i * n + x])), wi.x, wi.y, q), two_q);
+                }
+                return v;
+            });
+        }
+    }
+}
+
+#ifndef LB_KS32_MINB
+#define LB_KS32_MINB 3
+#endif
+// 64-bit words: three 32 KiB smem planes per CTA -> 2 CTAs/SM; 32-bit words
+// halve the planes, so registers decide
+template <class W> constexpr int ks_min_blocks() { return sizeof(W) == 8 ? 2 : LB_KS32_MINB; }
+
+template <int LOGN, class W>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inner_kernel(BfvDev d, KsInnerArgs a) {
     using S = NttShape<LOGN>;
-    extern __shared__ __align__(16) uint64_t smem[];
-    uint64_t* sm = smem;
-    uint64_t* acc0 = smem + S::M;
-    uint64_t* acc1 = smem + 2 * S::M;
+    using Pr = PairT<W>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    W* sm = reinterpret_cast<W*>(smem_raw);
+    W* acc0 = sm + S::M;
+    W* acc1 = sm + 2 * S::M;
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
     const uint32_t c = id / LK, r = id % LK;
     const PrimeDev& P = d.primes[r];
-    const uint64_t q = P.q, two_q = 2 * q;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
     const uint32_t cta_base = rank * S::M;
     const uint64_t n = 1ull << LOGN;
+    const Pr* key = static_cast<const Pr*>(a.key);
 #pragma unroll
     for (int jj = 0; jj < kE; ++jj) {
         const uint32_t y = threadIdx.x + jj * S::T;
@@ -59,12 +138,12 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
     // elements; key loads (L2-resident, shared by every ciphertext of the
     // batch) are issued a half at a time ahead of their use.
     auto mac_all = [&](uint32_t j, auto&& value_of) {
-        const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
-        const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
+        const Pr* k0 = key + ((uint64_t(j) * 2 * LK + r) << LOGN);
+        const Pr* k1 = k0 + (uint64_t(LK) << LOGN);
         constexpr int kHalf = 8;  // elements whose key loads are in flight together
 #pragma unroll
         for (int part = 0; part < kE / kHalf; ++part) {
-            ulonglong2 w0[kHalf], w1[kHalf];
+            Pr w0[kHalf], w1[kHalf];
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
                 const uint32_t x = cta_base + threadIdx.x + (part * kHalf + jj) * S::T;
@@ -74,9 +153,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
                 const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
-                const uint64_t v = value_of(y, cta_base + y);
-                acc0[y] = add_lazy2(acc0[y], mul_shoup_lazy(v, w0[jj].x, w0[jj].y, q), two_q);
-                acc1[y] = add_lazy2(acc1[y], mul_shoup_lazy(v, w1[jj].x, w1[jj].y, q), two_q);
+                const W v = value_of(y, cta_base + y);
+                acc0[y] = add_lazy2<W>(acc0[y], shoup_lazy<W>(v, w0[jj].x, w0[jj].y, q), two_q);
+                acc1[y] = add_lazy2<W>(acc1[y], shoup_lazy<W>(v, w1[jj].x, w1[jj].y, q), two_q);
             }
         }
     };
@@ -86,45 +165,24 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, 2) ks_inner_kernel(BfvDev d
             // the digit already lives in this prime: use the input's evaluations
             const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
             mac_all(j, [&](uint32_t, uint32_t x) {
-                return __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
+                return static_cast<W>(__ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]));
             });
             continue;
         }
+        // src limbs hold y_i = [d_i (D_j/q_i)^-1]_{q_i} (a single-prime digit:
+        // d itself); ModUp = sum_i y_i [D_j/q_i]_r computed in the loader
         const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
-        if (hi - lo == 1) {
-            // single-prime digit: the coefficient (< q_lo < 4 q_r) feeds the
-            // lazy transform unreduced
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
-        } else if (hi - lo == 2) {
-            // two-prime digit, fully unrolled so every load of the pass is in
-            // flight at once: y_0 [D/q_0]_r + y_1 [D/q_1]_r in [0, 4r)
-            const ulonglong2 w0 = d.dhat_mod_sh[lo * LK + r], w1 = d.dhat_mod_sh[(lo + 1) * LK + r];
-            const uint64_t* src1 = src + n;
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-                return mul_shoup_lazy(__ldg(&src[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&src1[x]), w1.x, w1.y, q);
-            });
-        } else {
-            // src limbs already hold y_i = [d_i (D_j/q_i)^-1]_{q_i}; fast base
-            // conversion sum_i y_i [D_j/q_i]_r, kept lazily in [0, 2r)
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-                uint64_t v = 0;
-                for (uint32_t i = lo; i < hi; ++i) {
-                    const ulonglong2 w = d.dhat_mod_sh[i * LK + r];
-                    v = add_lazy2(v, mul_shoup_lazy(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), w.x, w.y, q), two_q);
-                }
-                return v;
-            });
-        }
-        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q(sm[swz(y)], q, two_q); });
+        fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK);
+        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm[swz(y)], q, two_q); });
     }
     uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     uint64_t* out1 = out0 + uint64_t(LK) * n;
 #pragma unroll
     for (int jj = 0; jj < kE; ++jj) {
         const uint32_t y = threadIdx.x + jj * S::T;
-        const uint64_t v0 = acc0[y], v1 = acc1[y];
-        out0[y] = v0 >= q ? v0 - q : v0;
-        out1[y] = v1 >= q ? v1 - q : v1;
+        const W v0 = acc0[y], v1 = acc1[y];
+        out0[y] = static_cast<uint64_t>(v0 >= q ? v0 - q : v0);
+        out1[y] = static_cast<uint64_t>(v1 >= q ? v1 - q : v1);
     }
     // no trailing cluster barrier: the last remote access to this CTA's smem
     // (a scatter) is ordered before the cluster sync inside fwd_core
@@ -209,7 +267,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
     // acc_h[e] += v_e * key_j[h][r][x_e] for the thread's 16 elements, two
     // at a time: columns [4e, 4e+4) of the thread's block = (acc0, acc1) words
     auto mac_all = [&](uint32_t j, bool first, auto&& value_of) {
-        const ulonglong2* k0 = a.key + ((uint64_t(j) * 2 * LK + r) << LOGN);
+        const ulonglong2* k0 = static_cast<const ulonglong2*>(a.key) + ((uint64_t(j) * 2 * LK + r) << LOGN);
         const ulonglong2* k1 = k0 + (uint64_t(LK) << LOGN);
 #pragma unroll 2
         for (int pair = 0; pair < kE / 2; ++pair) {
@@ -252,27 +310,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
             continue;
         }
         const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
-        if (hi - lo == 1) {
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&src[x]); });
-        } else if (hi - lo == 2) {
-            // two-prime digit, fully unrolled so every load of the pass is in
-            // flight at once: y_0 [D/q_0]_r + y_1 [D/q_1]_r in [0, 4r)
-            const ulonglong2 w0 = d.dhat_mod_sh[lo * LK + r], w1 = d.dhat_mod_sh[(lo + 1) * LK + r];
-            const uint64_t* src1 = src + n;
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-                return mul_shoup_lazy(__ldg(&src[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&src1[x]), w1.x, w1.y, q);
-            });
-        } else {
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-                uint64_t v = 0;
-                for (uint32_t i = lo; i < hi; ++i) {
-                    const ulonglong2 w = d.dhat_mod_sh[i * LK + r];
-                    v = add_lazy2(v, mul_shoup_lazy(__ldg(&src[(uint64_t(i - lo) << LOGN) + x]), w.x, w.y, q), two_q);
-                }
-                return v;
-            });
-        }
-        mac_all(j, first, [&](uint32_t y, uint32_t) { return reduce_4q(sm[swz(y)], q, two_q); });
+        fwd_conv<LOGN, uint64_t>(sm, P, rank, src, hi - lo, d.dhat_mod_sh + lo * LK + r, LK);
+        mac_all(j, first, [&](uint32_t y, uint32_t) { return reduce_4q<uint64_t>(sm[swz(y)], q, two_q); });
     }
     uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     uint64_t* out1 = out0 + uint64_t(LK) * n;
@@ -306,43 +345,26 @@ struct ModDownArgs {
     uint64_t* out0;
     uint64_t* out1;
     uint64_t out_stride;
-    const ulonglong2* p_inv;  // [L] (P^-1 mod q_r, Shoup)
+    const void* p_inv;        // [L] (P^-1 mod q_r, Shoup): PairT<W>
     uint32_t count;
 };
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(BfvDev d, ModDownArgs a) {
+template <int LOGN, class W>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
-    __shared__ __align__(16) uint64_t sm[S::M];
+    __shared__ __align__(16) W sm[S::M];
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
     const uint32_t r = id % d.L, h = (id / d.L) & 1, c = id / (2 * d.L);
     const PrimeDev& P = d.primes[r];
-    const uint64_t q = P.q, two_q = 2 * q;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
     const uint64_t n = 1ull << LOGN;
     const uint64_t* accp = a.acc + ((uint64_t(c) * 2 + h) * LK + d.L) * n;
-    if (d.K == 1) {
-        // [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldg(&accp[x]); });
-    } else if (d.K == 2) {
-        const ulonglong2 w0 = d.phat_mod_sh[r], w1 = d.phat_mod_sh[d.L + r];
-        const uint64_t* accp1 = accp + n;
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-            return mul_shoup_lazy(__ldg(&accp[x]), w0.x, w0.y, q) + mul_shoup_lazy(__ldg(&accp1[x]), w1.x, w1.y, q);
-        });
-    } else {
-        // P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded into the
-        // inverse transform); sum_l y_l [P/p_l]_{q_r}, lazily in [0, 2q)
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
-            uint64_t v = 0;
-            for (uint32_t l = 0; l < d.K; ++l) {
-                const ulonglong2 w = d.phat_mod_sh[l * d.L + r];
-                v = add_lazy2(v, mul_shoup_lazy(__ldg(&accp[(uint64_t(l) << LOGN) + x]), w.x, w.y, q), two_q);
-            }
-            return v;
-        });
-    }
+    // K == 1: [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced;
+    // else the P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded
+    // into the inverse transform) and the loader forms sum_l y_l [P/p_l]_{q_r}
+    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L);
     const uint32_t cta_base = rank * S::M;
     const uint64_t* accq = a.acc + ((uint64_t(c) * 2 + h) * LK + r) * n;
     const uint64_t* add = h ? a.add1 : a.add0;
@@ -350,29 +372,31 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) moddown_kernel(
     const uint64_t* sum = h ? a.sum1 : a.sum0;
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
-    const ulonglong2 pinv = a.p_inv[r];
+    const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
     // any of them, so their latencies overlap.
     constexpr int kHalf = 8;
 #pragma unroll
     for (int part = 0; part < kE / kHalf; ++part) {
-        uint64_t va[kHalf], vb[kHalf], vs[kHalf];
+        W va[kHalf], vb[kHalf], vs[kHalf];
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t x = cta_base + threadIdx.x + (part * kHalf + jj) * S::T;
-            va[jj] = __ldg(&accq[x]);
-            vb[jj] = add ? __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]) : 0;
-            vs[jj] = sum ? __ldg(&sum[x]) : 0;
+            va[jj] = static_cast<W>(__ldg(&accq[x]));
+            vb[jj] = add ? static_cast<W>(__ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x])) : 0;
+            vs[jj] = sum ? static_cast<W>(__ldg(&sum[x])) : 0;
         }
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
-            const uint64_t conv = reduce_4q(sm[swz(y)], q, two_q);
-            uint64_t u = mul_shoup(va[jj] + q - conv, pinv.x, pinv.y, q);
-            u = add_mod(u, vb[jj], q);
-            u = add_mod(u, vs[jj], q);
-            out[cta_base + y] = u;
+            const W conv = reduce_4q<W>(sm[swz(y)], q, two_q);
+            W u = shoup_full<W>(va[jj] + q - conv, pinv.x, pinv.y, q);
+            u += vb[jj];
+            u = u >= q ? u - q : u;
+            u += vs[jj];
+            u = u >= q ? u - q : u;
+            out[cta_base + y] = static_cast<uint64_t>(u);
         }
     }
 }

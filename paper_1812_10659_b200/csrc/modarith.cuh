@@ -58,6 +58,12 @@ inline uint64_t shoup_companion(uint64_t w, uint64_t q) {
     return static_cast<uint64_t>((static_cast<unsigned __int128>(w) << 64) / q);
 }
 
+// 32-bit Shoup companion floor(w * 2^32 / q) for w < q < 2^30 (host side).
+inline uint32_t shoup_companion32(uint64_t w, uint64_t q) { return static_cast<uint32_t>((w << 32) / q); }
+
+// Primes below this bound are transformed with 32-bit words (4q < 2^32).
+constexpr uint64_t kWord32Bound = uint64_t{1} << 30;
+
 // x * w mod q, result in [0, 2q); any 64-bit x.
 LB_HD uint64_t mul_shoup_lazy(uint64_t x, uint64_t w, uint64_t wp, uint64_t q) {
     uint64_t hi = mulhi64(x, wp);

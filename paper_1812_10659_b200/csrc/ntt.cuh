@@ -42,7 +42,50 @@ struct PrimeDev {
     const ulonglong2* inv;
     uint64_t ninv, ninv_shoup;
     uint64_t inv1n, inv1n_shoup;  // psi^-bitrev(1) * n^-1
+    // 32-bit copies for primes below 2^30 (NULL otherwise): Shoup companions
+    // floor(w * 2^32 / q), used by the 32-bit word kernels
+    const uint2* fwd32;
+    const uint2* inv32;
+    uint2 ninv32, inv1n32;
 };
+
+// Arithmetic word of a kernel instance. Residues are stored as u64 in HBM
+// either way; a batch whose primes are all below 2^30 is transformed with
+// 32-bit words (values < 4q < 2^32, one IMAD.HI + two IMADs per Shoup
+// product instead of the ~14-instruction 64-bit emulation).
+template <class W> struct WordT;
+template <> struct WordT<uint64_t> { using Pair = ulonglong2; };
+template <> struct WordT<uint32_t> { using Pair = uint2; };
+template <class W> using PairT = typename WordT<W>::Pair;
+
+__device__ __forceinline__ uint32_t mulhi_w(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+__device__ __forceinline__ uint64_t mulhi_w(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// x * w mod q in [0, 2q) for any word x (Shoup, companion wp).
+template <class W>
+__device__ __forceinline__ W shoup_lazy(W x, W w, W wp, W q) { return x * w - mulhi_w(x, wp) * q; }
+template <class W>
+__device__ __forceinline__ W shoup_full(W x, W w, W wp, W q) {
+    const W r = shoup_lazy(x, w, wp, q);
+    return r >= q ? r - q : r;
+}
+
+template <class W> __device__ __forceinline__ const PairT<W>* fwd_table(const PrimeDev& P);
+template <> __device__ __forceinline__ const ulonglong2* fwd_table<uint64_t>(const PrimeDev& P) { return P.fwd; }
+template <> __device__ __forceinline__ const uint2* fwd_table<uint32_t>(const PrimeDev& P) { return P.fwd32; }
+template <class W> __device__ __forceinline__ const PairT<W>* inv_table(const PrimeDev& P);
+template <> __device__ __forceinline__ const ulonglong2* inv_table<uint64_t>(const PrimeDev& P) { return P.inv; }
+template <> __device__ __forceinline__ const uint2* inv_table<uint32_t>(const PrimeDev& P) { return P.inv32; }
+template <class W> __device__ __forceinline__ PairT<W> ninv_pair(const PrimeDev& P);
+template <> __device__ __forceinline__ ulonglong2 ninv_pair<uint64_t>(const PrimeDev& P) {
+    return make_ulonglong2(P.ninv, P.ninv_shoup);
+}
+template <> __device__ __forceinline__ uint2 ninv_pair<uint32_t>(const PrimeDev& P) { return P.ninv32; }
+template <class W> __device__ __forceinline__ PairT<W> inv1n_pair(const PrimeDev& P);
+template <> __device__ __forceinline__ ulonglong2 inv1n_pair<uint64_t>(const PrimeDev& P) {
+    return make_ulonglong2(P.inv1n, P.inv1n_shoup);
+}
+template <> __device__ __forceinline__ uint2 inv1n_pair<uint32_t>(const PrimeDev& P) { return P.inv1n32; }
 
 // Descriptor of a batch of RNS polynomials laid out [poly][limb][N]:
 // limb l of every poly uses prime first_prime + l.
@@ -66,8 +109,13 @@ struct LimbBatch {
     uint64_t galois = 0;
     // inverse transform only: per limb position l (< limbs), the final-stage
     // constants {n^-1 * s_l, psi^-bitrev(1) * n^-1 * s_l} as (value, Shoup)
-    // pairs, which scale the output by s_l for free (NULL = s_l = 1).
+    // pairs, which scale the output by s_l for free (NULL = s_l = 1);
+    // last_stage32 is the same for the 32-bit word path.
     const ulonglong2* last_stage = nullptr;
+    const uint2* last_stage32 = nullptr;
+    // prime_map batches only: every mapped prime is below 2^30 (the caller
+    // knows; contiguous batches are checked on the host)
+    bool map_small = false;
 };
 
 // Evaluation-domain source position of x under x -> x^g (bit-reversed order).
@@ -90,32 +138,35 @@ constexpr int kMinBlocks = kThreads == 128 ? 4 : 3;  // resident CTAs per SM the
 __device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
 
 // Harvey lazy CT butterfly: X, Y in [0, 4q) -> X + WY, X - WY in [0, 4q).
-__device__ __forceinline__ void ct_bfly(uint64_t& x, uint64_t& y, ulonglong2 w, uint64_t q, uint64_t two_q) {
-    uint64_t xx = x >= two_q ? x - two_q : x;
-    uint64_t t = mul_shoup_lazy(y, w.x, w.y, q);
+template <class W, class Pr>
+__device__ __forceinline__ void ct_bfly(W& x, W& y, Pr w, W q, W two_q) {
+    W xx = x >= two_q ? x - two_q : x;
+    W t = shoup_lazy<W>(y, w.x, w.y, q);
     x = xx + t;
     y = xx - t + two_q;
 }
 
 // Harvey lazy GS butterfly: X, Y in [0, 2q) -> X + Y, (X - Y) W in [0, 2q).
-__device__ __forceinline__ void gs_bfly(uint64_t& x, uint64_t& y, ulonglong2 w, uint64_t q, uint64_t two_q) {
-    uint64_t s = x + y;
+template <class W, class Pr>
+__device__ __forceinline__ void gs_bfly(W& x, W& y, Pr w, W q, W two_q) {
+    W s = x + y;
     s = s >= two_q ? s - two_q : s;
-    uint64_t d = x - y + two_q;
+    W d = x - y + two_q;
     x = s;
-    y = mul_shoup_lazy(d, w.x, w.y, q);
+    y = shoup_lazy<W>(d, w.x, w.y, q);
 }
 
-__device__ __forceinline__ uint64_t reduce_4q(uint64_t v, uint64_t q, uint64_t two_q) {
+template <class W>
+__device__ __forceinline__ W reduce_4q(W v, W q, W two_q) {
     v = v >= two_q ? v - two_q : v;
     return v >= q ? v - q : v;
 }
 
 // Forward radix-2^C pass over one group held in r[0..2^C): global stages
 // s0 .. s0+C-1, B = global block index at stage s0.
-template <int C>
-__device__ __forceinline__ void fwd_group(uint64_t* r, const ulonglong2* __restrict__ tw, uint32_t s0, uint32_t B,
-                                          uint64_t q, uint64_t two_q) {
+template <int C, class W>
+__device__ __forceinline__ void fwd_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                          W two_q) {
 #pragma unroll
     for (int l = 0; l < C; ++l) {
         const int half = 1 << (C - 1 - l);
@@ -129,9 +180,9 @@ __device__ __forceinline__ void fwd_group(uint64_t* r, const ulonglong2* __restr
 }
 
 // Inverse pass over one group: stages s0+C-1 down to s0.
-template <int C>
-__device__ __forceinline__ void inv_group(uint64_t* r, const ulonglong2* __restrict__ tw, uint32_t s0, uint32_t B,
-                                          uint64_t q, uint64_t two_q) {
+template <int C, class W>
+__device__ __forceinline__ void inv_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                          W two_q) {
 #pragma unroll
     for (int l = C - 1; l >= 0; --l) {
         const int half = 1 << (C - 1 - l);
@@ -146,9 +197,9 @@ __device__ __forceinline__ void inv_group(uint64_t* r, const ulonglong2* __restr
 
 // One local radix-2^C pass over the CTA's smem chunk (global stages
 // s0..s0+C-1; every block at stage s0 lies inside one CTA).
-template <int LOGN, int C, bool INVERSE>
-__device__ __forceinline__ void local_pass(uint64_t* sm, const ulonglong2* __restrict__ tw, uint32_t s0,
-                                           uint32_t cta_base, uint64_t q, uint64_t two_q) {
+template <int LOGN, int C, bool INVERSE, class W>
+__device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t cta_base,
+                                           W q, W two_q) {
     constexpr int G = kE >> C;  // groups per thread
     const uint32_t stride = (1u << LOGN) >> (s0 + C);
     const uint32_t log_bs = LOGN - s0;
@@ -158,7 +209,7 @@ __device__ __forceinline__ void local_pass(uint64_t* sm, const ulonglong2* __res
         const uint32_t b = g / stride, o = g % stride;
         const uint32_t base = (b << log_bs) + o;
         const uint32_t B = (cta_base >> log_bs) + b;
-        uint64_t r[1 << C];
+        W r[1 << C];
 #pragma unroll
         for (int k = 0; k < (1 << C); ++k) r[k] = sm[swz(base + k * stride)];
         if (INVERSE)
@@ -171,14 +222,14 @@ __device__ __forceinline__ void local_pass(uint64_t* sm, const ulonglong2* __res
 }
 
 // local pass of C stages, C chosen at run time among 1..kLogE
-template <int LOGN, bool INVERSE, int C = kLogE>
-__device__ __forceinline__ void local_pass_n(int c, uint64_t* sm, const ulonglong2* __restrict__ tw, uint32_t s0,
-                                             uint32_t cta_base, uint64_t q, uint64_t two_q) {
+template <int LOGN, bool INVERSE, int C = kLogE, class W>
+__device__ __forceinline__ void local_pass_n(int c, W* sm, const PairT<W>* __restrict__ tw, uint32_t s0,
+                                             uint32_t cta_base, W q, W two_q) {
     if constexpr (C >= 1) {
         if (c == C)
             local_pass<LOGN, C, INVERSE>(sm, tw, s0, cta_base, q, two_q);
         else
-            local_pass_n<LOGN, INVERSE, C - 1>(c, sm, tw, s0, cta_base, q, two_q);
+            local_pass_n<LOGN, INVERSE, C - 1, W>(c, sm, tw, s0, cta_base, q, two_q);
     }
 }
 
@@ -213,20 +264,20 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // evaluations sits in `sm` (swizzled, values in [0, 4q)).
 // Callers looping over several transforms must cluster-sync between them
 // (peers scatter into this CTA's smem).
-template <int LOGN, class Load>
-__device__ __forceinline__ void fwd_core(uint64_t* sm, const PrimeDev& P, uint32_t rank, Load&& load) {
+template <int LOGN, class W, class Load>
+__device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
-    const uint64_t q = P.q, two_q = 2 * q;
-    const ulonglong2* __restrict__ tw = P.fwd;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = fwd_table<W>(P);
     // Every CTA of the cluster must be running (and done reading its smem)
     // before peers write into it: arrive now, wait before the remote stores.
     if constexpr (S::CL > 1) cluster_arrive();
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
-        uint64_t r[kE];
+        W r[kE];
 #pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = load(rho + k * S::NE);
+        for (int k = 0; k < kE; ++k) r[k] = static_cast<W>(load(rho + k * S::NE));
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
         if constexpr (S::CL > 1) cluster_wait();
         else __syncthreads();
@@ -235,7 +286,7 @@ __device__ __forceinline__ void fwd_core(uint64_t* sm, const PrimeDev& P, uint32
             const uint32_t dst = k / S::PER_CTA;
             const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
             if constexpr (S::CL > 1) {
-                uint64_t* remote = cg::this_cluster().map_shared_rank(sm, dst);
+                W* remote = cg::this_cluster().map_shared_rank(sm, dst);
                 remote[swz(y)] = r[k];
             } else {
                 sm[swz(y)] = r[k];
@@ -260,40 +311,45 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 }
 
 // grid.x = CL * (polys * limbs); cluster dims (CL, 1, 1).
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+#ifndef LB_NTT32_MINB
+#define LB_NTT32_MINB 4
+#endif
+template <class W> constexpr int ntt_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_NTT32_MINB; }
+
+template <int LOGN, class W>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
     using S = NttShape<LOGN>;
-    __shared__ __align__(16) uint64_t sm[S::M];
+    __shared__ __align__(16) W sm[S::M];
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t limb_id = blockIdx.x / S::CL;
     const int pidx = prime_index(b, limb_id);
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
     uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
-    fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return __ldcs(&a[x]); });
+    fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return static_cast<W>(__ldcs(&a[x])); });
     // Coalesced store of the CTA's chunk, fully reduced.
-    const uint64_t q = P.q, two_q = 2 * q;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
     uint64_t* out = a + rank * S::M;
 #pragma unroll
     for (int j = 0; j < kE; ++j) {
         const uint32_t y = threadIdx.x + j * S::T;
-        __stcs(&out[y], reduce_4q(sm[swz(y)], q, two_q));
+        __stcs(&out[y], static_cast<uint64_t>(reduce_4q<W>(sm[swz(y)], q, two_q)));
     }
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+template <int LOGN, class W>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
-    __shared__ __align__(16) uint64_t sm[S::M];
+    __shared__ __align__(16) W sm[S::M];
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t limb_id = blockIdx.x / S::CL;
     const int pidx = prime_index(b, limb_id);
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
-    const uint64_t q = P.q, two_q = 2 * q;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
     uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
-    const ulonglong2* __restrict__ tw = P.inv;
+    const PairT<W>* __restrict__ tw = inv_table<W>(P);
     const uint32_t cta_base = rank * S::M;
 
     if (b.src) {
@@ -303,26 +359,26 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
             const uint32_t x = cta_base + y;
-            sm[swz(y)] = __ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]);
+            sm[swz(y)] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
         }
     } else {
         const uint64_t* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
-            sm[swz(y)] = __ldcs(&in[y]);
+            sm[swz(y)] = static_cast<W>(__ldcs(&in[y]));
         }
     }
     __syncthreads();
     // Local passes in reverse: the last (possibly short) chunk first.
     constexpr int kTail = (LOGN - kLogE) % kLogE;
     if constexpr (kTail > 0) {
-        local_pass<LOGN, kTail, true>(sm, tw, LOGN - kTail, cta_base, q, two_q);
+        local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
         __syncthreads();
     }
 #pragma unroll
     for (int s0 = LOGN - kTail - kLogE; s0 >= kLogE; s0 -= kLogE) {
-        local_pass<LOGN, kLogE, true>(sm, tw, s0, cta_base, q, two_q);
+        local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
     if constexpr (S::CL > 1) cg::this_cluster().sync();
@@ -330,13 +386,13 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
     // Cross-CTA pass: stages 3..0 gathered from the owners, n^-1 folded in.
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
-        uint64_t r[kE];
+        W r[kE];
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
             const uint32_t src = k / S::PER_CTA;
             const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
             if constexpr (S::CL > 1) {
-                const uint64_t* remote = cg::this_cluster().map_shared_rank(sm, src);
+                const W* remote = cg::this_cluster().map_shared_rank(sm, src);
                 r[k] = remote[swz(y)];
             } else {
                 r[k] = sm[swz(y)];
@@ -354,22 +410,27 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, kMinBlocks) ntt_inverse_ker
             }
         }
         constexpr int half0 = kE / 2;
-        ulonglong2 c0 = make_ulonglong2(P.ninv, P.ninv_shoup), c1 = make_ulonglong2(P.inv1n, P.inv1n_shoup);
-        if (b.last_stage) {
+        PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
+        const PairT<W>* last = nullptr;
+        if constexpr (sizeof(W) == 8)
+            last = b.last_stage;
+        else
+            last = b.last_stage32;
+        if (last) {
             const uint32_t l = limb_id % b.limbs;
-            c0 = b.last_stage[2 * l];
-            c1 = b.last_stage[2 * l + 1];
+            c0 = last[2 * l];
+            c1 = last[2 * l + 1];
         }
 #pragma unroll
         for (int k = 0; k < half0; ++k) {
-            uint64_t x = r[k], y = r[k + half0];
-            uint64_t s = x + y;  // < 4q
-            uint64_t d = x - y + two_q;
-            r[k] = mul_shoup(s, c0.x, c0.y, q);
-            r[k + half0] = mul_shoup(d, c1.x, c1.y, q);
+            W x = r[k], y = r[k + half0];
+            W s = x + y;  // < 4q
+            W d = x - y + two_q;
+            r[k] = shoup_full<W>(s, c0.x, c0.y, q);
+            r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
         }
 #pragma unroll
-        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], r[k]);
+        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<uint64_t>(r[k]));
     }
     if constexpr (S::CL > 1) cg::this_cluster().sync();  // keep smem alive for peers
 }

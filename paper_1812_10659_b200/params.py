@@ -59,10 +59,14 @@ def make_params(n: int, L: int, T: int = 1, K: int = 1, dnum: int = 0, bits: int
                 plain: list[int] | None = None) -> BfvParams:
     """Ciphertext primes: the L largest `bits`-bit primes == 1 mod 2^16 (so
     one chain serves every n <= 32768); special primes and the auxiliary
-    base (L + 1 primes, needed for the exact tensor product) are the next
-    ones down, all distinct."""
+    base B are the next ones down, all distinct. B must hold round(t D / Q)
+    for the tensor D (|D| < n Q^2 / 4): log2 B >= log2 Q + log2 t + log2 n + 2,
+    i.e. L + 1 primes of 60 bits or L + 2 of 30 bits."""
+    import math
+
     log_mod = 16
-    allp = find_primes(bits, log_mod, L + K + L + 1)
+    extra = max(1, math.ceil((32 + math.log2(n) + 3) / (bits - 1)))
+    allp = find_primes(bits, log_mod, L + K + L + extra)
     q, p, b = allp[:L], allp[L:L + K], allp[L + K:]
     t = plain if plain is not None else plain_primes(n, T)
     return BfvParams(n=n, q=q, p=p, b=b, t=t, dnum=dnum or L, seed=seed)
@@ -79,6 +83,14 @@ def lola_mnist_params(seed: int = 1) -> BfvParams:
     limb transforms per key switch (vs 42 with K = 1, dnum = 5), measured
     84 vs 76 images/s on B200."""
     return make_params(16384, L=5, T=5, K=2, dnum=3, seed=seed)
+
+
+def lola_mnist_params_w32(seed: int = 1) -> BfvParams:
+    """Config 0/2 on 30-bit primes (below 2^30, so every transform and key
+    switch runs on 32-bit words): L = 10 ciphertext primes (Q ~ 300 bits, as
+    the 60-bit chain), K = 4 special primes, dnum = 3 digits of <= 4 primes:
+    log2(QP) ~ 420 <= 438."""
+    return make_params(16384, L=10, T=5, K=4, dnum=3, bits=30, seed=seed)
 
 
 def lola_cifar_params(seed: int = 1) -> BfvParams:

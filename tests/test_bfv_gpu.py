@@ -15,11 +15,15 @@ from paper_1812_10659_b200.params import make_params
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[(4096, 3, 2, 1, 0), (8192, 4, 1, 1, 0), (4096, 5, 2, 2, 3)],
-                ids=["n4096_L3_T2", "n8192_L4_T1", "n4096_L5_K2_dnum3"])
+# 60-bit primes run the 64-bit word kernels; 30-bit primes (< 2^30) the
+# 32-bit word NTT / key-switch kernels, with 1-, 3- and 4-prime digits.
+@pytest.fixture(scope="module", params=[(4096, 3, 2, 1, 0, 60), (8192, 4, 1, 1, 0, 60), (4096, 5, 2, 2, 3, 60),
+                                        (4096, 6, 2, 3, 2, 30), (8192, 10, 2, 4, 3, 30), (4096, 4, 1, 1, 4, 30)],
+                ids=["n4096_L3_T2", "n8192_L4_T1", "n4096_L5_K2_dnum3", "w32_n4096_L6_K3_dnum2",
+                     "w32_n8192_L10_K4_dnum3", "w32_n4096_L4_K1"])
 def env(request):
-    n, L, T, K, dnum = request.param
-    prm = make_params(n, L=L, T=T, K=K, dnum=dnum, seed=11)
+    n, L, T, K, dnum, bits = request.param
+    prm = make_params(n, L=L, T=T, K=K, dnum=dnum, bits=bits, seed=11)
     cx = BfvContext(prm)
     o = Oracle.from_params(prm)
     return prm, cx, o

@@ -47,6 +47,13 @@ def test_lola_mnist_config0():
     _check(lola_mnist_params(), nets.lola_mnist_net(), "lola-mnist", batch=2, config=0)
 
 
+def test_lola_mnist_config0_word32():
+    """The same network on 30-bit RNS primes (32-bit word kernels)."""
+    from paper_1812_10659_b200.params import lola_mnist_params_w32
+
+    _check(lola_mnist_params_w32(), nets.lola_mnist_net(), "lola-mnist", batch=2, config=0)
+
+
 def test_lola_cifar_config4_single_image():
     """BASELINE config 4 (83 + 163 maps, 57,252 rotations per instance, 6
     plaintext primes): decrypted logits == forward_integer; per-step counters

@@ -18,6 +18,8 @@ from paper_1812_10659_b200.params import make_params
 pytestmark = pytest.mark.gpu
 
 SWEEP = [(4096, 2), (4096, 12), (8192, 8), (16384, 4), (16384, 12), (32768, 2), (32768, 8)]
+# 30-bit primes: the 32-bit word transforms
+SWEEP32 = [(4096, 12), (16384, 14), (32768, 6)]
 
 
 def coeffs(cx, ct):
@@ -42,6 +44,26 @@ def test_ntt_every_limb_matches_reference(n, L):
     br = bitrev_perm(n)
     for i, p in enumerate(primes):
         assert np.array_equal(got[1, i][br], R.ntt_forward(p, data[1, i])), f"limb {i} (p={p})"
+    cx.ntt_inverse(dev, limbs=len(primes))
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy().astype(np.uint64), data)
+
+
+@pytest.mark.parametrize("n,L", SWEEP32, ids=[f"w32_n{n}_L{L}" for n, L in SWEEP32])
+def test_ntt_word32_matches_reference(n, L):
+    prm = make_params(n, L=L, T=1, K=1, bits=30, seed=n + L)
+    cx = BfvContext(prm)
+    primes = cx.primes
+    assert all(p < 1 << 30 for p in primes[:L])
+    rng = np.random.default_rng(n * 37 + L)
+    data = np.stack([np.stack([rng.integers(0, p, n, dtype=np.uint64) for p in primes]) for _ in range(2)])
+    dev = torch.from_numpy(data.astype(np.int64)).cuda()
+    cx.ntt_forward(dev, limbs=len(primes))
+    torch.cuda.synchronize()
+    got = dev.cpu().numpy().astype(np.uint64)
+    br = bitrev_perm(n)
+    for i, p in enumerate(primes):
+        assert np.array_equal(got[0, i][br], R.ntt_forward(p, data[0, i])), f"limb {i} (p={p})"
     cx.ntt_inverse(dev, limbs=len(primes))
     torch.cuda.synchronize()
     assert np.array_equal(dev.cpu().numpy().astype(np.uint64), data)
