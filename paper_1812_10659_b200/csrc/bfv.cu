@@ -885,7 +885,9 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     ensure_key(cx, key_id, s);
     const void* key = key_shoup_ptr(cx, key_id);
     const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
-    DeviceBuffer dc(uint64_t(count) * L * n * 8, s);
+    // intermediates in the kernels' word size (u32 when ks32)
+    const size_t wb = d.ks32 ? 4 : 8;
+    DeviceBuffer dc(uint64_t(count) * L * n * wb, s);
     {
         // coefficients of d, pre-multiplied by [(D_j/q_i)^-1]_{q_i} for
         // multi-prime digits (folded into the transform's n^-1)
@@ -893,17 +895,20 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
         lb.src = d_ntt;
         lb.src_stride = d_stride;
         lb.galois = d_galois;
+        lb.packed32 = d.ks32;
         if (d.alpha > 1) {
             lb.last_stage = d.ks_last_q;
             lb.last_stage32 = d.ks_last_q32;
         }
         cx.ntt_inverse(lb, s);
     }
-    DeviceBuffer acc(uint64_t(count) * 2 * LK * n * 8, s);
+    DeviceBuffer acc(uint64_t(count) * 2 * LK * n * wb, s);
     KsInnerArgs ka{dc.get(), d_ntt, d_stride, d_galois, key, acc.get(), count};
     dispatch_ks(cx.logn(), d, ka, nullptr, s);
     {
-        LimbBatch pb{acc.get() + uint64_t(L) * n, count * 2, K, L, uint64_t(LK) * n};
+        uint8_t* p_limbs = acc.get<uint8_t>() + uint64_t(L) * n * wb;
+        LimbBatch pb{reinterpret_cast<uint64_t*>(p_limbs), count * 2, K, L, uint64_t(LK) * n};
+        pb.packed32 = d.ks32;
         if (K > 1) {  // times [(P/p_l)^-1]_{p_l}
             pb.last_stage = d.ks_last_p;
             pb.last_stage32 = d.ks_last_p32;

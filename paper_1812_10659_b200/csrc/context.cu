@@ -140,7 +140,7 @@ Context::~Context() {
 
 namespace {
 
-template <int LOGN, class W>
+template <int LOGN, class W, class St>
 void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
     using S = NttShape<LOGN>;
     const uint64_t limbs = static_cast<uint64_t>(b.polys) * b.limbs;
@@ -158,28 +158,32 @@ void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (inverse)
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W, St>, b, primes));
     else
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W, St>, b, primes));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
-template <class W>
+template <class W, class St>
 void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
     switch (logn) {
-        case 12: launch_ntt<12, W>(b, primes, inverse, s); break;
-        case 13: launch_ntt<13, W>(b, primes, inverse, s); break;
-        case 14: launch_ntt<14, W>(b, primes, inverse, s); break;
-        case 15: launch_ntt<15, W>(b, primes, inverse, s); break;
+        case 12: launch_ntt<12, W, St>(b, primes, inverse, s); break;
+        case 13: launch_ntt<13, W, St>(b, primes, inverse, s); break;
+        case 14: launch_ntt<14, W, St>(b, primes, inverse, s); break;
+        case 15: launch_ntt<15, W, St>(b, primes, inverse, s); break;
         default: throw std::invalid_argument("unsupported ring degree");
     }
 }
 
 void dispatch_ntt(bool word32, int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
-    if (word32)
-        dispatch_ntt<uint32_t>(logn, b, primes, inverse, s);
-    else
-        dispatch_ntt<uint64_t>(logn, b, primes, inverse, s);
+    if (b.packed32) {
+        if (!word32) throw std::invalid_argument("packed 32-bit limbs need primes below 2^30");
+        dispatch_ntt<uint32_t, uint32_t>(logn, b, primes, inverse, s);
+    } else if (word32) {
+        dispatch_ntt<uint32_t, uint64_t>(logn, b, primes, inverse, s);
+    } else {
+        dispatch_ntt<uint64_t, uint64_t>(logn, b, primes, inverse, s);
+    }
 }
 
 void check_batch(const Context& cx, const LimbBatch& b) {

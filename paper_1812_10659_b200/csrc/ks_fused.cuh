@@ -19,12 +19,12 @@
 namespace lb {
 
 struct KsInnerArgs {
-    const uint64_t* dc;      // [count][L][n] coefficients of the input
+    const void* dc;          // [count][L][n] coefficients of the input (word-sized: u64 or u32)
     const uint64_t* dn;      // input evaluations, poly stride d_stride
     uint64_t d_stride;
     uint64_t d_galois;       // automorphism applied to dn reads (0 = none)
     const void* key;         // [dnum][2][L+K][n] (value, Shoup companion): PairT<W>
-    uint64_t* acc;           // [count][2][L+K][n] evaluations
+    void* acc;               // [count][2][L+K][n] evaluations (word-sized)
     uint32_t count;
 };
 
@@ -51,8 +51,8 @@ template <> struct KsTables<uint32_t> {
 // raw residue (< 4r: every prime of Q and P is within a factor 4 of every
 // other). A is a compile-time constant so all A loads of an element are
 // independent (a runtime loop serializes them).
-template <int A, int LOGN, class W>
-__device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const uint64_t* __restrict__ src,
+template <int A, int LOGN, class W, class St>
+__device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
                                            const PairT<W>* w, uint32_t w_stride) {
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
@@ -77,17 +77,17 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
     }
 }
 
-template <int LOGN, class W>
-__device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const uint64_t* src, uint32_t A,
+template <int LOGN, class W, class St>
+__device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride) {
     switch (A) {
-        case 1: fwd_conv_n<1, LOGN, W>(sm, P, rank, src, w, w_stride); break;
-        case 2: fwd_conv_n<2, LOGN, W>(sm, P, rank, src, w, w_stride); break;
+        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride); break;
+        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W>(sm, P, rank, src, w, w_stride); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W>(sm, P, rank, src, w, w_stride); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride); break; } }
         [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -171,18 +171,18 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         }
         // src limbs hold y_i = [d_i (D_j/q_i)^-1]_{q_i} (a single-prime digit:
         // d itself); ModUp = sum_i y_i [D_j/q_i]_r computed in the loader
-        const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
+        const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK);
         mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm[swz(y)], q, two_q); });
     }
-    uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
-    uint64_t* out1 = out0 + uint64_t(LK) * n;
+    W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
+    W* out1 = out0 + uint64_t(LK) * n;
 #pragma unroll
     for (int jj = 0; jj < kE; ++jj) {
         const uint32_t y = threadIdx.x + jj * S::T;
         const W v0 = acc0[y], v1 = acc1[y];
-        out0[y] = static_cast<uint64_t>(v0 >= q ? v0 - q : v0);
-        out1[y] = static_cast<uint64_t>(v1 >= q ? v1 - q : v1);
+        out0[y] = v0 >= q ? v0 - q : v0;
+        out1[y] = v1 >= q ? v1 - q : v1;
     }
     // no trailing cluster barrier: the last remote access to this CTA's smem
     // (a scatter) is ordered before the cluster sync inside fwd_core
@@ -309,11 +309,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
             });
             continue;
         }
-        const uint64_t* src = a.dc + (uint64_t(c) * d.L + lo) * n;
+        const uint64_t* src = static_cast<const uint64_t*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, uint64_t>(sm, P, rank, src, hi - lo, d.dhat_mod_sh + lo * LK + r, LK);
         mac_all(j, first, [&](uint32_t y, uint32_t) { return reduce_4q<uint64_t>(sm[swz(y)], q, two_q); });
     }
-    uint64_t* out0 = a.acc + (uint64_t(c) * 2 * LK + r) * n + cta_base;
+    uint64_t* out0 = static_cast<uint64_t*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     uint64_t* out1 = out0 + uint64_t(LK) * n;
 #pragma unroll
     for (int quarter = 0; quarter < kE / 4; ++quarter) {
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
 }
 
 struct ModDownArgs {
-    const uint64_t* acc;      // [count][2][L+K][n]: Q limbs evaluations, P limbs coefficients
+    const void* acc;          // [count][2][L+K][n]: Q limbs evaluations, P limbs coefficients (word-sized)
     const uint64_t* add0;     // optional, poly stride add_stride
     const uint64_t* add1;
     uint64_t add_stride;
@@ -360,13 +360,13 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
     const PrimeDev& P = d.primes[r];
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     const uint64_t n = 1ull << LOGN;
-    const uint64_t* accp = a.acc + ((uint64_t(c) * 2 + h) * LK + d.L) * n;
+    const W* accp = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + d.L) * n;
     // K == 1: [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced;
     // else the P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded
     // into the inverse transform) and the loader forms sum_l y_l [P/p_l]_{q_r}
     fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L);
     const uint32_t cta_base = rank * S::M;
-    const uint64_t* accq = a.acc + ((uint64_t(c) * 2 + h) * LK + r) * n;
+    const W* accq = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + r) * n;
     const uint64_t* add = h ? a.add1 : a.add0;
     if (add) add += c * a.add_stride + (uint64_t(r) << LOGN);
     const uint64_t* sum = h ? a.sum1 : a.sum0;

@@ -116,6 +116,9 @@ struct LimbBatch {
     // prime_map batches only: every mapped prime is below 2^30 (the caller
     // knows; contiguous batches are checked on the host)
     bool map_small = false;
+    // `data` holds u32 residues (32-bit word batches only; strides in
+    // elements): the key switch keeps its intermediates packed
+    bool packed32 = false;
 };
 
 // Evaluation-domain source position of x under x -> x^g (bit-reversed order).
@@ -249,9 +252,10 @@ __device__ __forceinline__ int prime_index(const LimbBatch& b, uint32_t limb_id)
     return static_cast<int>(b.first_prime + limb_id % b.limbs);
 }
 
-__device__ __forceinline__ uint64_t* limb_ptr(const LimbBatch& b, uint32_t limb_id, int logn) {
+template <class St = uint64_t>
+__device__ __forceinline__ St* limb_ptr(const LimbBatch& b, uint32_t limb_id, int logn) {
     const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
-    return b.data + (uint64_t)poly * b.poly_stride + ((uint64_t)l << logn);
+    return reinterpret_cast<St*>(b.data) + (uint64_t)poly * b.poly_stride + ((uint64_t)l << logn);
 }
 
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;\n" ::: "memory"); }
@@ -316,7 +320,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 #endif
 template <class W> constexpr int ntt_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_NTT32_MINB; }
 
-template <int LOGN, class W>
+template <int LOGN, class W, class St = uint64_t>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
     using S = NttShape<LOGN>;
     __shared__ __align__(16) W sm[S::M];
@@ -325,19 +329,19 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     const int pidx = prime_index(b, limb_id);
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
-    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
+    St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
     fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return static_cast<W>(__ldcs(&a[x])); });
     // Coalesced store of the CTA's chunk, fully reduced.
     const W q = static_cast<W>(P.q), two_q = 2 * q;
-    uint64_t* out = a + rank * S::M;
+    St* out = a + rank * S::M;
 #pragma unroll
     for (int j = 0; j < kE; ++j) {
         const uint32_t y = threadIdx.x + j * S::T;
-        __stcs(&out[y], static_cast<uint64_t>(reduce_4q<W>(sm[swz(y)], q, two_q)));
+        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm[swz(y)], q, two_q)));
     }
 }
 
-template <int LOGN, class W>
+template <int LOGN, class W, class St = uint64_t>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
     const W q = static_cast<W>(P.q), two_q = 2 * q;
-    uint64_t* __restrict__ a = limb_ptr(b, limb_id, LOGN);
+    St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
     const PairT<W>* __restrict__ tw = inv_table<W>(P);
     const uint32_t cta_base = rank * S::M;
 
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
             sm[swz(y)] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
         }
     } else {
-        const uint64_t* in = a + cta_base;
+        const St* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
             r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
         }
 #pragma unroll
-        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<uint64_t>(r[k]));
+        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
     }
     if constexpr (S::CL > 1) cg::this_cluster().sync();  // keep smem alive for peers
 }
