@@ -43,7 +43,10 @@ def workload_objects(name: str, word: int = 64):
         prm = params.lola_mnist_params_w32() if word == 32 else params.lola_mnist_params()
         return cfg, strategy, batch, nets.lola_mnist_net(config=2), prm
     if name == "lola-small":
-        return cfg, strategy, batch, nets.lola_small_net(config=3), params.lola_small_params()
+        prm = params.lola_small_params_w32() if word == 32 else params.lola_small_params()
+        return cfg, strategy, batch, nets.lola_small_net(config=3), prm
+    # config 4 stays on 60-bit primes: with u64 storage its 12-limb 30-bit
+    # chain does not fit the plan's live messages in 180 GB
     return cfg, strategy, batch, nets.lola_cifar_net(config=4), params.lola_cifar_params()
 
 
@@ -58,8 +61,9 @@ def parse():
                     help="lola-mnist = BASELINE config 2 (the headline); lola-small = config 3; lola-cifar = config 4")
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
-    ap.add_argument("--word", type=int, default=64, choices=[32, 64],
-                    help="RNS word: 64 = 60-bit primes, 32 = 30-bit primes (32-bit word kernels)")
+    ap.add_argument("--word", type=int, default=32, choices=[32, 64],
+                    help="RNS word: 32 = 30-bit primes (32-bit word kernels, default), 64 = 60-bit primes "
+                         "(lola-cifar always 64)")
     return ap.parse_args()
 
 
@@ -218,8 +222,9 @@ def run_reference(a, world, rank):
 # ---- our arm -----------------------------------------------------------------------------
 
 def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
-    """Dominant kernel (batched 64-bit NTT at n=16384) timed alone with CUDA
-    events on its launch stream, against the measured integer-pipe roof."""
+    """Dominant kernel (batched NTT at n=16384, the workload's word size)
+    timed alone with CUDA events on its launch stream, against the measured
+    integer-pipe roof of the same word size."""
     import ctypes as C
 
     import torch
@@ -228,7 +233,8 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
 
     n, L = cx.n, cx.L
     polys = max(1, limbs // L)
-    data = torch.randint(0, 2**59, (polys, L, n), dtype=torch.int64, device="cuda")
+    data = torch.randint(0, min(cx.params.q), (polys, L, n), dtype=torch.int64, device="cuda")
+    word = 32 if max(cx.params.q) < 2**30 else 64
     s = torch.cuda.current_stream()
     for _ in range(3):
         cx.ntt_forward(data, limbs=L, stream=s)
@@ -253,7 +259,8 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
     return {
-        "kernel": f"ntt_forward_kernel<14> ({polys * L} limbs of n={n}, 60-bit q)",
+        "kernel": f"ntt_forward_kernel<14, u{word}> ({polys * L} limbs of n={n}, "
+                  f"{max(cx.params.q).bit_length()}-bit q, {word}-bit words)",
         "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
         "frac": achieved / (peak.value / 1e9),
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
@@ -262,6 +269,58 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
         "limb_transforms_per_s": polys * L / (ms * 1e-3),
         "hbm_view": {"achieved_gbs": hbm_bytes / (ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                      "frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": hbm_bytes},
+    }
+
+
+def ks_roofline(cx, count: int, reps: int = 10) -> dict:
+    """The dominant unit: one key switch (inverse NTT of the input, fused
+    ModUp+NTT+key MAC over Q∪P, inverse NTT of the P limbs, fused ModDown),
+    i.e. ks_inner_kernel + moddown_kernel + ntt_inverse_kernel (~82% of the
+    step's device time), timed with CUDA events on its launch stream over a
+    batch of `count` ciphertext rotations. Achieved = algorithmic limb-transform
+    butterflies per second (MAC / base-conversion multiplies not counted, so
+    conservative) against the live butterfly peak of the same word size."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1812_10659_b200 import _native as nat
+    from paper_1812_10659_b200.bfv import galois_exponent_columns
+
+    n, L, K, dnum = cx.n, cx.L, cx.K, cx.dnum
+    alpha = -(-L // dnum)
+    digits = [min(L, (j + 1) * alpha) - j * alpha for j in range(dnum)]
+    transforms = L + sum(L + K - a for a in digits) + 2 * K + 2 * L
+    logn = n.bit_length() - 1
+    bfly_per_ct = transforms * (n // 2) * logn
+    ct = torch.randint(0, min(cx.params.q), (count, 2, L, n), dtype=torch.int64, device="cuda")
+    out = torch.empty_like(ct)
+    g = galois_exponent_columns(n, 1)
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        cx.rotate(ct, g, out=out, stream=s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(reps):
+        cx.rotate(ct, g, out=out, stream=s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    word = 32 if max(cx.params.q) < 2**30 else 64
+    peak = C.c_double()
+    nat.call("lb_bench_butterfly_peak", cx.params.q[0], 4, 4000, C.byref(peak))
+    achieved = count * bfly_per_ct / (ms * 1e-3) / 1e9
+    del ct, out
+    return {
+        "kernel": f"key switch = ntt_inverse + ks_inner_kernel + ntt_inverse(P) + moddown_kernel, u{word} words, "
+                  f"{count} ciphertext rotations per launch set (n={n}, L={L}, K={K}, dnum={dnum})",
+        "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
+        "frac": achieved / (peak.value / 1e9),
+        "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
+        "traffic": None,
+        "algorithmic": f"{transforms} limb transforms x {(n // 2) * logn} butterflies per ciphertext",
+        "launch_set_ms": ms, "rotations_per_s": count / (ms * 1e-3),
     }
 
 
@@ -351,9 +410,11 @@ def run_ours(a, world, rank, local):
         del one
         torch.cuda.empty_cache()
         extras["latency_ms"] = {"he_steps": min(lat), "e2e": min(lat_e2e), "images": 1}
-        # roofline of the dominant kernel, at the batch's key-switch limb count
+        # roofline of the dominant unit (the key switch, at a typical plan
+        # launch size) and of its NTT component alone
+        extras["roofline"] = ks_roofline(cx, 16 * len(prm.t))
         ks_limbs = B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1)
-        extras["roofline"] = ntt_roofline(cx, ks_limbs)
+        extras["roofline_ntt"] = ntt_roofline(cx, ks_limbs)
         # CPU baseline: the reference on this host, one thread, bounded sample
         try:
             from oracle import refbind as R
@@ -371,10 +432,12 @@ def run_ours(a, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": elapsed / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (SplitMix64-seeded pixels and weights)",
+            "vs_baseline": None, "dtype": "u32" if max(prm.q) < 2**30 else "u64",
+            "data": "synthetic (SplitMix64-seeded pixels and weights)",
             "config": {"workload": f"{strategy} cfg{cfg} batched throughput", "images_per_gpu_per_step": B,
                        "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
-                       "q_bits": 60, "parallelism": f"images sharded over {world} GPU(s), no collective",
+                       "q_bits": max(prm.q).bit_length(), "residue_storage": "u64 in HBM (key-switch "
+                       "intermediates u32 when q_bits <= 30)", "parallelism": f"images sharded over {world} GPU(s), no collective",
                        "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes) * world,
                     "d2h_bytes_per_step": int(scores.nbytes) * world},

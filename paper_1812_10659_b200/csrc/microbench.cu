@@ -13,13 +13,16 @@ namespace lb {
 // Same butterfly sequence as fwd_group<4> (radix-16 pass: 32 butterflies),
 // twiddles held in registers, repeated `iters` times. Results folded into
 // `sink` so nothing is dead code.
-__global__ void __launch_bounds__(256) butterfly_peak_kernel(uint64_t q, ulonglong2 w0, ulonglong2 w1, int iters,
+template <class W>
+__global__ void __launch_bounds__(256) butterfly_peak_kernel(W q, PairT<W> w0, PairT<W> w1, int iters,
                                                                uint64_t* sink) {
-    const uint64_t two_q = 2 * q;
-    uint64_t r[kE];
+    const W two_q = 2 * q;
+    W r[kE];
 #pragma unroll
-    for (int k = 0; k < kE; ++k) r[k] = (threadIdx.x * 2654435761ull + k * 97ull) % q;
-    ulonglong2 w[4] = {w0, w1, make_ulonglong2(w0.x ^ 1, w0.y), make_ulonglong2(w1.x ^ 1, w1.y)};
+    for (int k = 0; k < kE; ++k) r[k] = static_cast<W>((threadIdx.x * 2654435761ull + k * 97ull) % q);
+    PairT<W> w[4] = {w0, w1, w0, w1};
+    w[2].x ^= 1;
+    w[3].x ^= 1;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int l = 0; l < kLogE; ++l) {
@@ -31,10 +34,10 @@ __global__ void __launch_bounds__(256) butterfly_peak_kernel(uint64_t q, ulonglo
             }
         }
     }
-    uint64_t acc = 0;
+    W acc = 0;
 #pragma unroll
     for (int k = 0; k < kE; ++k) acc ^= r[k];
-    if (acc == 0x5555555555555555ull) sink[0] = acc;
+    if (acc == static_cast<W>(0x5555555555555555ull)) sink[0] = acc;
 }
 
 }  // namespace lb
@@ -47,15 +50,26 @@ extern "C" int lb_bench_butterfly_peak(uint64_t q, int blocks_per_sm, int iters,
         uint64_t* sink = nullptr;
         LB_CUDA(cudaMalloc(&sink, 8));
         const uint64_t w = 0x123456789abcdefull % q, w2 = 0x0fedcba987654321ull % q;
-        ulonglong2 w0 = make_ulonglong2(w, lb::shoup_companion(w, q));
-        ulonglong2 w1 = make_ulonglong2(w2, lb::shoup_companion(w2, q));
         const int grid = sms * blocks_per_sm;
-        lb::butterfly_peak_kernel<<<grid, 256>>>(q, w0, w1, iters / 10 + 1, sink);  // warm-up
+        // q < 2^30: the 32-bit word butterfly the NTT kernels use for such primes
+        const bool w32 = q < lb::kWord32Bound;
+        auto launch = [&](int it) {
+            if (w32) {
+                const uint2 w0 = make_uint2(uint32_t(w), lb::shoup_companion32(w, q));
+                const uint2 w1 = make_uint2(uint32_t(w2), lb::shoup_companion32(w2, q));
+                lb::butterfly_peak_kernel<uint32_t><<<grid, 256>>>(uint32_t(q), w0, w1, it, sink);
+            } else {
+                const ulonglong2 w0 = make_ulonglong2(w, lb::shoup_companion(w, q));
+                const ulonglong2 w1 = make_ulonglong2(w2, lb::shoup_companion(w2, q));
+                lb::butterfly_peak_kernel<uint64_t><<<grid, 256>>>(q, w0, w1, it, sink);
+            }
+        };
+        launch(iters / 10 + 1);  // warm-up
         cudaEvent_t a, b;
         LB_CUDA(cudaEventCreate(&a));
         LB_CUDA(cudaEventCreate(&b));
         LB_CUDA(cudaEventRecord(a));
-        lb::butterfly_peak_kernel<<<grid, 256>>>(q, w0, w1, iters, sink);
+        launch(iters);
         LB_CUDA(cudaEventRecord(b));
         LB_CUDA(cudaEventSynchronize(b));
         float ms = 0;

@@ -103,3 +103,8 @@ def lola_cifar_params(seed: int = 1) -> BfvParams:
 def lola_small_params(seed: int = 1) -> BfvParams:
     """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square)."""
     return make_params(8192, L=3, T=2, K=1, dnum=3, seed=seed)
+
+
+def lola_small_params_w32(seed: int = 1) -> BfvParams:
+    """Config 3 on 30-bit primes: L = 6, K = 2, dnum = 3 digits of 2."""
+    return make_params(8192, L=6, T=2, K=2, dnum=3, bits=30, seed=seed)

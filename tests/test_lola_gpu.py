@@ -47,6 +47,12 @@ def test_lola_mnist_config0():
     _check(lola_mnist_params(), nets.lola_mnist_net(), "lola-mnist", batch=2, config=0)
 
 
+def test_lola_small_config3_word32():
+    from paper_1812_10659_b200.params import lola_small_params_w32
+
+    _check(lola_small_params_w32(), nets.lola_small_net(), "lola-small", batch=2, config=3)
+
+
 def test_lola_mnist_config0_word32():
     """The same network on 30-bit RNS primes (32-bit word kernels)."""
     from paper_1812_10659_b200.params import lola_mnist_params_w32
