@@ -259,6 +259,12 @@ __device__ __forceinline__ St* limb_ptr(const LimbBatch& b, uint32_t limb_id, in
 }
 
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;\n" ::: "memory"); }
+// No release fence: for barriers that only order this CTA's earlier smem
+// READS (whose values are already consumed) before peers' remote writes, or
+// keep this CTA resident until peers finish reading it.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
 
 // Forward transform core, shared by the plain and the fused kernels. The
@@ -276,7 +282,7 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
     const PairT<W>* __restrict__ tw = fwd_table<W>(P);
     // Every CTA of the cluster must be running (and done reading its smem)
     // before peers write into it: arrive now, wait before the remote stores.
-    if constexpr (S::CL > 1) cluster_arrive();
+    if constexpr (S::CL > 1) cluster_arrive_relaxed();
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
         W r[kE];
@@ -436,7 +442,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
 #pragma unroll
         for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
     }
-    if constexpr (S::CL > 1) cg::this_cluster().sync();  // keep smem alive for peers
+    if constexpr (S::CL > 1) {  // keep smem alive for peers
+        cluster_arrive_relaxed();
+        cluster_wait();
+    }
 }
 
 }  // namespace lb
