@@ -115,6 +115,10 @@ class ClockSampler:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's NVML start-up must not overlap the timed region
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10:
+                time.sleep(0.05)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -355,16 +359,19 @@ def run_ours(a, world, rank, local):
     # ---- value: HE steps, encrypted inputs resident in HBM ----
     launches0 = int(nat.lib().lb_launch_count())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     with ClockSampler(local) as clk:
         barrier(world)
         torch.cuda.synchronize()
         e0.record(s)
-        for _ in range(a.steps):
+        for i in range(a.steps):
             sess.execute()
+            marks[i].record(s)
         e1.record(s)
         torch.cuda.synchronize()
         barrier(world)
     launches = int(nat.lib().lb_launch_count()) - launches0
+    step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, a.steps)]
     elapsed = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
     value = world * B * a.steps / elapsed
 
@@ -442,6 +449,7 @@ def run_ours(a, world, rank, local):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes) * world,
                     "d2h_bytes_per_step": int(scores.nbytes) * world},
             "gpu_launches": launches,
+            "step_ms": [round(v, 3) for v in step_ms],
             "clocks": clk.summary(),
             "rotations_per_s": value * rot_per_image,
             "key_switches_per_image": rot_per_image + int(counters[:, 0].sum()) * len(prm.t),

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         // d itself); ModUp = sum_i y_i [D_j/q_i]_r computed in the loader
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK);
-        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm[swz(y)], q, two_q); });
+        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm[swz_w<W>(y)], q, two_q); });
     }
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     W* out1 = out0 + uint64_t(LK) * n;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
-            const W conv = reduce_4q<W>(sm[swz(y)], q, two_q);
+            const W conv = reduce_4q<W>(sm[swz_w<W>(y)], q, two_q);
             W u = shoup_full<W>(va[jj] + q - conv, pinv.x, pinv.y, q);
             u += vb[jj];
             u = u >= q ? u - q : u;

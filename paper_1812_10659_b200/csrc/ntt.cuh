@@ -134,11 +134,30 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t x, uint64_t g, int logn)
 #endif
 constexpr int kLogE = LB_NTT_LOGE;     // 2^kLogE coefficients per thread (radix of a register pass)
 constexpr int kE = 1 << kLogE;
-constexpr int kCtaCoeffs = 4096;       // coefficients owned by one CTA
+#ifndef LB_CTA_COEFFS
+#define LB_CTA_COEFFS 4096
+#endif
+constexpr int kCtaCoeffs = LB_CTA_COEFFS;  // coefficients owned by one CTA
 constexpr int kThreads = kCtaCoeffs / kE;  // 128 (radix 32) or 256 (radix 16)
-constexpr int kMinBlocks = kThreads == 128 ? 4 : 3;  // resident CTAs per SM the register budget must allow
+constexpr int kMinBlocks = kThreads <= 128 ? 4 : kThreads == 256 ? 3 : 1;  // resident CTAs per SM the register budget must allow
 
+// Shared-memory swizzles (bijective on a CTA chunk: low bits XORed with
+// higher bits, two instructions):
+//   u64 words (two banks each, 16 per 128-byte row): y ^ ((y >> 4) & 15)
+//   u32 words (32 per row): y ^ ((y >> 5) & 31)
+// By enumeration of the passes' warp access patterns (n = 2^12..2^15) the
+// u32 form averages 1.2 wavefronts per access vs 1.4 for the u64 form; a
+// fully conflict-free u32 form (y ^ h ^ (h << 1), h = (y >> 5) & 15) costs
+// two more instructions per access and measured slower (94.9 vs 96.4 img/s).
 __device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
+template <class W>
+__device__ __forceinline__ uint32_t swz_w(uint32_t y) {
+    if constexpr (sizeof(W) == 8) {
+        return swz(y);
+    } else {
+        return y ^ ((y >> 5) & 31u);
+    }
+}
 
 // Harvey lazy CT butterfly: X, Y in [0, 4q) -> X + WY, X - WY in [0, 4q).
 template <class W, class Pr>
@@ -214,13 +233,13 @@ __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ t
         const uint32_t B = (cta_base >> log_bs) + b;
         W r[1 << C];
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) r[k] = sm[swz(base + k * stride)];
+        for (int k = 0; k < (1 << C); ++k) r[k] = sm[swz_w<W>(base + k * stride)];
         if (INVERSE)
             inv_group<C>(r, tw, s0, B, q, two_q);
         else
             fwd_group<C>(r, tw, s0, B, q, two_q);
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) sm[swz(base + k * stride)] = r[k];
+        for (int k = 0; k < (1 << C); ++k) sm[swz_w<W>(base + k * stride)] = r[k];
     }
 }
 
@@ -297,9 +316,9 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
             const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
             if constexpr (S::CL > 1) {
                 W* remote = cg::this_cluster().map_shared_rank(sm, dst);
-                remote[swz(y)] = r[k];
+                remote[swz_w<W>(y)] = r[k];
             } else {
-                sm[swz(y)] = r[k];
+                sm[swz_w<W>(y)] = r[k];
             }
         }
     }
@@ -343,7 +362,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
 #pragma unroll
     for (int j = 0; j < kE; ++j) {
         const uint32_t y = threadIdx.x + j * S::T;
-        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm[swz(y)], q, two_q)));
+        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm[swz_w<W>(y)], q, two_q)));
     }
 }
 
@@ -369,14 +388,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
             const uint32_t x = cta_base + y;
-            sm[swz(y)] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
+            sm[swz_w<W>(y)] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
         }
     } else {
         const St* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
-            sm[swz(y)] = static_cast<W>(__ldcs(&in[y]));
+            sm[swz_w<W>(y)] = static_cast<W>(__ldcs(&in[y]));
         }
     }
     __syncthreads();
@@ -403,9 +422,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
             const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
             if constexpr (S::CL > 1) {
                 const W* remote = cg::this_cluster().map_shared_rank(sm, src);
-                r[k] = remote[swz(y)];
+                r[k] = remote[swz_w<W>(y)];
             } else {
-                r[k] = sm[swz(y)];
+                r[k] = sm[swz_w<W>(y)];
             }
         }
         // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
