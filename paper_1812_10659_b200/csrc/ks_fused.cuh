@@ -32,7 +32,7 @@ struct KsInnerArgs {
 template <class W>
 __device__ __forceinline__ W add_lazy2(W a, W b, W two_q) {
     const W s = a + b;
-    return s >= two_q ? s - two_q : s;
+    return csub<W>(s, two_q);
 }
 
 // Word-specific views of the key-switch constant tables.
@@ -69,7 +69,7 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
             W acc = shoup_lazy<W>(v[0], ww[0].x, ww[0].y, q) + shoup_lazy<W>(v[1], ww[1].x, ww[1].y, q);
 #pragma unroll
             for (int i = 2; i < A; ++i) {
-                acc = acc >= two_q ? acc - two_q : acc;
+                acc = csub<W>(acc, two_q);
                 acc += shoup_lazy<W>(v[i], ww[i].x, ww[i].y, q);
             }
             return acc;
@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
     for (int jj = 0; jj < kE; ++jj) {
         const uint32_t y = threadIdx.x + jj * S::T;
         const W v0 = acc0[y], v1 = acc1[y];
-        out0[y] = v0 >= q ? v0 - q : v0;
-        out1[y] = v1 >= q ? v1 - q : v1;
+        out0[y] = csub<W>(v0, q);
+        out1[y] = csub<W>(v1, q);
     }
     // no trailing cluster barrier: the last remote access to this CTA's smem
     // (a scatter) is ordered before the cluster sync inside fwd_core
@@ -393,9 +393,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
             const W conv = reduce_4q<W>(sm[swz_w<W>(y)], q, two_q);
             W u = shoup_full<W>(va[jj] + q - conv, pinv.x, pinv.y, q);
             u += vb[jj];
-            u = u >= q ? u - q : u;
+            u = csub<W>(u, q);
             u += vs[jj];
-            u = u >= q ? u - q : u;
+            u = csub<W>(u, q);
             out[cta_base + y] = static_cast<uint64_t>(u);
         }
     }
