@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         // d itself); ModUp = sum_i y_i [D_j/q_i]_r computed in the loader
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK);
-        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm[swz_w<W>(y)], q, two_q); });
+        const uint32_t sbt = swb<W>(threadIdx.x);
+        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm_at(sm, sbt, y - threadIdx.x), q, two_q); });
     }
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     W* out1 = out0 + uint64_t(LK) * n;
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
+    const uint32_t sbt = swb<W>(threadIdx.x);
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
     // any of them, so their latencies overlap.
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
-            const W conv = reduce_4q<W>(sm[swz_w<W>(y)], q, two_q);
+            const W conv = reduce_4q<W>(sm_at(sm, sbt, (part * kHalf + jj) * S::T), q, two_q);
             W u = shoup_full<W>(va[jj] + q - conv, pinv.x, pinv.y, q);
             u += vb[jj];
             u = csub<W>(u, q);

@@ -155,6 +155,21 @@ constexpr int kMinBlocks = kThreads <= 128 ? 4 : kThreads == 256 ? 3 : 1;  // re
 // two more instructions per access and measured slower (94.9 vs 96.4 img/s).
 __device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
 template <class W>
+__device__ __forceinline__ uint32_t swz_w(uint32_t y);
+
+// Both swizzles are linear over GF(2), so for y = base + c with base and c
+// bit-disjoint (every access below: a thread-dependent base plus a
+// compile-time multiple of a power-of-two stride that is larger than the
+// base's set bits) swz(y) = swz(base) ^ swz(c). swb() is the swizzled byte
+// offset of the base, computed once; sm_at() costs one LOP3 per access.
+template <class W>
+__device__ __forceinline__ uint32_t swb(uint32_t base) { return swz_w<W>(base) * static_cast<uint32_t>(sizeof(W)); }
+template <class W>
+__device__ __forceinline__ W& sm_at(W* sm, uint32_t sb, uint32_t c) {
+    return *reinterpret_cast<W*>(reinterpret_cast<char*>(sm) + (sb ^ swb<W>(c)));
+}
+
+template <class W>
 __device__ __forceinline__ uint32_t swz_w(uint32_t y) {
     if constexpr (sizeof(W) == 8) {
         return swz(y);
@@ -234,15 +249,17 @@ __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ t
         const uint32_t b = g / stride, o = g % stride;
         const uint32_t base = (b << log_bs) + o;
         const uint32_t B = (cta_base >> log_bs) + b;
+        // base has no bits in [log2 stride, log_bs), where k * stride lives
+        const uint32_t sb = swb<W>(base);
         W r[1 << C];
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) r[k] = sm[swz_w<W>(base + k * stride)];
+        for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k * stride);
         if (INVERSE)
             inv_group<C>(r, tw, s0, B, q, two_q);
         else
             fwd_group<C>(r, tw, s0, B, q, two_q);
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) sm[swz_w<W>(base + k * stride)] = r[k];
+        for (int k = 0; k < (1 << C); ++k) sm_at(sm, sb, k * stride) = r[k];
     }
 }
 
@@ -313,15 +330,16 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
         if constexpr (S::CL > 1) cluster_wait();
         else __syncthreads();
+        const uint32_t sb = swb<W>(rho);  // rho < NE
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
             const uint32_t dst = k / S::PER_CTA;
-            const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
+            const uint32_t c = (k % S::PER_CTA) * S::NE;
             if constexpr (S::CL > 1) {
                 W* remote = cg::this_cluster().map_shared_rank(sm, dst);
-                remote[swz_w<W>(y)] = r[k];
+                sm_at(remote, sb, c) = r[k];
             } else {
-                sm[swz_w<W>(y)] = r[k];
+                sm_at(sm, sb, c) = r[k];
             }
         }
     }
@@ -362,10 +380,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     // Coalesced store of the CTA's chunk, fully reduced.
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     St* out = a + rank * S::M;
+    const uint32_t sb = swb<W>(threadIdx.x);
 #pragma unroll
     for (int j = 0; j < kE; ++j) {
         const uint32_t y = threadIdx.x + j * S::T;
-        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm[swz_w<W>(y)], q, two_q)));
+        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm_at(sm, sb, j * S::T), q, two_q)));
     }
 }
 
@@ -384,6 +403,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     const PairT<W>* __restrict__ tw = inv_table<W>(P);
     const uint32_t cta_base = rank * S::M;
 
+    const uint32_t sbt = swb<W>(threadIdx.x);
     if (b.src) {
         const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
         const uint64_t* in = b.src + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
@@ -391,14 +411,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
             const uint32_t x = cta_base + y;
-            sm[swz_w<W>(y)] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
+            sm_at(sm, sbt, j * S::T) = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
         }
     } else {
         const St* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
-            sm[swz_w<W>(y)] = static_cast<W>(__ldcs(&in[y]));
+            sm_at(sm, sbt, j * S::T) = static_cast<W>(__ldcs(&in[y]));
         }
     }
     __syncthreads();
@@ -419,15 +439,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
         W r[kE];
+        const uint32_t sb = swb<W>(rho);  // rho < NE
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
             const uint32_t src = k / S::PER_CTA;
-            const uint32_t y = (k % S::PER_CTA) * S::NE + rho;
+            const uint32_t c = (k % S::PER_CTA) * S::NE;
             if constexpr (S::CL > 1) {
-                const W* remote = cg::this_cluster().map_shared_rank(sm, src);
-                r[k] = remote[swz_w<W>(y)];
+                W* remote = cg::this_cluster().map_shared_rank(sm, src);
+                r[k] = sm_at(remote, sb, c);
             } else {
-                r[k] = sm[swz_w<W>(y)];
+                r[k] = sm_at(sm, sb, c);
             }
         }
         // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
