@@ -281,11 +281,15 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
 def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     """The dominant unit: one key switch (inverse NTT of the input, fused
     ModUp+NTT+key MAC over Q∪P, inverse NTT of the P limbs, fused ModDown),
-    i.e. ks_inner_kernel + moddown_kernel + ntt_inverse_kernel (~82% of the
+    i.e. ks_inner_kernel + moddown_kernel + ntt_inverse_kernel (~80% of the
     step's device time), timed with CUDA events on its launch stream over a
-    batch of `count` ciphertext rotations. Achieved = algorithmic limb-transform
-    butterflies per second (MAC / base-conversion multiplies not counted, so
-    conservative) against the live butterfly peak of the same word size."""
+    batch of `count` ciphertext rotations.
+
+    Algorithmic work = modular (Shoup) products per ciphertext: one per NTT
+    butterfly, per ModUp base-conversion term, per key MAC, per ModDown
+    conversion term and P^-1 scaling. Peak = the live butterfly
+    microbenchmark (one Shoup product + three ALU ops each), so the fraction
+    is conservative; the butterfly-only view is reported beside it."""
     import ctypes as C
 
     import torch
@@ -298,7 +302,11 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     digits = [min(L, (j + 1) * alpha) - j * alpha for j in range(dnum)]
     transforms = L + sum(L + K - a for a in digits) + 2 * K + 2 * L
     logn = n.bit_length() - 1
-    bfly_per_ct = transforms * (n // 2) * logn
+    bfly = transforms * (n // 2) * logn
+    modup = sum(a * (L + K - a) for a in digits if a > 1) * n
+    mac = 2 * dnum * (L + K) * n
+    moddown = ((K * 2 * L) if K > 1 else 0) * n + 2 * L * n
+    products = bfly + modup + mac + moddown
     ct = torch.randint(0, min(cx.params.q), (count, 2, L, n), dtype=torch.int64, device="cuda")
     out = torch.empty_like(ct)
     g = galois_exponent_columns(n, 1)
@@ -316,16 +324,20 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     word = 32 if max(cx.params.q) < 2**30 else 64
     peak = C.c_double()
     nat.call("lb_bench_butterfly_peak", cx.params.q[0], 4, 4000, C.byref(peak))
-    achieved = count * bfly_per_ct / (ms * 1e-3) / 1e9
+    peak_g = peak.value / 1e9
+    achieved = count * products / (ms * 1e-3) / 1e9
+    achieved_bfly = count * bfly / (ms * 1e-3) / 1e9
     del ct, out
     return {
         "kernel": f"key switch = ntt_inverse + ks_inner_kernel + ntt_inverse(P) + moddown_kernel, u{word} words, "
                   f"{count} ciphertext rotations per launch set (n={n}, L={L}, K={K}, dnum={dnum})",
-        "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
-        "frac": achieved / (peak.value / 1e9),
+        "bound": "int", "achieved": achieved, "peak": peak_g, "unit": "G Shoup products/s",
+        "frac": achieved / peak_g,
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
         "traffic": None,
-        "algorithmic": f"{transforms} limb transforms x {(n // 2) * logn} butterflies per ciphertext",
+        "algorithmic": f"per ciphertext: {transforms} limb transforms ({bfly} butterflies) + {modup} ModUp + "
+                       f"{mac} MAC + {moddown} ModDown products",
+        "butterflies_only": {"achieved": achieved_bfly, "frac": achieved_bfly / peak_g},
         "launch_set_ms": ms, "rotations_per_s": count / (ms * 1e-3),
     }
 
@@ -354,9 +366,23 @@ def run_ours(a, world, rank, local):
 
     # warm-up: key generation, plaintext encoding, pool growth
     sess.encrypt(dev_imgs, on_device=True)
-    for _ in range(a.warmup):
+
+    def untimed_step() -> float:
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(s)
         sess.execute()
-    torch.cuda.synchronize()
+        w1.record(s)
+        torch.cuda.synchronize()
+        return w0.elapsed_time(w1)
+
+    warm = [untimed_step() for _ in range(a.warmup)]
+    # settle: a fresh box occasionally shows one slow step right after start-up
+    # (device-side, not ours); keep warming (at most 5 more, untimed) until two
+    # consecutive steps agree within 3%
+    for _ in range(5):
+        if len(warm) >= 2 and abs(warm[-1] - warm[-2]) <= 0.03 * min(warm[-2:]):
+            break
+        warm.append(untimed_step())
 
     # ---- value: HE steps, encrypted inputs resident in HBM ----
     launches0 = int(nat.lib().lb_launch_count())
@@ -452,6 +478,7 @@ def run_ours(a, world, rank, local):
                     "d2h_bytes_per_step": int(scores.nbytes) * world},
             "gpu_launches": launches,
             "step_ms": [round(v, 3) for v in step_ms],
+            "warmup_ms": [round(v, 3) for v in warm],
             "clocks": clk.summary(),
             "rotations_per_s": value * rot_per_image,
             "key_switches_per_image": rot_per_image + int(counters[:, 0].sum()) * len(prm.t),
