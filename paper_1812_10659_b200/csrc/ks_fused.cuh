@@ -57,15 +57,16 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return static_cast<W>(__ldg(&src[x])); });
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); });
     } else {
         PairT<W> ww[A];
 #pragma unroll
         for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride];
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
+            const St* s0 = src + rho;
             W v[A];
 #pragma unroll
-            for (int i = 0; i < A; ++i) v[i] = static_cast<W>(__ldg(&src[i * n + x]));
+            for (int i = 0; i < A; ++i) v[i] = static_cast<W>(__ldg(&s0[i * n + off]));
             W acc = shoup_lazy<W>(v[0], ww[0].x, ww[0].y, q) + shoup_lazy<W>(v[1], ww[1].x, ww[1].y, q);
 #pragma unroll
             for (int i = 2; i < A; ++i) {
@@ -92,7 +93,8 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
             constexpr uint64_t n = 1ull << LOGN;
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) {
+            fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
+                const uint32_t x = rho + off;
                 W v = 0;
                 for (uint32_t i = 0; i < A; ++i) {
                     const PairT<W> wi = w[i * w_stride];

@@ -307,8 +307,11 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
 
 // Forward transform core, shared by the plain and the fused kernels. The
-// cluster's CTAs cooperatively transform one limb: `load(x)` supplies input
-// coefficient x (any value < 4q, so loaders may skip their final reduction),
+// cluster's CTAs cooperatively transform one limb: `load(rho, off)` supplies
+// input coefficient rho + off (any value < 4q, so loaders may skip their
+// final reduction); off is a compile-time multiple of n/16 and rho the
+// thread's fixed lane, so loaders address from `base + rho` with immediate
+// offsets,
 // and on return the CTA's chunk [rank*M, (rank+1)*M) of the bit-reversed
 // evaluations sits in `sm` (swizzled, values in [0, 4q)).
 // Callers looping over several transforms must cluster-sync between them
@@ -326,7 +329,7 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
         const uint32_t rho = rank * S::T + threadIdx.x;
         W r[kE];
 #pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = static_cast<W>(load(rho + k * S::NE));
+        for (int k = 0; k < kE; ++k) r[k] = static_cast<W>(load(rho, k * S::NE));
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
         if constexpr (S::CL > 1) cluster_wait();
         else __syncthreads();
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
     St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
-    fwd_core<LOGN>(sm, P, rank, [&](uint32_t x) { return static_cast<W>(__ldcs(&a[x])); });
+    fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); });
     // Coalesced store of the CTA's chunk, fully reduced.
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     St* out = a + rank * S::M;
