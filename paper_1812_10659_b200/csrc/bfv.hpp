@@ -140,4 +140,10 @@ void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t p
 void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
                 cudaStream_t s);
 
+// Record-tensor dense layer (simd.cu): outs[r] = sum_i W[r][i] * xs[i] for
+// R output and F input ciphertext groups of `cts` ciphertexts each; xs, outs:
+// device arrays of device pointers; W: device int64 [R][F], |W| < 2^31.
+void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint64_t* const* outs, uint32_t R,
+                        const int64_t* W, uint32_t cts, cudaStream_t s);
+
 }  // namespace lb

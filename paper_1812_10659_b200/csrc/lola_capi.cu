@@ -137,8 +137,16 @@ int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* st
         cx->cx.activate();
         auto s = std::make_unique<lb_lola_session>();
         s->net = to_network(net);
-        s->plan = lb::lola::build_plan(s->net, lb::lola::strategy_from_name(strategy), cx->cx.n());
-        s->ecx = std::make_unique<lb::lola::EvalContext>(cx->cx, batch, max_depth, static_cast<cudaStream_t>(stream));
+        const lb::lola::Strategy strat = lb::lola::strategy_from_name(strategy);
+        s->plan = lb::lola::build_plan(s->net, strat, cx->cx.n());
+        // record tensors (cryptonets-simd) pack the images into the slots of
+        // one message: one batch entry carrying `batch` records
+        const bool records = strat == lb::lola::Strategy::CryptonetsSimd;
+        if (records && (batch == 0 || batch > cx->cx.n()))
+            throw std::invalid_argument("cryptonets-simd packs at most n images per session");
+        s->ecx = std::make_unique<lb::lola::EvalContext>(cx->cx, records ? 1 : batch, max_depth,
+                                                         static_cast<cudaStream_t>(stream));
+        if (records) s->ecx->set_records(batch);
         s->ev = std::make_unique<lb::lola::Evaluator>(*s->ecx);
         s->batch = batch;
         s->outputs = s->net.stages.back().out_shape.values();

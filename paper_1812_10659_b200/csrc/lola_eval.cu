@@ -452,6 +452,82 @@ Message Evaluator::mask(const Message& a, const std::vector<uint8_t>& bits) {  /
     return mul_plain(a, std::vector<int64_t>(bits.begin(), bits.end()));
 }
 
+std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, uint64_t rows, const int64_t* host_w,
+                                             const int64_t* dev_w) {  // kernels.cpp:302-318
+    const uint64_t F = xs.size();
+    if (F == 0 || rows == 0) throw std::invalid_argument("weighted sums: empty operand");
+    auto absu = [](int64_t v) { return v < 0 ? uint64_t(-(v + 1)) + 1 : uint64_t(v); };
+    uint32_t depth = 0, plain_depth = 0;
+    bool small = true;  // every magnitude < 2^64: 128-bit bookkeeping suffices
+    for (const Message& x : xs) {
+        depth = std::max(depth, x.depth);
+        plain_depth = std::max(plain_depth, x.plain_depth + 1);
+        for (size_t k = 1; k < x.magnitude.w.size(); ++k) small = small && x.magnitude.w[k] == 0;
+    }
+    const Mag& cap = cx_->capacity();
+    std::vector<Mag> mags(rows);
+    for (uint64_t r = 0; r < rows; ++r) {
+        const int64_t* wr = host_w + r * F;
+        bool over = false;
+        if (small) {
+            unsigned __int128 acc = 0;
+            for (uint64_t i = 0; i < F; ++i) {
+                const uint64_t aw = absu(wr[i]);
+                if (aw >> 31) throw std::invalid_argument("weighted sums: |weight| must be below 2^31");
+                acc += static_cast<unsigned __int128>(xs[i].magnitude.w[0]) * aw;  // < 2^95 per term, F < 2^17
+            }
+            Mag m;
+            m.w[0] = static_cast<uint64_t>(acc);
+            m.w[1] = static_cast<uint64_t>(acc >> 64);
+            mags[r] = m;
+            over = m > cap;
+        } else {
+            Mag m(0);
+            for (uint64_t i = 0; i < F; ++i) m = m + xs[i].magnitude * Mag(absu(wr[i]));
+            mags[r] = m;
+            over = m > cap;
+        }
+        if (over) {
+            // replay the reference's sequence to raise at the same operation
+            counters_.ops.scalar_mul += r * F;
+            counters_.ops.add += r * (F - 1);
+            Mag acc = xs[0].magnitude * Mag(absu(wr[0]));
+            check_magnitude(acc, "mul_scalar");
+            counters_.ops.scalar_mul += 1;
+            for (uint64_t i = 1; i < F; ++i) {
+                const Mag p = xs[i].magnitude * Mag(absu(wr[i]));
+                check_magnitude(p, "mul_scalar");
+                counters_.ops.scalar_mul += 1;
+                acc = acc + p;
+                check_magnitude(acc, "add");
+                counters_.ops.add += 1;
+            }
+            throw std::logic_error("weighted sums: magnitude bookkeeping diverged");
+        }
+    }
+    counters_.ops.scalar_mul += rows * F;
+    counters_.ops.add += rows * (F - 1);
+    std::vector<Message> out;
+    out.reserve(rows);
+    std::vector<const uint64_t*> xp(F);
+    std::vector<uint64_t*> op(rows);
+    for (uint64_t i = 0; i < F; ++i) xp[i] = xs[i].data();
+    for (uint64_t r = 0; r < rows; ++r) {
+        out.push_back(fresh(depth, plain_depth, mags[r]));
+        op[r] = out.back().data();
+    }
+    cudaStream_t s = stream_;
+    DeviceBuffer dx(F * 8, s), dout(rows * 8, s);
+    LB_CUDA(cudaMemcpyAsync(dx.get(), xp.data(), F * 8, cudaMemcpyHostToDevice, s));
+    LB_CUDA(cudaMemcpyAsync(dout.get(), op.data(), rows * 8, cudaMemcpyHostToDevice, s));
+    simd_weighted_sums(cx_->device(), reinterpret_cast<const uint64_t* const*>(dx.get()), static_cast<uint32_t>(F),
+                       reinterpret_cast<uint64_t* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w,
+                       static_cast<uint32_t>(cx_->cts()), s);
+    // dx / dout are freed stream-ordered after the kernel (cudaFreeAsync on s);
+    // the host arrays were staged by the pageable-memory copies already
+    return out;
+}
+
 Message Evaluator::mul_scalar(const Message& a, int64_t sc) {  // evaluator.cpp:242-258
     const uint64_t as = sc < 0 ? uint64_t(-(sc + 1)) + 1 : uint64_t(sc);
     const Mag mag = a.magnitude * Mag(as);

@@ -101,6 +101,10 @@ public:
     uint32_t n() const { return cx_->n(); }
     uint32_t half() const { return cx_->n() / 2; }
     uint32_t batch() const { return batch_; }
+    // records packed into the slots of one message (record/SIMD tensors,
+    // representation.cpp:167-183); defaults to 1
+    uint32_t records() const { return records_; }
+    void set_records(uint32_t r) { records_ = r; }
     uint32_t primes() const { return cx_->T(); }  // plaintext CRT primes
     uint32_t max_depth() const { return max_depth_; }
     const Mag& capacity() const { return capacity_; }
@@ -117,6 +121,7 @@ public:
 private:
     Context* cx_;
     uint32_t batch_;
+    uint32_t records_ = 1;
     uint32_t max_depth_;
     cudaStream_t stream_;
     Mag capacity_;
@@ -179,6 +184,15 @@ public:
     Message rotate_columns_add(const Message& base, const Message& x, int64_t k);
     Message rotate_rows_add(const Message& base, const Message& x);
     Message rotate_bundle_add(const Message& base, const Message& x, uint32_t amount);
+
+    // Record-tensor dense layer (simd_dense, kernels.cpp:302-318): row r of
+    // the rows x xs.size() row-major integer matrix gives
+    //   out_r = mul_scalar(x_0, W[r][0]) + ... + mul_scalar(x_k, W[r][k])
+    // with exactly the reference's counters, depth and magnitude checks (and
+    // error texts) of that sequence, computed as one batched kernel.
+    // host_w feeds the bookkeeping, dev_w (same matrix on the device) the kernel.
+    std::vector<Message> weighted_sums(const std::vector<Message>& xs, uint64_t rows, const int64_t* host_w,
+                                       const int64_t* dev_w);
 
     void note_live(uint64_t live) { counters_.note_live(live); }
     Evaluator fork() const;

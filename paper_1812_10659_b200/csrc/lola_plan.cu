@@ -3,6 +3,7 @@
 // operation sequence — and therefore every counter — is identical; the
 // payload work behind each counted op runs batched on the GPU.
 #include <algorithm>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 
@@ -622,12 +623,81 @@ EncodedTensor add_bias(Evaluator& ev, const EncodedTensor& x, const std::vector<
         fan.join(out.messages);
         return out;
     }
-    require(x.rep.kind != RepKind::Simd, "record tensors are not supported");
+    if (x.rep.kind == RepKind::Simd) {
+        // bias of message i in the slots of every record (kernels.cpp:338-346)
+        require(bias.size() == x.messages.size(), "one bias per message required");
+        FanOut fan(ev, x.messages.size());
+        std::vector<int64_t> b(n, 0);
+        for (size_t i = 0; i < x.messages.size(); ++i) {
+            std::fill(b.begin(), b.begin() + x.rep.copies, bias[i]);
+            out.messages.push_back(fan[i].add_plain(x.messages[i], b));
+        }
+        fan.join(out.messages);
+        return out;
+    }
     require(x.messages.size() == 1, "per-value bias needs a single message");
     require(bias.size() == x.rep.length, "one bias per value required");
     std::vector<int64_t> b(n, 0);
     for (uint64_t i = 0; i < x.rep.length; ++i) b[x.rep.slot(i)] = bias[i];
     out.messages.push_back(ev.add_plain(x.messages[0], b));
+    return out;
+}
+
+// ---- record (SIMD) tensors -----------------------------------------------------------
+
+// One message per feature; slot r of message j = record r's feature j
+// (representation.cpp:167-183). The records are the session's images, packed
+// into the slots of a single batch entry.
+EncodedTensor encode_simd(Evaluator& ev, const int64_t* dev_images, uint64_t features, int64_t max_abs) {
+    const uint32_t recs = ev.context().records();
+    require(ev.context().batch() == 1, "record tensors pack the records into the slots of one message");
+    require(recs >= 1 && recs <= ev.context().n(), "more records than slots");
+    require(uint64_t(recs) * features < (1ull << 31), "record tensor too large");
+    EncodedTensor t;
+    t.rep.kind = RepKind::Simd;
+    t.rep.length = features;
+    t.rep.copies = recs;
+    std::vector<int32_t> map(recs);
+    for (uint64_t j = 0; j < features; ++j) {
+        for (uint32_t r = 0; r < recs; ++r) map[r] = static_cast<int32_t>(uint64_t(r) * features + j);
+        t.messages.push_back(ev.lift_gather(dev_images, features, map, max_abs));
+    }
+    return t;
+}
+
+// A stage's full row-major matrix, materialised once per plan (host for the
+// magnitude bookkeeping, device for the kernel).
+struct SimdMatrix {
+    uint64_t rows = 0, cols = 0;
+    std::vector<int64_t> host;
+    DeviceBuffer dev;
+    std::mutex mu;
+};
+
+EncodedTensor simd_dense(Evaluator& ev, const EncodedTensor& x, const Weights& W, SimdMatrix& M) {  // kernels.cpp:302-318
+    require(x.rep.kind == RepKind::Simd, "expected a record tensor");
+    require(x.messages.size() == x.rep.length && x.rep.length >= 1, "bad record tensor");
+    require(W.at && W.rows >= 1, "missing weights");
+    require(W.cols == x.rep.length, "weight columns do not match feature count");
+    {
+        std::lock_guard<std::mutex> lock(M.mu);
+        if (!M.dev.get()) {
+            M.rows = W.rows;
+            M.cols = W.cols;
+            M.host.resize(W.rows * W.cols);
+            for (uint64_t r = 0; r < W.rows; ++r)
+                for (uint64_t c = 0; c < W.cols; ++c) M.host[r * W.cols + c] = W.at(r, c);
+            cudaStream_t s = ev.stream();
+            M.dev = DeviceBuffer(M.host.size() * 8, s);
+            LB_CUDA(cudaMemcpyAsync(M.dev.get(), M.host.data(), M.host.size() * 8, cudaMemcpyHostToDevice, s));
+            LB_CUDA(cudaStreamSynchronize(s));
+            M.dev.rebind(nullptr);  // outlives the session's streams
+        }
+    }
+    EncodedTensor out;
+    out.rep = x.rep;
+    out.rep.length = W.rows;
+    out.messages = ev.weighted_sums(x.messages, W.rows, M.host.data(), M.dev.get<int64_t>());
     return out;
 }
 
@@ -955,6 +1025,47 @@ void build_lola_small(Plan& plan, const Network& net, uint32_t n) {
     plan.live_entering.push_back(rows);
 }
 
+CounterDelta simd_dense_cost(uint64_t nodes, uint64_t fan_in) {  // kernels.cpp:116-121
+    CounterDelta d;
+    d.scalar_mul = nodes * fan_in;
+    d.add = fan_in ? nodes * (fan_in - 1) : 0;
+    return d;
+}
+
+void build_cryptonets_simd(Plan& plan, const Network& net) {  // plan.cpp:464-502
+    require(!net.stages.empty(), "empty network");
+    require(net.squares_after.size() == net.stages.size(), "malformed network");
+    plan.in_kind = RepKind::Simd;
+    plan.in_messages = net.stages[0].in_shape.values();
+    plan.in_length = plan.in_messages;
+    const uint64_t features = plan.in_messages;
+    const int64_t bound = net.input_bound;
+    plan.encode_input = [features, bound](Evaluator& ev, const int64_t* imgs) {
+        return encode_simd(ev, imgs, features, bound);
+    };
+    const Network* np = &net;
+    uint32_t depth = 0;
+    for (size_t k = 0; k < net.stages.size(); ++k) {
+        const uint64_t fan_in = net.stages[k].in_shape.values();
+        const uint64_t nodes = net.stages[k].out_shape.values();
+        CounterDelta d = simd_dense_cost(nodes, fan_in);
+        d += add_bias_cost(nodes);
+        auto M = std::make_shared<SimdMatrix>();
+        add_step(plan, fan_in, 1, rep_name(RepKind::Simd), "per-value weighted sums, " + num(nodes) + " outputs", d,
+                 [np, k, M](Evaluator& ev, const EncodedTensor& x) {
+                     EncodedTensor t = simd_dense(ev, x, matrix_rows(np->stages[k]), *M);
+                     return add_bias(ev, t, output_bias(np->stages[k]));
+                 });
+        for (uint32_t q = 0; q < net.squares_after[k]; ++q) {
+            add_step(plan, nodes, 1, rep_name(RepKind::Simd), "square every message", square_cost(nodes),
+                     [](Evaluator& ev, const EncodedTensor& x) { return square_activation(ev, x); });
+            depth += 1;
+        }
+    }
+    plan.depth_needed = depth;
+    plan.live_entering.push_back(net.stages.back().out_shape.values());
+}
+
 void build_linear_features(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:614-646
     require(net.stages.size() == 1 && !net.stages[0].is_conv, "strategy expects a single matrix stage");
     require(net.squares_after.size() == 1 && net.squares_after[0] == 0, "strategy expects no squarings");
@@ -983,8 +1094,8 @@ void build_linear_features(Plan& plan, const Network& net, uint32_t n) {  // pla
 }  // namespace
 
 Strategy strategy_from_name(const std::string& name) {
-    for (Strategy s : {Strategy::LolaMnist, Strategy::LolaDenseMnist, Strategy::LolaCifar, Strategy::LolaSmall,
-                       Strategy::LinearFeatures})
+    for (Strategy s : {Strategy::LolaMnist, Strategy::LolaDenseMnist, Strategy::LolaCifar, Strategy::CryptonetsSimd,
+                       Strategy::LolaSmall, Strategy::LinearFeatures})
         if (name == strategy_name(s)) return s;
     throw std::invalid_argument("unknown strategy: " + name);
 }
@@ -994,6 +1105,7 @@ const char* strategy_name(Strategy s) {
         case Strategy::LolaMnist: return "lola-mnist";
         case Strategy::LolaDenseMnist: return "lola-dense-mnist";
         case Strategy::LolaCifar: return "lola-cifar";
+        case Strategy::CryptonetsSimd: return "cryptonets-simd";
         case Strategy::LolaSmall: return "lola-small";
         case Strategy::LinearFeatures: return "linear-features";
     }
@@ -1016,6 +1128,7 @@ Plan build_plan(const Network& net, Strategy s, uint32_t n) {
         case Strategy::LolaDenseMnist: build_lola_dense_mnist(plan, net, n); break;
         case Strategy::LolaCifar: build_lola_cifar(plan, net, n); break;
         case Strategy::LolaSmall: build_lola_small(plan, net, n); break;
+        case Strategy::CryptonetsSimd: build_cryptonets_simd(plan, net); break;
         case Strategy::LinearFeatures: build_linear_features(plan, net, n); break;
     }
     return plan;
@@ -1036,7 +1149,10 @@ ExecutionResult execute(const Plan& plan, EncodedTensor input, Evaluator& ev) { 
         const PlanStep& st = plan.steps[i];
         if (i > 0) {
             const Probe pr = probe_of(cur);
-            if (pr.count != st.in_count || pr.dim != st.in_dim || pr.rep != st.in_rep)
+            // record tensors: the reference plans a single record (dim 1); a
+            // session packs `records` of them, so only count and rep compare
+            const bool dim_ok = pr.dim == st.in_dim || (cur.rep.kind == RepKind::Simd && st.in_dim == 1);
+            if (pr.count != st.in_count || !dim_ok || pr.rep != st.in_rep)
                 throw std::logic_error("plan row diverged before step: " + st.op);
         }
         const CounterDelta before = ev.counters().ops;
@@ -1067,8 +1183,21 @@ DeviceBuffer decode_values(Evaluator& ev, const EncodedTensor& t) {
             parts.push_back(ev.lower_slots(m, {t.rep.broadcast ? 0u : t.rep.value_slot}));
             widths.push_back(1);
         }
+    } else if (t.rep.kind == RepKind::Simd) {
+        // value j of record r sits in slot r of message j: [records][values]
+        const uint32_t recs = t.rep.copies;
+        require(B == 1 && recs == ev.context().records(), "record tensor does not match the evaluator");
+        std::vector<uint32_t> slots(recs);
+        for (uint32_t r = 0; r < recs; ++r) slots[r] = r;
+        const uint64_t total = t.messages.size();
+        DeviceBuffer out(uint64_t(recs) * total * 32, s);
+        for (uint64_t j = 0; j < total; ++j) {
+            DeviceBuffer part = ev.lower_slots(t.messages[j], slots);  // [1][recs][4]
+            LB_CUDA(cudaMemcpy2DAsync(out.get() + j * 4, total * 32, part.get(), 32, 32, recs,
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+        return out;
     } else {
-        require(t.rep.kind != RepKind::Simd, "record tensors are not supported");
         std::vector<uint32_t> slots(t.rep.length);
         for (uint64_t i = 0; i < t.rep.length; ++i) slots[i] = t.rep.slot(i);
         for (const auto& m : t.messages) {

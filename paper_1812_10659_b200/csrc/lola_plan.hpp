@@ -83,7 +83,7 @@ struct Network {
     int64_t input_bound = 255;
 };
 
-enum class Strategy { LolaMnist, LolaDenseMnist, LolaCifar, LolaSmall, LinearFeatures };
+enum class Strategy { LolaMnist, LolaDenseMnist, LolaCifar, CryptonetsSimd, LolaSmall, LinearFeatures };
 Strategy strategy_from_name(const std::string& name);
 const char* strategy_name(Strategy s);
 

@@ -39,6 +39,16 @@ def test_toy_lola_dense_mnist_n4096():
     _check(prm, nets.toy_net(), "lola-dense-mnist", batch=2, config=9)
 
 
+@pytest.mark.parametrize("bits", [60, 30])
+def test_toy_cryptonets_simd_n4096(bits):
+    """Record tensors: 5 images packed into the slots of one message per
+    feature (plan.cpp:464-502); counters == the reference run on one record,
+    every record's logits == forward_integer."""
+    prm = make_params(4096, L=7 if bits == 60 else 14, T=3, K=1 if bits == 60 else 2,
+                      dnum=0 if bits == 60 else 7, bits=bits, seed=7)
+    _check(prm, nets.toy_net(), "cryptonets-simd", batch=5, config=9)
+
+
 def test_lola_small_config3():
     _check(lola_small_params(), nets.lola_small_net(), "lola-small", batch=2, config=3)
 

@@ -16,6 +16,7 @@ CASES = [
     ("lola-dense-mnist", nets.lola_mnist_net, 16384, 5, [2, 49, 125, 32, 356, 237, 11]),
     ("lola-small", nets.lola_small_net, 8192, 2, [1, 10, 125, 0, 235, 104, 0]),
     ("lola-mnist", nets.toy_net, 4096, 3, None),
+    ("cryptonets-simd", nets.toy_net, 4096, 3, None),
 ]
 
 
@@ -35,6 +36,17 @@ def test_cifar_counters_match_golden_totals():
     mine, depth, peak = plan_counters(nets.lola_cifar_net(), "lola-cifar", 16384)
     assert mine.sum(0).tolist() == [2, 8160, 15936, 4075, 81265, 53177, 4075]
     assert depth == 2 and peak == 4075
+
+
+def test_cryptonets_simd_counters_match_golden():
+    # proj/tests/golden/cryptonets_simd.txt:1-10 — the CIFAR net as per-value
+    # weighted sums at n=8192, every step
+    mine, depth, peak = plan_counters(nets.lola_cifar_net(), "cryptonets-simd", 8192)
+    assert mine.tolist() == [[0, 0, 49975296, 0, 49975296, 0, 0], [16268, 0, 0, 0, 0, 0, 0],
+                             [0, 0, 66292100, 0, 66292100, 0, 0], [4075, 0, 0, 0, 0, 0, 0],
+                             [0, 0, 40750, 0, 40750, 0, 0]]
+    assert mine.sum(0).tolist() == [20343, 0, 116308146, 0, 116308146, 0, 0]
+    assert depth == 2 and peak == 16268
 
 
 def test_strategy_mismatch_is_rejected():
