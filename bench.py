@@ -32,6 +32,10 @@ WORKLOADS = {
     "lola-mnist": (2, "lola-mnist", 64),
     "lola-small": (3, "lola-small", 256),
     "lola-cifar": (4, "lola-cifar", 1),
+    # the CryptoNets baseline representation of the paper's comparison: the
+    # cfg0 net with one message per value and the images in the slots
+    # (n = 16384 images per step); not a BASELINE config
+    "cryptonets-simd": (2, "cryptonets-simd", 16384),
 }
 
 
@@ -40,6 +44,9 @@ def workload_objects(name: str, word: int = 64):
 
     cfg, strategy, batch = WORKLOADS[name]
     if name == "lola-mnist":
+        prm = params.lola_mnist_params_w32() if word == 32 else params.lola_mnist_params()
+        return cfg, strategy, batch, nets.lola_mnist_net(config=2), prm
+    if name == "cryptonets-simd":
         prm = params.lola_mnist_params_w32() if word == 32 else params.lola_mnist_params()
         return cfg, strategy, batch, nets.lola_mnist_net(config=2), prm
     if name == "lola-small":
@@ -58,7 +65,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (default per workload)")
     ap.add_argument("--workload", default="lola-mnist", choices=list(WORKLOADS),
-                    help="lola-mnist = BASELINE config 2 (the headline); lola-small = config 3; lola-cifar = config 4")
+                    help="lola-mnist = BASELINE config 2 (the headline); lola-small = config 3; lola-cifar = config 4; "
+                         "cryptonets-simd = the cfg0 net in the CryptoNets representation (images in slots)")
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
     ap.add_argument("--word", type=int, default=32, choices=[32, 64],

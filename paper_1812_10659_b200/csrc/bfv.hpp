@@ -142,8 +142,9 @@ void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, u
 
 // Record-tensor dense layer (simd.cu): outs[r] = sum_i W[r][i] * xs[i] for
 // R output and F input ciphertext groups of `cts` ciphertexts each; xs, outs:
-// device arrays of device pointers; W: device int64 [R][F], |W| < 2^31.
+// device arrays of device pointers; W: device int64 [R][F], |W| < 2^31
+// (small_weights: |W| < 2^15, enabling the 32-bit path when every q < 2^30).
 void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint64_t* const* outs, uint32_t R,
-                        const int64_t* W, uint32_t cts, cudaStream_t s);
+                        const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s);
 
 }  // namespace lb

@@ -465,6 +465,8 @@ std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, ui
         for (size_t k = 1; k < x.magnitude.w.size(); ++k) small = small && x.magnitude.w[k] == 0;
     }
     const Mag& cap = cx_->capacity();
+    bool small_w = true;
+    for (uint64_t k = 0; k < rows * F; ++k) small_w = small_w && absu(host_w[k]) < (1u << 15);
     std::vector<Mag> mags(rows);
     for (uint64_t r = 0; r < rows; ++r) {
         const int64_t* wr = host_w + r * F;
@@ -521,7 +523,7 @@ std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, ui
     LB_CUDA(cudaMemcpyAsync(dx.get(), xp.data(), F * 8, cudaMemcpyHostToDevice, s));
     LB_CUDA(cudaMemcpyAsync(dout.get(), op.data(), rows * 8, cudaMemcpyHostToDevice, s));
     simd_weighted_sums(cx_->device(), reinterpret_cast<const uint64_t* const*>(dx.get()), static_cast<uint32_t>(F),
-                       reinterpret_cast<uint64_t* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w,
+                       reinterpret_cast<uint64_t* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w, small_w,
                        static_cast<uint32_t>(cx_->cts()), s);
     // dx / dout are freed stream-ordered after the kernel (cudaFreeAsync on s);
     // the host arrays were staged by the pageable-memory copies already

@@ -70,17 +70,66 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const u
     }
 }
 
+// 32-bit residues (every q < 2^30) and |W| < 2^15: each product is exact in a
+// signed 64-bit accumulator (|sum| < 2^17 * 2^15 * 2^30 = 2^62), one
+// IMAD.WIDE per term; 16 rows per thread halve the x loads per product.
+constexpr int kRowTile32 = 16;
+
+__global__ void __launch_bounds__(kColThreads) k_weighted_sums32(BfvDev d, const uint64_t* const* __restrict__ xs,
+                                                                    uint32_t F, uint64_t* const* __restrict__ outs,
+                                                                    uint32_t R, const int64_t* __restrict__ W,
+                                                                    uint64_t cols) {
+    __shared__ int32_t wsh[kChunk][kRowTile32];
+    const uint64_t c = blockIdx.x * uint64_t(kColThreads) + threadIdx.x;
+    const uint32_t r0 = blockIdx.y * kRowTile32;
+    const bool live = c < cols;
+    const uint32_t limb = static_cast<uint32_t>((c >> d.logn) % d.L);
+    int64_t acc[kRowTile32] = {};
+    for (uint32_t f0 = 0; f0 < F; f0 += kChunk) {
+        const uint32_t fc = min(uint32_t(kChunk), F - f0);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < kRowTile32 * kChunk; k += kColThreads) {
+            const uint32_t rr = k / kChunk, ff = k % kChunk;
+            wsh[ff][rr] = (r0 + rr < R && ff < fc) ? static_cast<int32_t>(W[uint64_t(r0 + rr) * F + f0 + ff]) : 0;
+        }
+        __syncthreads();
+        if (!live) continue;
+#pragma unroll 4
+        for (uint32_t ff = 0; ff < fc; ++ff) {
+            const int32_t x = static_cast<int32_t>(__ldg(&xs[f0 + ff][c]));  // < 2^30
+#pragma unroll
+            for (int rr = 0; rr < kRowTile32; ++rr) acc[rr] += static_cast<int64_t>(x) * wsh[ff][rr];
+        }
+    }
+    if (!live) return;
+    const Modulus m = modulus_of(d.primes[limb]);
+#pragma unroll
+    for (int rr = 0; rr < kRowTile32; ++rr) {
+        if (r0 + rr >= R) break;
+        const int64_t v = acc[rr];
+        const uint64_t a = reduce_u64(static_cast<uint64_t>(v < 0 ? -v : v), m);
+        outs[r0 + rr][c] = v < 0 ? neg_mod(a, m.q) : a;
+    }
+}
+
 }  // namespace
 
 void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint64_t* const* outs, uint32_t R,
-                        const int64_t* W, uint32_t cts, cudaStream_t s) {
+                        const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s) {
     if (!F || !R) return;
     if (F >= (1u << 17)) throw std::invalid_argument("weighted sums: fan-in above 2^17");
     const BfvDev& d = cx.bfv()->dev;
     const uint64_t cols = uint64_t(cts) * 2 * d.L * d.n;
-    const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + kRowTile - 1) / kRowTile);
-    if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
-    k_weighted_sums<<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+    if (small_weights && cx.primes_small(0, d.L)) {
+        const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads),
+                        (R + kRowTile32 - 1) / kRowTile32);
+        if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
+        k_weighted_sums32<<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+    } else {
+        const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + kRowTile - 1) / kRowTile);
+        if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
+        k_weighted_sums<<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+    }
     LB_KERNEL_DONE();
 }
 
