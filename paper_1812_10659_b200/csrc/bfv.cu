@@ -790,6 +790,14 @@ bool ks_use_tmem() {
     return on;
 }
 
+bool ks_use_planes() {
+    static const bool on = [] {
+        const char* e = std::getenv("LB_KS_PLANES");
+        return e ? e[0] != '0' : true;
+    }();
+    return on;
+}
+
 template <int LOGN, class W>
 void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
     using S = NttShape<LOGN>;
@@ -808,6 +816,32 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_tmem_kernel<LOGN>, d, a));
         launch_counter().fetch_add(1, std::memory_order_relaxed);
         return;
+    }
+    if constexpr (sizeof(W) == 4) {
+        if (d.dnum <= kMaxPlanes && ks_use_planes()) {
+            const size_t smem = size_t(d.dnum) * S::M * sizeof(W);
+            static bool configured32 = false;
+            if (!configured32) {
+                LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kMaxPlanes * S::M * sizeof(W))));
+                configured32 = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * (d.L + d.K) * S::CL));
+            cfg.blockDim = dim3(S::T);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = S::CL;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_planes_kernel<LOGN>, d, a));
+            launch_counter().fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
     }
     const size_t smem = 3ull * S::M * sizeof(W);
     static bool configured = false;

@@ -53,11 +53,12 @@ template <> struct KsTables<uint32_t> {
 // independent (a runtime loop serializes them).
 template <int A, int LOGN, class W, class St>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
-                                           const PairT<W>* w, uint32_t w_stride) {
+                                           const PairT<W>* w, uint32_t w_stride, bool start_sync) {
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); });
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
+                       start_sync);
     } else {
         PairT<W> ww[A];
 #pragma unroll
@@ -74,21 +75,21 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
                 acc += shoup_lazy<W>(v[i], ww[i].x, ww[i].y, q);
             }
             return acc;
-        });
+        }, start_sync);
     }
 }
 
 template <int LOGN, class W, class St>
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
-                                         const PairT<W>* w, uint32_t w_stride) {
+                                         const PairT<W>* w, uint32_t w_stride, bool start_sync = true) {
     switch (A) {
-        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride); break;
-        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride); break;
+        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break;
+        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break; } }
         [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -101,7 +102,7 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
                     v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&src[i * n + x])), wi.x, wi.y, q), two_q);
                 }
                 return v;
-            });
+            }, start_sync);
         }
     }
 }
@@ -191,6 +192,84 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
     // (a scatter) is ordered before the cluster sync inside fwd_core
 }
 
+
+// ---- plane variant (32-bit words, dnum <= 3) ---------------------------------------
+// Same result as ks_inner_kernel. Each foreign digit's transform lands in its
+// own smem plane (dnum x 16 KiB = the accumulator kernel's footprint), so
+// the key inner product runs once at the end with the accumulators in
+// registers (no smem read-modify-write per digit), and transforms after the
+// first skip the start barrier (nothing they overwrite is still being read).
+constexpr uint32_t kMaxPlanes = 3;
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<uint32_t>()) ks_inner_planes_kernel(BfvDev d,
+                                                                                                     KsInnerArgs a) {
+    using S = NttShape<LOGN>;
+    using W = uint32_t;
+    using Pr = uint2;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    W* planes = reinterpret_cast<W*>(smem_raw);
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t id = blockIdx.x / S::CL;
+    const uint32_t c = id / LK, r = id % LK;
+    const PrimeDev& P = d.primes[r];
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const uint64_t n = 1ull << LOGN;
+    const uint32_t xt = rank * S::M + threadIdx.x;
+    int own = -1;
+    bool first = true;
+    for (uint32_t j = 0; j < d.dnum; ++j) {
+        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+        if (r >= lo && r < hi) {
+            own = static_cast<int>(j);
+            continue;
+        }
+        const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
+        fwd_conv<LOGN, W>(planes + j * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, first);
+        first = false;
+    }
+    // acc_h[x] = sum_j v_j[x] * key_j[h][r][x], four elements at a time
+    const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
+    const uint64_t kstride_j = uint64_t(2 * LK) << LOGN, kstride_h = uint64_t(LK) << LOGN;
+    const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+    const uint32_t sbt = swb<W>(threadIdx.x);
+    W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
+    W* out1 = out0 + uint64_t(LK) * n;
+    constexpr int kChunk = 4;
+#pragma unroll
+    for (int e0 = 0; e0 < kE; e0 += kChunk) {
+        W acc0[kChunk] = {}, acc1[kChunk] = {};
+#pragma unroll
+        for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+            if (j >= d.dnum) break;
+            Pr w0[kChunk], w1[kChunk];
+            W v[kChunk];
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                const uint32_t off = (e0 + e) * S::T;
+                w0[e] = __ldg(&key[j * kstride_j + off]);
+                w1[e] = __ldg(&key[j * kstride_j + kstride_h + off]);
+                if (static_cast<int>(j) == own) {
+                    const uint32_t x = xt + off;
+                    v[e] = static_cast<W>(__ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]));
+                } else {
+                    v[e] = reduce_4q<W>(sm_at(planes + j * S::M, sbt, off), q, two_q);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                acc0[e] = add_lazy2<W>(acc0[e], shoup_lazy<W>(v[e], w0[e].x, w0[e].y, q), two_q);
+                acc1[e] = add_lazy2<W>(acc1[e], shoup_lazy<W>(v[e], w1[e].x, w1[e].y, q), two_q);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kChunk; ++e) {
+            out0[(e0 + e) * S::T] = csub<W>(acc0[e], q);
+            out1[(e0 + e) * S::T] = csub<W>(acc1[e], q);
+        }
+    }
+}
 
 // ---- TMEM-accumulator variant ------------------------------------------------------
 // Same algorithm as ks_inner_kernel; the two accumulators of every element

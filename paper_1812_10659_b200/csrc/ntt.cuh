@@ -316,23 +316,31 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // evaluations sits in `sm` (swizzled, values in [0, 4q)).
 // Callers looping over several transforms must cluster-sync between them
 // (peers scatter into this CTA's smem).
+// start_sync = false skips the barrier that protects `sm` from being
+// overwritten while still being read: for callers whose transforms each write
+// a fresh smem plane after a first synchronised one.
 template <int LOGN, class W, class Load>
-__device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load) {
+__device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load,
+                                         bool start_sync = true) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     const PairT<W>* __restrict__ tw = fwd_table<W>(P);
     // Every CTA of the cluster must be running (and done reading its smem)
     // before peers write into it: arrive now, wait before the remote stores.
-    if constexpr (S::CL > 1) cluster_arrive_relaxed();
+    if constexpr (S::CL > 1) {
+        if (start_sync) cluster_arrive_relaxed();
+    }
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
         W r[kE];
 #pragma unroll
         for (int k = 0; k < kE; ++k) r[k] = static_cast<W>(load(rho, k * S::NE));
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
-        if constexpr (S::CL > 1) cluster_wait();
-        else __syncthreads();
+        if (start_sync) {
+            if constexpr (S::CL > 1) cluster_wait();
+            else __syncthreads();
+        }
         const uint32_t sb = swb<W>(rho);  // rho < NE
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
