@@ -204,35 +204,65 @@ __device__ __forceinline__ W reduce_4q(W v, W q, W two_q) {
 
 // Forward radix-2^C pass over one group held in r[0..2^C): global stages
 // s0 .. s0+C-1, B = global block index at stage s0.
-template <int C, class W>
-__device__ __forceinline__ void fwd_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                          W two_q) {
+// The 2^l twiddles of stage l of a group are consecutive table entries at a
+// 2^l-aligned index, so 32-bit (w, w') pairs load two per 16-byte LDG.128.
+template <class W, int COUNT>
+__device__ __forceinline__ void load_twiddles(const PairT<W>* __restrict__ p, PairT<W> (&t)[COUNT]) {
+    if constexpr (sizeof(W) == 4 && COUNT >= 2) {
+        const uint4* v = reinterpret_cast<const uint4*>(p);
 #pragma unroll
-    for (int l = 0; l < C; ++l) {
-        const int half = 1 << (C - 1 - l);
-#pragma unroll
-        for (int k = 0; k < (1 << C); ++k) {
-            if (k & half) continue;
-            const uint32_t idx = (1u << (s0 + l)) + (B << l) + (uint32_t)(k >> (C - l));
-            ct_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
+        for (int i = 0; i < COUNT / 2; ++i) {
+            const uint4 x = __ldg(&v[i]);
+            t[2 * i] = make_uint2(x.x, x.y);
+            t[2 * i + 1] = make_uint2(x.z, x.w);
         }
+    } else {
+#pragma unroll
+        for (int i = 0; i < COUNT; ++i) t[i] = __ldg(&p[i]);
     }
 }
 
-// Inverse pass over one group: stages s0+C-1 down to s0.
+// stage Lv of a radix-2^C group (compile-time Lv so the twiddle array is sized)
+template <int C, int Lv, bool INVERSE, class W>
+__device__ __forceinline__ void group_stage(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                            W two_q) {
+    constexpr int half = 1 << (C - 1 - Lv);
+    PairT<W> t[1 << Lv];
+    load_twiddles<W>(tw + (1u << (s0 + Lv)) + (B << Lv), t);
+#pragma unroll
+    for (int k = 0; k < (1 << C); ++k) {
+        if (k & half) continue;
+        if constexpr (INVERSE)
+            gs_bfly(r[k], r[k + half], t[k >> (C - Lv)], q, two_q);
+        else
+            ct_bfly(r[k], r[k + half], t[k >> (C - Lv)], q, two_q);
+    }
+}
+
+template <int C, int Lv, class W>
+__device__ __forceinline__ void fwd_stages(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                           W two_q) {
+    group_stage<C, Lv, false, W>(r, tw, s0, B, q, two_q);
+    if constexpr (Lv + 1 < C) fwd_stages<C, Lv + 1, W>(r, tw, s0, B, q, two_q);
+}
+
+// stages Lv down to LAST (inclusive)
+template <int C, int Lv, int LAST, class W>
+__device__ __forceinline__ void inv_stages(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                           W two_q) {
+    group_stage<C, Lv, true, W>(r, tw, s0, B, q, two_q);
+    if constexpr (Lv > LAST) inv_stages<C, Lv - 1, LAST, W>(r, tw, s0, B, q, two_q);
+}
+
+template <int C, class W>
+__device__ __forceinline__ void fwd_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
+                                          W two_q) {
+    fwd_stages<C, 0, W>(r, tw, s0, B, q, two_q);
+}
 template <int C, class W>
 __device__ __forceinline__ void inv_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
                                           W two_q) {
-#pragma unroll
-    for (int l = C - 1; l >= 0; --l) {
-        const int half = 1 << (C - 1 - l);
-#pragma unroll
-        for (int k = 0; k < (1 << C); ++k) {
-            if (k & half) continue;
-            const uint32_t idx = (1u << (s0 + l)) + (B << l) + (uint32_t)(k >> (C - l));
-            gs_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
-        }
-    }
+    inv_stages<C, C - 1, 0, W>(r, tw, s0, B, q, two_q);
 }
 
 // One local radix-2^C pass over the CTA's smem chunk (global stages
@@ -464,15 +494,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         }
         // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
 #pragma unroll
-        for (int l = kLogE - 1; l >= 1; --l) {
-            const int half = 1 << (kLogE - 1 - l);
-#pragma unroll
-            for (int k = 0; k < kE; ++k) {
-                if (k & half) continue;
-                const uint32_t idx = (1u << l) + (uint32_t)(k >> (kLogE - l));
-                gs_bfly(r[k], r[k + half], __ldg(&tw[idx]), q, two_q);
-            }
-        }
+        inv_stages<kLogE, kLogE - 1, 1, W>(r, tw, 0, 0, q, two_q);
         constexpr int half0 = kE / 2;
         PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
         const PairT<W>* last = nullptr;
