@@ -160,30 +160,43 @@ __device__ __forceinline__ uint64_t scaled_message(const BfvDev& d, uint32_t j, 
     return add_mod(mul_mod(d.delta[j * d.L + i], mval, qm), reduce_u64(extra, qm), qm.q);
 }
 
-// c0 (coefficient domain) = e + round(Q m / t); m: [count][n] mod t_j
+// c0 (coefficient domain) = e + round(Q m / t); m: [count][n] mod t_j. One
+// thread per coefficient: the error sample and the rounding term
+// floor(([Q]_t m + t/2) / t) (a 64-bit division) are limb-independent, so
+// they are computed once and the thread walks the L limbs.
 __global__ void k_enc_coeffs(BfvDev d, const uint64_t* __restrict__ mcoef, uint32_t count, uint64_t id_base,
                              uint64_t* __restrict__ ct) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * d.L * d.n) return;
+    if (idx >= uint64_t(count) * d.n) return;
     const uint32_t k = idx % d.n;
-    const uint32_t i = (idx / d.n) % d.L;
-    const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    const uint64_t c = idx / d.n;
     const uint32_t j = c % d.T;
-    const Modulus qm = modulus_of(d.primes[i]);
     const int64_t e = sample_cbd21(prng_at(stream_key(d.seed, stream_enc_e(id_base + c)), k));
-    const uint64_t v = add_mod(reduce_signed(e, qm), scaled_message(d, j, i, mcoef[c * d.n + k], qm), qm.q);
-    ct[(c * 2 * d.L + i) * d.n + k] = v;
+    const uint64_t mval = mcoef[c * d.n + k];
+    const uint64_t t = d.primes[d.tbase + j].q;
+    const uint64_t extra = (d.q_mod_t[j] * mval + (t >> 1)) / t;
+    uint64_t* out = ct + c * 2 * d.L * d.n + k;
+    for (uint32_t i = 0; i < d.L; ++i) {
+        const Modulus qm = modulus_of(d.primes[i]);
+        const uint64_t sm = add_mod(mul_mod(d.delta[j * d.L + i], mval, qm), reduce_u64(extra, qm), qm.q);
+        out[uint64_t(i) * d.n] = add_mod(reduce_signed(e, qm), sm, qm.q);
+    }
 }
 
 // c1 = a (sampled in the evaluation domain), c0 = NTT(e + round(Qm/t)) - a s
+// (blocks never straddle a row: n is a multiple of the block size, so the
+// row's PRNG stream key is derived once per block)
 __global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, uint64_t* __restrict__ ct) {
+    __shared__ uint64_t key_sh;
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(count) * d.L * d.n) return;
     const uint32_t pos = idx % d.n;
     const uint32_t i = (idx / d.n) % d.L;
     const uint64_t c = idx / (uint64_t(d.n) * d.L);
+    if (threadIdx.x == 0) key_sh = stream_key(d.seed, stream_enc_a(id_base + c, i));
+    __syncthreads();
+    if (idx >= uint64_t(count) * d.L * d.n) return;
     const Modulus qm = modulus_of(d.primes[i]);
-    const uint64_t a = sample_uniform(qm.q, prng_at(stream_key(d.seed, stream_enc_a(id_base + c, i)), pos));
+    const uint64_t a = sample_uniform(qm.q, prng_at(key_sh, pos));
     uint64_t* c0 = ct + (c * 2 * d.L + i) * d.n;
     uint64_t* c1 = c0 + uint64_t(d.L) * d.n;
     c1[pos] = a;
@@ -978,7 +991,7 @@ void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_b
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
-    k_enc_coeffs<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, m.get(), count, id_base, out);
+    k_enc_coeffs<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, id_base, out);
     LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{out, count, L, 0, 2ull * L * n}, s);
     k_enc_finish<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, count, id_base, out);
