@@ -357,6 +357,10 @@ __global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, 
 // ---- multiplication (§3.6) ----
 // exact centered extension from `F` primes (table offset fbase) to `G`
 // primes (table offset gbase); src: [polys][F][n] coeff, dst: [polys][G][n]
+// SMALL: every F and G prime below 2^30, so y_i [F/f_i]_g < 2^60 and up to
+// 16 of them sum exactly in 64 bits (one reduction per output instead of a
+// 128-bit accumulator); y stays in registers (unrolled over the 16-prime cap).
+template <bool SMALL>
 __global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint32_t polys, uint32_t F, uint32_t fbase,
                                const uint64_t* __restrict__ hat_inv, const ulonglong2* __restrict__ frac,
                                const uint64_t* __restrict__ hat_mod /*[F][G]*/, const uint64_t* __restrict__ prod_mod /*[G]*/,
@@ -365,9 +369,12 @@ __global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint3
     if (idx >= uint64_t(polys) * d.n) return;
     const uint32_t k = idx % d.n;
     const uint64_t p = idx / d.n;
-    uint64_t y[16];
+    constexpr int kMax = 16;
+    uint64_t y[kMax];
     uint64_t S_hi = 0, S_lo = 0;
-    for (uint32_t i = 0; i < F; ++i) {
+#pragma unroll
+    for (int i = 0; i < kMax; ++i) {
+        if (i >= F) break;
         const Modulus fm = modulus_of(d.primes[fbase + i]);
         y[i] = mul_mod(src[(p * F + i) * d.n + k], hat_inv[i], fm);
         uint64_t ip, fp;
@@ -378,9 +385,24 @@ __global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint3
     const uint64_t v = S_hi + (S_lo >> 63);  // round(sum y_i / f_i)
     for (uint32_t m = 0; m < G; ++m) {
         const Modulus gm = modulus_of(d.primes[gbase + m]);
-        Acc128 acc;
-        for (uint32_t i = 0; i < F; ++i) acc.mac(y[i], hat_mod[i * G + m]);
-        const uint64_t s = reduce_acc(acc, gm);
+        uint64_t s;
+        if constexpr (SMALL) {
+            uint64_t acc = 0;
+#pragma unroll
+            for (int i = 0; i < kMax; ++i) {
+                if (i >= F) break;
+                acc += y[i] * hat_mod[i * G + m];
+            }
+            s = reduce_u64(acc, gm);
+        } else {
+            Acc128 acc;
+#pragma unroll
+            for (int i = 0; i < kMax; ++i) {
+                if (i >= F) break;
+                acc.mac(y[i], hat_mod[i * G + m]);
+            }
+            s = reduce_acc(acc, gm);
+        }
         dst[(p * G + m) * d.n + k] = sub_mod(s, mul_mod(reduce_u64(v, gm), prod_mod[m], gm), gm.q);
     }
 }
@@ -1144,7 +1166,8 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     cx.ntt_inverse(LimbBatch{X.get(), count * 4, L, 0, LN}, s);
     // (b) exact Q -> B, (c) to evaluations
     DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
-    k_exact_extend<<<grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(
+    const bool small = cx.bfv()->qb_small;
+    (small ? k_exact_extend<true> : k_exact_extend<false>)<<<grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(
         d, X.get(), count * 4, L, 0, d.qhat_inv, d.q_frac, d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
     LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
@@ -1163,7 +1186,7 @@ void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, ui
     k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
     LB_KERNEL_DONE();
     DeviceBuffer E(uint64_t(count) * 3 * LN * 8, s);
-    k_exact_extend<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
+    (small ? k_exact_extend<true> : k_exact_extend<false>)<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
         d, Z.get(), count * 3, M, d.bbase, d.bhat_inv, d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, E.get());
     LB_KERNEL_DONE();
     cx.ntt_forward(LimbBatch{E.get(), count * 3, L, 0, LN}, s);
