@@ -148,8 +148,16 @@ void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaSt
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(limbs * S::CL));
     cfg.blockDim = dim3(S::T);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = inverse ? ntt_inverse_smem<LOGN, W>() : 0;
     cfg.stream = s;
+    if (inverse) {
+        static const bool configured = [] {
+            LB_CUDA(cudaFuncSetAttribute(ntt_inverse_kernel<LOGN, W, St>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(ntt_inverse_smem<LOGN, W>())));
+            return true;
+        }();
+        (void)configured;
+    }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = S::CL;

@@ -53,12 +53,12 @@ template <> struct KsTables<uint32_t> {
 // independent (a runtime loop serializes them).
 template <int A, int LOGN, class W, class St>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
-                                           const PairT<W>* w, uint32_t w_stride, bool start_sync) {
+                                           const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc) {
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
-                       start_sync);
+                       start_sync, xc);
     } else {
         PairT<W> ww[A];
 #pragma unroll
@@ -75,21 +75,22 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
                 acc += shoup_lazy<W>(v[i], ww[i].x, ww[i].y, q);
             }
             return acc;
-        }, start_sync);
+        }, start_sync, xc);
     }
 }
 
 template <int LOGN, class W, class St>
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
-                                         const PairT<W>* w, uint32_t w_stride, bool start_sync = true) {
+                                         const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
+                                         Xchg xc = Xchg{}) {
     switch (A) {
-        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break;
-        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break;
+        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break;
+        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; } }
         [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -102,7 +103,7 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
                     v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&src[i * n + x])), wi.x, wi.y, q), two_q);
                 }
                 return v;
-            }, start_sync);
+            }, start_sync, xc);
         }
     }
 }
@@ -162,6 +163,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
             }
         }
     };
+    __shared__ uint64_t mbar;
+    Xchg xc = xchg_init<S::CL>(&mbar, 1);
     for (uint32_t j = 0; j < d.dnum; ++j) {
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         if (r >= lo && r < hi) {
@@ -175,7 +178,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         // src limbs hold y_i = [d_i (D_j/q_i)^-1]_{q_i} (a single-prime digit:
         // d itself); ModUp = sum_i y_i [D_j/q_i]_r computed in the loader
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
-        fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK);
+        fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, true, xc);
+        xc.parity ^= 1;  // the same plane (and mbarrier) serves every digit
         const uint32_t sbt = swb<W>(threadIdx.x);
         mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm_at(sm, sbt, y - threadIdx.x), q, two_q); });
     }
@@ -219,6 +223,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<uint32_t>()) 
     const uint32_t xt = rank * S::M + threadIdx.x;
     int own = -1;
     bool first = true;
+    __shared__ uint64_t mbar[kMaxPlanes];
+    const Xchg xc0 = xchg_init<S::CL>(mbar, kMaxPlanes);
     for (uint32_t j = 0; j < d.dnum; ++j) {
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         if (r >= lo && r < hi) {
@@ -226,7 +232,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<uint32_t>()) 
             continue;
         }
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
-        fwd_conv<LOGN, W>(planes + j * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, first);
+        const Xchg xc{xc0.mbar ? xc0.mbar + 8 * j : 0u, 0u};
+        fwd_conv<LOGN, W>(planes + j * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, first, xc);
         first = false;
     }
     // acc_h[x] = sum_j v_j[x] * key_j[h][r][x], four elements at a time
@@ -381,6 +388,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     };
+    __shared__ uint64_t mbar;
+    Xchg xc = xchg_init<S::CL>(&mbar, 1);
     for (uint32_t j = 0; j < d.dnum; ++j) {
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         const bool first = j == 0;
@@ -392,7 +401,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
             continue;
         }
         const uint64_t* src = static_cast<const uint64_t*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
-        fwd_conv<LOGN, uint64_t>(sm, P, rank, src, hi - lo, d.dhat_mod_sh + lo * LK + r, LK);
+        fwd_conv<LOGN, uint64_t>(sm, P, rank, src, hi - lo, d.dhat_mod_sh + lo * LK + r, LK, true, xc);
+        xc.parity ^= 1;
         mac_all(j, first, [&](uint32_t y, uint32_t) { return reduce_4q<uint64_t>(sm[swz(y)], q, two_q); });
     }
     uint64_t* out0 = static_cast<uint64_t*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
@@ -446,7 +456,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
     // K == 1: [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced;
     // else the P limbs already hold y_l = [acc_l (P/p_l)^-1]_{p_l} (folded
     // into the inverse transform) and the loader forms sum_l y_l [P/p_l]_{q_r}
-    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L);
+    __shared__ uint64_t mbar;
+    const Xchg xc = xchg_init<S::CL>(&mbar, 1);
+    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
     const uint32_t cta_base = rank * S::M;
     const W* accq = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + r) * n;
     const uint64_t* add = h ? a.add1 : a.add0;

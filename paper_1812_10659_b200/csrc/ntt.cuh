@@ -336,6 +336,79 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
 
+// ---- transaction-count mbarriers for the cross-CTA pass ------------------------------
+// The forward transform's first pass scatters every thread's 16 outputs over
+// the cluster. Instead of a cluster-wide barrier (release fence + all-CTA
+// rendezvous) after the scatter, remote values travel as st.async stores
+// that complete_tx on the RECEIVER's mbarrier; each CTA waits only until its
+// own chunk has arrived (its threads' local stores counted as arrivals).
+#ifndef LB_NTT_MBAR
+#define LB_NTT_MBAR 1
+#endif
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+// makes mbarrier inits visible to the cluster (pairs with the start barrier)
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, uint32_t v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(raddr), "r"(v),
+                 "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, uint64_t v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr), "l"(v),
+                 "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t m) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t m, uint32_t tx) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(m), "r"(tx)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n LB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LB_WAIT_%=;\n}\n" ::"r"(m),
+        "r"(parity)
+        : "memory");
+}
+
+// Exchange state of one forward transform: this CTA's mbarrier (shared
+// address; 0 = use the cluster barrier instead) and the phase parity to wait
+// for. Kernels init one mbarrier per concurrently live smem plane with
+// count = threads per CTA before their first transform.
+struct Xchg {
+    uint32_t mbar = 0;
+    uint32_t parity = 0;
+};
+
+// Thread 0 inits `count` mbarriers (expected arrivals: every thread of the
+// CTA); visible to the cluster after the first transform's start barrier.
+// Returns the exchange state of mbarrier 0 (none for single-CTA limbs).
+template <int CL>
+__device__ __forceinline__ Xchg xchg_init(uint64_t* mbar, int count) {
+    if constexpr (CL > 1 && LB_NTT_MBAR) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < count; ++i) mbar_init(&mbar[i], blockDim.x);
+            mbar_fence_init();
+        }
+        return Xchg{smem_addr(mbar), 0};
+    } else {
+        return Xchg{};
+    }
+}
+
 // Forward transform core, shared by the plain and the fused kernels. The
 // cluster's CTAs cooperatively transform one limb: `load(rho, off)` supplies
 // input coefficient rho + off (any value < 4q, so loaders may skip their
@@ -351,7 +424,7 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // a fresh smem plane after a first synchronised one.
 template <int LOGN, class W, class Load>
 __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load,
-                                         bool start_sync = true) {
+                                         bool start_sync = true, Xchg xc = Xchg{}) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
     const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -372,22 +445,50 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
             else __syncthreads();
         }
         const uint32_t sb = swb<W>(rho);  // rho < NE
+        if constexpr (S::CL > 1 && LB_NTT_MBAR) {
+            const uint32_t lbase = smem_addr(sm);
 #pragma unroll
-        for (int k = 0; k < kE; ++k) {
-            const uint32_t dst = k / S::PER_CTA;
-            const uint32_t c = (k % S::PER_CTA) * S::NE;
-            if constexpr (S::CL > 1) {
-                W* remote = cg::this_cluster().map_shared_rank(sm, dst);
-                sm_at(remote, sb, c) = r[k];
-            } else {
-                sm_at(sm, sb, c) = r[k];
+            for (int dst = 0; dst < S::CL; ++dst) {
+                if (dst == static_cast<int>(rank)) {
+#pragma unroll
+                    for (int i = 0; i < S::PER_CTA; ++i) sm_at(sm, sb, i * S::NE) = r[dst * S::PER_CTA + i];
+                } else {
+                    const uint32_t rbase = mapa_rank(lbase, dst), rmbar = mapa_rank(xc.mbar, dst);
+#pragma unroll
+                    for (int i = 0; i < S::PER_CTA; ++i)
+                        st_async(rbase + (sb ^ swb<W>(i * S::NE)), r[dst * S::PER_CTA + i], rmbar);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                const uint32_t dst = k / S::PER_CTA;
+                const uint32_t c = (k % S::PER_CTA) * S::NE;
+                if constexpr (S::CL > 1) {
+                    W* remote = cg::this_cluster().map_shared_rank(sm, dst);
+                    sm_at(remote, sb, c) = r[k];
+                } else {
+                    sm_at(sm, sb, c) = r[k];
+                }
             }
         }
     }
-    if constexpr (S::CL > 1)
-        cg::this_cluster().sync();
-    else
+    if constexpr (S::CL > 1) {
+        if constexpr (LB_NTT_MBAR) {
+            // remote bytes this CTA receives: PER_CTA words from every thread of
+            // every peer
+            constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+            if (threadIdx.x == 0)
+                mbar_arrive_tx(xc.mbar, kRemoteBytes);
+            else
+                mbar_arrive(xc.mbar);
+            mbar_wait(xc.mbar, xc.parity);
+        } else {
+            cg::this_cluster().sync();
+        }
+    } else {
         __syncthreads();
+    }
     const uint32_t cta_base = rank * S::M;
 #pragma unroll
     for (int s0 = kLogE; s0 < LOGN; s0 += kLogE) {
@@ -417,7 +518,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     if (pidx < 0) return;  // whole cluster skips together
     const PrimeDev& P = primes[pidx];
     St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
-    fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); });
+    __shared__ uint64_t mbar;
+    const Xchg xc = xchg_init<S::CL>(&mbar, 1);
+    fwd_core<LOGN>(
+        sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); }, true, xc);
     // Coalesced store of the CTA's chunk, fully reduced.
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     St* out = a + rank * S::M;
@@ -429,15 +533,33 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     }
 }
 
+// Inverse transform. With LB_NTT_MBAR the cross-CTA pass is push-based: the
+// last local pass (stages 7..4) sends its outputs straight from registers to
+// the owning CTA's receive plane (st.async + complete_tx), so the owner waits
+// on its own mbarrier instead of two cluster-wide barriers around remote
+// loads. Dynamic smem: M words (+ M receive words when pushing).
+template <int LOGN> constexpr bool inv_push() { return NttShape<LOGN>::CL > 1 && LB_NTT_MBAR; }
+template <int LOGN, class W> constexpr size_t ntt_inverse_smem() {
+    return (inv_push<LOGN>() ? 2 : 1) * NttShape<LOGN>::M * sizeof(W);
+}
+
 template <int LOGN, class W, class St = uint64_t>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
-    __shared__ __align__(16) W sm[S::M];
+    constexpr bool kPush = inv_push<LOGN>();
+    extern __shared__ __align__(16) uint8_t inv_smem_raw[];
+    W* sm = reinterpret_cast<W*>(inv_smem_raw);
+    W* recv = sm + S::M;  // receive plane [kE][T] (push only)
+    __shared__ uint64_t mbar;
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t limb_id = blockIdx.x / S::CL;
     const int pidx = prime_index(b, limb_id);
     if (pidx < 0) return;  // whole cluster skips together
+    if constexpr (kPush) {
+        xchg_init<S::CL>(&mbar, 1);
+        cluster_arrive_relaxed();  // peers may push once every mbarrier is initialised
+    }
     const PrimeDev& P = primes[pidx];
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
@@ -469,17 +591,53 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
         __syncthreads();
     }
+    constexpr int kLastLocal = kPush ? 2 * kLogE : kLogE;  // the push pass handles s0 = kLogE itself
 #pragma unroll
-    for (int s0 = LOGN - kTail - kLogE; s0 >= kLogE; s0 -= kLogE) {
+    for (int s0 = LOGN - kTail - kLogE; s0 >= kLastLocal; s0 -= kLogE) {
         local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
-    if constexpr (S::CL > 1) cg::this_cluster().sync();
 
-    // Cross-CTA pass: stages 3..0 gathered from the owners, n^-1 folded in.
-    {
-        const uint32_t rho = rank * S::T + threadIdx.x;
-        W r[kE];
+    // Cross-CTA pass: stages 3..0 over the elements rho + k * NE, n^-1 folded in.
+    const uint32_t rho = rank * S::T + threadIdx.x;
+    W r[kE];
+    if constexpr (kPush) {
+        // stages 7..4 (s0 = kLogE, one radix-16 group per thread): block bb,
+        // offset o; element k (chunk index bb*NE + o + k*stride) belongs to
+        // CTA k / PER_CTA, thread o + (k % PER_CTA) * stride, slot
+        // (rank * PER_CTA + bb) of its receive plane
+        constexpr uint32_t stride = S::N >> (2 * kLogE);
+        static_assert(S::T % stride == 0 && S::T / stride == S::PER_CTA, "push layout");
+        const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
+        const uint32_t sb = swb<W>(bb * S::NE + o);
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[k] = sm_at(sm, sb, k * stride);
+        inv_group<kLogE>(r, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
+        cluster_wait();
+        const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
+        const uint32_t lrecv = smem_addr(recv + slot);
+#pragma unroll
+        for (int dst = 0; dst < S::CL; ++dst) {
+            if (dst == static_cast<int>(rank)) {
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i) recv[slot + i * stride] = r[dst * S::PER_CTA + i];
+            } else {
+                const uint32_t rb = mapa_rank(lrecv, dst), rm = mapa_rank(smem_addr(&mbar), dst);
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i)
+                    st_async(rb + i * stride * static_cast<uint32_t>(sizeof(W)), r[dst * S::PER_CTA + i], rm);
+            }
+        }
+        constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+        if (threadIdx.x == 0)
+            mbar_arrive_tx(smem_addr(&mbar), kRemoteBytes);
+        else
+            mbar_arrive(smem_addr(&mbar));
+        mbar_wait(smem_addr(&mbar), 0);
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[k] = recv[k * S::T + threadIdx.x];
+    } else {
+        if constexpr (S::CL > 1) cg::this_cluster().sync();
         const uint32_t sb = swb<W>(rho);  // rho < NE
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
@@ -492,8 +650,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
                 r[k] = sm_at(sm, sb, c);
             }
         }
+    }
+    {
         // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
-#pragma unroll
         inv_stages<kLogE, kLogE - 1, 1, W>(r, tw, 0, 0, q, two_q);
         constexpr int half0 = kE / 2;
         PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
@@ -518,7 +677,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
 #pragma unroll
         for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
     }
-    if constexpr (S::CL > 1) {  // keep smem alive for peers
+    if constexpr (S::CL > 1 && !kPush) {  // keep smem alive for peers' remote loads
         cluster_arrive_relaxed();
         cluster_wait();
     }
