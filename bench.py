@@ -237,6 +237,23 @@ def run_reference(a, world, rank):
 
 # ---- our arm -----------------------------------------------------------------------------
 
+TRAFFIC_JSON = ROOT / "profiles" / "ncu_traffic.json"
+
+
+def ncu_traffic(match) -> tuple[float | None, str | None]:
+    """DRAM bytes per unit (ciphertext or limb) summed over the committed ncu
+    --set full captures whose kernel name satisfies `match` (written by
+    profiles/traffic_from_ncu.py); (None, None) when absent."""
+    try:
+        d = json.loads(TRAFFIC_JSON.read_text())
+    except Exception:
+        return None, None
+    ks = {k: v for k, v in d["kernels"].items() if match(k)}
+    if not ks:
+        return None, None
+    return sum(v["bytes_per_unit"] for v in ks.values()), f"{TRAFFIC_JSON.relative_to(ROOT)}: " + ", ".join(sorted(ks))
+
+
 def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
     """Dominant kernel (batched NTT at n=16384, the workload's word size)
     timed alone with CUDA events on its launch stream, against the measured
@@ -274,13 +291,16 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
+    per_limb, src = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned long>")) \
+        if word == 32 else (None, None)
     return {
         "kernel": f"ntt_forward_kernel<14, u{word}> ({polys * L} limbs of n={n}, "
                   f"{max(cx.params.q).bit_length()}-bit q, {word}-bit words)",
         "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
         "frac": achieved / (peak.value / 1e9),
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
-        "traffic": None,
+        "traffic": per_limb * polys * L if per_limb else None,
+        "traffic_source": src,
         "launch_ms": ms,
         "limb_transforms_per_s": polys * L / (ms * 1e-3),
         "hbm_view": {"achieved_gbs": hbm_bytes / (ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
@@ -338,13 +358,18 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     achieved = count * products / (ms * 1e-3) / 1e9
     achieved_bfly = count * bfly / (ms * 1e-3) / 1e9
     del ct, out
+    ks_names = ("ks_inner", "moddown_kernel", "ntt_inverse_kernel<14, unsigned int, unsigned int>",
+                "ntt_inverse_kernel<14, unsigned int, unsigned long>")
+    per_ct, src = ncu_traffic(lambda k: k.startswith(ks_names)) if word == 32 else (None, None)
     return {
         "kernel": f"key switch = ntt_inverse + ks_inner_kernel + ntt_inverse(P) + moddown_kernel, u{word} words, "
                   f"{count} ciphertext rotations per launch set (n={n}, L={L}, K={K}, dnum={dnum})",
         "bound": "int", "achieved": achieved, "peak": peak_g, "unit": "G Shoup products/s",
         "frac": achieved / peak_g,
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
-        "traffic": None,
+        "traffic": per_ct * count if per_ct else None,
+        "traffic_unit": "bytes per launch set (DRAM read + write)",
+        "traffic_source": src,
         "algorithmic": f"per ciphertext: {transforms} limb transforms ({bfly} butterflies) + {modup} ModUp + "
                        f"{mac} MAC + {moddown} ModDown products",
         "butterflies_only": {"achieved": achieved_bfly, "frac": achieved_bfly / peak_g},

@@ -567,7 +567,36 @@ EncodedTensor matvec_stacked_rowmajor(Evaluator& ev, const EncodedTensor& x, con
     return out;
 }
 
-EncodedTensor conv_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weights& W) {  // kernels.cpp:269-292
+// A stage's full row-major matrix, materialised once per plan (host for the
+// magnitude bookkeeping, device for the kernel).
+struct SimdMatrix {
+    uint64_t rows = 0, cols = 0;
+    std::vector<int64_t> host;
+    DeviceBuffer dev;
+    std::mutex mu;
+};
+
+void materialise(Evaluator& ev, const Weights& W, SimdMatrix& M) {
+    std::lock_guard<std::mutex> lock(M.mu);
+    if (M.dev.get()) return;
+    M.rows = W.rows;
+    M.cols = W.cols;
+    M.host.resize(W.rows * W.cols);
+    for (uint64_t r = 0; r < W.rows; ++r)
+        for (uint64_t c = 0; c < W.cols; ++c) M.host[r * W.cols + c] = W.at(r, c);
+    cudaStream_t s = ev.stream();
+    M.dev = DeviceBuffer(M.host.size() * 8, s);
+    LB_CUDA(cudaMemcpyAsync(M.dev.get(), M.host.data(), M.host.size() * 8, cudaMemcpyHostToDevice, s));
+    LB_CUDA(cudaStreamSynchronize(s));
+    M.dev.rebind(nullptr);  // outlives the session's streams
+}
+
+// Every output map is sum_j W[map][j] * window_j (the reference's
+// mul_scalar + add chain per map, same counters, depths and magnitude checks:
+// Evaluator::weighted_sums replays the chain where a bound would trip); all
+// maps run as one pass over the window messages instead of a
+// read-modify-write of the accumulator per term.
+EncodedTensor conv_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weights& W, SimdMatrix& M) {  // kernels.cpp:269-292
     require(x.rep.kind == RepKind::Convolution, "expected a convolution tensor");
     require(x.messages.size() == x.rep.windows && x.rep.windows >= 1, "window count does not match messages");
     require(W.at && W.rows >= 1, "missing weights");
@@ -580,6 +609,13 @@ EncodedTensor conv_rowmajor(Evaluator& ev, const EncodedTensor& x, const Weights
     if (out.rep.identity_layout()) {
         out.rep.kind = RepKind::Dense;
         out.rep.slot_of.clear();
+    }
+    materialise(ev, W, M);
+    bool small = true;  // weighted_sums' 128-bit bookkeeping takes |w| < 2^31
+    for (int64_t w : M.host) small = small && w > -(int64_t(1) << 31) && w < (int64_t(1) << 31);
+    if (small) {
+        out.messages = ev.weighted_sums(x.messages, W.rows, M.host.data(), M.dev.get<int64_t>());
+        return out;
     }
     FanOut fan(ev, W.rows);
     for (uint64_t map = 0; map < W.rows; ++map) {
@@ -665,35 +701,12 @@ EncodedTensor encode_simd(Evaluator& ev, const int64_t* dev_images, uint64_t fea
     return t;
 }
 
-// A stage's full row-major matrix, materialised once per plan (host for the
-// magnitude bookkeeping, device for the kernel).
-struct SimdMatrix {
-    uint64_t rows = 0, cols = 0;
-    std::vector<int64_t> host;
-    DeviceBuffer dev;
-    std::mutex mu;
-};
-
 EncodedTensor simd_dense(Evaluator& ev, const EncodedTensor& x, const Weights& W, SimdMatrix& M) {  // kernels.cpp:302-318
     require(x.rep.kind == RepKind::Simd, "expected a record tensor");
     require(x.messages.size() == x.rep.length && x.rep.length >= 1, "bad record tensor");
     require(W.at && W.rows >= 1, "missing weights");
     require(W.cols == x.rep.length, "weight columns do not match feature count");
-    {
-        std::lock_guard<std::mutex> lock(M.mu);
-        if (!M.dev.get()) {
-            M.rows = W.rows;
-            M.cols = W.cols;
-            M.host.resize(W.rows * W.cols);
-            for (uint64_t r = 0; r < W.rows; ++r)
-                for (uint64_t c = 0; c < W.cols; ++c) M.host[r * W.cols + c] = W.at(r, c);
-            cudaStream_t s = ev.stream();
-            M.dev = DeviceBuffer(M.host.size() * 8, s);
-            LB_CUDA(cudaMemcpyAsync(M.dev.get(), M.host.data(), M.host.size() * 8, cudaMemcpyHostToDevice, s));
-            LB_CUDA(cudaStreamSynchronize(s));
-            M.dev.rebind(nullptr);  // outlives the session's streams
-        }
-    }
+    materialise(ev, W, M);
     EncodedTensor out;
     out.rep = x.rep;
     out.rep.length = W.rows;
@@ -849,7 +862,9 @@ void build_lola_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp
     };
     add_step(plan, v, p, rep_name(RepKind::Convolution), "weighted sum of window messages per map",
              conv_rowmajor_cost(maps, v),
-             [np](Evaluator& ev, const EncodedTensor& x) { return conv_rowmajor(ev, x, window_rows(np->stages[0])); });
+             [np, M = std::make_shared<SimdMatrix>()](Evaluator& ev, const EncodedTensor& x) {
+                 return conv_rowmajor(ev, x, window_rows(np->stages[0]), *M);
+             });
     const auto offsets = uniform_offsets(static_cast<uint32_t>(maps), static_cast<uint32_t>(p));
     add_step(plan, maps, p, rep_name(RepKind::Dense), "combine " + num(maps) + " messages into one",
              combine_cost(offsets, true), [np, offsets](Evaluator& ev, const EncodedTensor& x) {
@@ -897,7 +912,9 @@ void build_lola_dense_mnist(Plan& plan, const Network& net, uint32_t n) {  // pl
     for (size_t i = 0; i < base.size(); ++i) grid_identity &= base[i] == i;
     add_step(plan, v, p, rep_name(RepKind::Convolution, !grid_identity), "weighted sum of window messages per map",
              conv_rowmajor_cost(maps, v),
-             [np](Evaluator& ev, const EncodedTensor& x) { return conv_rowmajor(ev, x, window_rows(np->stages[0])); });
+             [np, M = std::make_shared<SimdMatrix>()](Evaluator& ev, const EncodedTensor& x) {
+                 return conv_rowmajor(ev, x, window_rows(np->stages[0]), *M);
+             });
     const std::vector<uint32_t> shifts = packing.map_shifts;
     add_step(plan, maps, p, rep_name(grid_identity ? RepKind::Dense : RepKind::Interleaved),
              "combine " + num(maps) + " messages into one", combine_cost(shifts, true),
@@ -947,7 +964,9 @@ void build_lola_cifar(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp
     };
     add_step(plan, v, p, rep_name(RepKind::Convolution, !split_identity), "weighted sum of window messages per map",
              conv_rowmajor_cost(maps, v),
-             [np](Evaluator& ev, const EncodedTensor& x) { return conv_rowmajor(ev, x, window_rows(np->stages[0])); });
+             [np, M = std::make_shared<SimdMatrix>()](Evaluator& ev, const EncodedTensor& x) {
+                 return conv_rowmajor(ev, x, window_rows(np->stages[0]), *M);
+             });
     const auto offsets = uniform_offsets(static_cast<uint32_t>(maps), split);
     add_step(plan, maps, p, part_rep, "combine " + num(maps) + " messages into one", combine_cost(offsets, true),
              [np, offsets](Evaluator& ev, const EncodedTensor& x) {
@@ -1006,7 +1025,9 @@ void build_lola_small(Plan& plan, const Network& net, uint32_t n) {
     };
     add_step(plan, v, p, rep_name(RepKind::Convolution), "weighted sum of window messages per map",
              conv_rowmajor_cost(maps, v),
-             [np](Evaluator& ev, const EncodedTensor& x) { return conv_rowmajor(ev, x, window_rows(np->stages[0])); });
+             [np, M = std::make_shared<SimdMatrix>()](Evaluator& ev, const EncodedTensor& x) {
+                 return conv_rowmajor(ev, x, window_rows(np->stages[0]), *M);
+             });
     const auto offsets = uniform_offsets(static_cast<uint32_t>(maps), static_cast<uint32_t>(p));
     add_step(plan, maps, p, rep_name(RepKind::Dense), "combine " + num(maps) + " messages into one",
              combine_cost(offsets, true), [np, offsets](Evaluator& ev, const EncodedTensor& x) {

@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const u
 
 // 32-bit residues (every q < 2^30) and |W| < 2^15: each product is exact in a
 // signed 64-bit accumulator (|sum| < 2^17 * 2^15 * 2^30 = 2^62), one
-// IMAD.WIDE per term; 16 rows per thread halve the x loads per product.
-constexpr int kRowTile32 = 16;
-
+// IMAD.WIDE per term; up to 16 rows per thread divide the x loads per
+// product (fewer when R is small: the conv layers have 5 maps).
+template <int kRowTile32>
 __global__ void __launch_bounds__(kColThreads) k_weighted_sums32(BfvDev d, const uint64_t* const* __restrict__ xs,
                                                                     uint32_t F, uint64_t* const* __restrict__ outs,
                                                                     uint32_t R, const int64_t* __restrict__ W,
@@ -121,10 +121,15 @@ void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint
     const BfvDev& d = cx.bfv()->dev;
     const uint64_t cols = uint64_t(cts) * 2 * d.L * d.n;
     if (small_weights && cx.primes_small(0, d.L)) {
-        const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads),
-                        (R + kRowTile32 - 1) / kRowTile32);
+        const int tile = R <= 4 ? 4 : R <= 8 ? 8 : 16;
+        const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + tile - 1) / tile);
         if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
-        k_weighted_sums32<<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+        if (tile == 4)
+            k_weighted_sums32<4><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+        else if (tile == 8)
+            k_weighted_sums32<8><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+        else
+            k_weighted_sums32<16><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
     } else {
         const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + kRowTile - 1) / kRowTile);
         if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
