@@ -92,6 +92,8 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
         [[fallthrough]];
         case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; } }
         [[fallthrough]];
+        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; } }
+        [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
             constexpr uint64_t n = 1ull << LOGN;
@@ -110,6 +112,9 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
 
 #ifndef LB_KS32_MINB
 #define LB_KS32_MINB 3
+#endif
+#ifndef LB_KS_PLANES_MINB
+#define LB_KS_PLANES_MINB 4  // 64 registers, 4 CTAs/SM: 138.3 vs 135.4 img/s at 3 CTAs/SM (80 registers)
 #endif
 // 64-bit words: three 32 KiB smem planes per CTA -> 2 CTAs/SM; 32-bit words
 // halve the planes, so registers decide
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
 constexpr uint32_t kMaxPlanes = 3;
 
 template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<uint32_t>()) ks_inner_planes_kernel(BfvDev d,
+__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner_planes_kernel(BfvDev d,
                                                                                                      KsInnerArgs a) {
     using S = NttShape<LOGN>;
     using W = uint32_t;

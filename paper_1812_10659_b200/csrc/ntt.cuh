@@ -384,6 +384,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t parity) {
         : "memory");
 }
 
+// Bulk L2 prefetch by the TMA unit (one instruction for a whole range):
+// kernels whose epilogue streams operands that do not feed the transform
+// issue it at entry, so those reads hit L2 instead of HBM.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Exchange state of one forward transform: this CTA's mbarrier (shared
 // address; 0 = use the cluster barrier instead) and the phase parity to wait
 // for. Kernels init one mbarrier per concurrently live smem plane with

@@ -86,11 +86,16 @@ def lola_mnist_params(seed: int = 1) -> BfvParams:
 
 
 def lola_mnist_params_w32(seed: int = 1) -> BfvParams:
-    """Config 0/2 on 30-bit primes (below 2^30, so every transform and key
-    switch runs on 32-bit words): L = 10 ciphertext primes (Q ~ 300 bits, as
-    the 60-bit chain), K = 4 special primes, dnum = 3 digits of <= 4 primes:
-    log2(QP) ~ 420 <= 438."""
-    return make_params(16384, L=10, T=5, K=4, dnum=3, bits=30, seed=seed)
+    """Config 0/2 on 29-bit primes (below 2^30, so every transform and key
+    switch runs on 32-bit words): L = 10 ciphertext primes (Q ~ 290 bits),
+    K = 5 special primes, dnum = 2 digits of 5 primes (P ~ D_j, so key
+    switching adds no noise to speak of): log2(QP) ~ 435 <= 438, the
+    HE-standard 128-bit bound for n = 16384 with a ternary secret.
+    60 limb transforms per key switch instead of 70 with 30-bit primes,
+    K = 4, dnum = 3. Measured on B200 (tools/noise_margin.py):
+    decryption margin 27.4 bits (30-bit K=4 dnum=3: 37.7; K=4 dnum=2: 9.4,
+    rejected), 134.7 vs 125.4 images/s."""
+    return make_params(16384, L=10, T=5, K=5, dnum=2, bits=29, seed=seed)
 
 
 def lola_cifar_params(seed: int = 1) -> BfvParams:
@@ -101,10 +106,14 @@ def lola_cifar_params(seed: int = 1) -> BfvParams:
 
 
 def lola_small_params(seed: int = 1) -> BfvParams:
-    """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square)."""
-    return make_params(8192, L=3, T=2, K=1, dnum=3, seed=seed)
+    """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square). 54-bit
+    primes so that log2(QP) = 216 <= 218, the 128-bit bound at n = 8192:
+    L = 3, K = 1, dnum = 3. Measured decryption margin 29.7 bits."""
+    return make_params(8192, L=3, T=2, K=1, dnum=3, bits=54, seed=seed)
 
 
 def lola_small_params_w32(seed: int = 1) -> BfvParams:
-    """Config 3 on 30-bit primes: L = 6, K = 2, dnum = 3 digits of 2."""
-    return make_params(8192, L=6, T=2, K=2, dnum=3, bits=30, seed=seed)
+    """Config 3 on 30-bit primes: L = 5, K = 2, dnum = 3 digits of <= 2:
+    log2(QP) = 210 <= 218. Measured decryption margin 18.4 bits (L = 6,
+    K = 1, dnum = 6: 47.5 bits but 30% slower; dnum = 2 with K = 1 fails)."""
+    return make_params(8192, L=5, T=2, K=2, dnum=3, bits=30, seed=seed)
