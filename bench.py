@@ -337,7 +337,7 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     mac = 2 * dnum * (L + K) * n
     moddown = ((K * 2 * L) if K > 1 else 0) * n + 2 * L * n
     products = bfly + modup + mac + moddown
-    ct = torch.randint(0, min(cx.params.q), (count, 2, L, n), dtype=torch.int64, device="cuda")
+    ct = torch.randint(0, min(cx.params.q), (count, 2, L, n), dtype=cx.res_dtype, device="cuda")
     out = torch.empty_like(ct)
     g = galois_exponent_columns(n, 1)
     s = torch.cuda.current_stream()
@@ -506,8 +506,8 @@ def run_ours(a, world, rank, local):
             "data": "synthetic (SplitMix64-seeded pixels and weights)",
             "config": {"workload": f"{strategy} cfg{cfg} batched throughput", "images_per_gpu_per_step": B,
                        "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
-                       "q_bits": max(prm.q).bit_length(), "residue_storage": "u64 in HBM (key-switch "
-                       "intermediates u32 when q_bits <= 30)", "parallelism": f"images sharded over {world} GPU(s), no collective",
+                       "q_bits": max(prm.q).bit_length(), "residue_storage": "u32 words in HBM when every "
+                       "ciphertext and special prime < 2^30, else u64", "parallelism": f"images sharded over {world} GPU(s), no collective",
                        "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes) * world,
                     "d2h_bytes_per_step": int(scores.nbytes) * world},

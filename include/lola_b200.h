@@ -17,7 +17,12 @@
  *       5 plan divergence (std::logic_error).
  *     lb_last_error() returns the message of the calling thread's last error.
  *   - `stream` is a cudaStream_t (NULL = the legacy default stream).
- *   - Device pointers are plain `uint64_t*` into device memory.
+ *   - Device pointers are plain pointers into device memory. Limb batches of
+ *     the NTT engine are `uint64_t*`. Ciphertexts and plaintext operands
+ *     ("residue buffers", `void*` below) hold the context's RESIDUE WORD:
+ *     uint32_t when every ciphertext and special prime is below 2^30 (the
+ *     32-bit word kernels; half the HBM traffic), else uint64_t — see
+ *     lb_context_residue_bytes.
  *   - RNS layout is limb-major: a polynomial is `limbs` contiguous length-n
  *     u64 arrays in [0, q_i); batches of polynomials are contiguous with a
  *     caller-given stride (in elements).
@@ -72,6 +77,9 @@ int lb_find_primes(uint32_t bits, uint32_t log_mod, uint32_t count, const uint64
 int lb_context_create(const lb_params* params, lb_context** out);
 int lb_context_destroy(lb_context* cx);
 int lb_context_prime(const lb_context* cx, uint32_t index, uint64_t* prime, uint64_t* psi);
+/* residue word of the context's ciphertexts and plaintext operands: 4
+ * (uint32_t; every ciphertext and special prime below 2^30) or 8 bytes */
+int lb_context_residue_bytes(const lb_context* cx, uint32_t* bytes);
 int lb_sync(lb_context* cx, void* stream);
 
 /* ---- NTT engine (replaces NttTables::forward / inverse, ring.cpp:97-115) --
@@ -83,7 +91,7 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
                    uint32_t first_prime, uint64_t poly_stride, void* stream);
 
 /* ---- BFV ciphertext operations ---------------------------
- * A ciphertext is [2][L][n] u64 in the evaluation (NTT) domain. A message
+ * A ciphertext is [2][L][n] residue words in the evaluation (NTT) domain. A message
  * is T ciphertexts, one per plaintext CRT prime: [T][2][L][n]; a batch of B
  * messages is [B][T][2][L][n]. Ops on `count` ciphertexts use plaintext prime
  * t_{c mod T} for ciphertext c. Every pointer is device memory; outputs may
@@ -93,44 +101,41 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
  * [B][n] int64 slot values (reduced mod each t_j, slot-encoded with the
  * reference's generator-3 order, ring.cpp:138-144), out [B][T][2][L][n];
  * ciphertext c gets randomness id id_base + c. */
-int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
-                     void* stream);
+int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, void* stream);
 /* decryption + Evaluator::lower's slot decode (evaluator.cpp:98-118, before
  * the CRT join): out [B][T][n] slot residues mod t_j. */
-int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream);
+int lb_decrypt_slots(lb_context* cx, const void* ct, uint32_t B, uint64_t* out, void* stream);
 /* decryption to plaintext coefficients mod t_j, out [B][T][n]. */
-int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream);
+int lb_decrypt_coeffs(lb_context* cx, const void* ct, uint32_t B, uint64_t* out, void* stream);
 /* plaintext operand encoding (plain_limbs + slot_encode, evaluator.cpp:120-135,
  * 166-169, 214-217): values [n] int64; pt_mul, pt_add [T][L][n] (either may
  * be NULL). */
-int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, void* stream);
+int lb_encode_plain(lb_context* cx, const int64_t* values, void* pt_mul, void* pt_add, void* stream);
 
-int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
+int lb_ct_add(lb_context* cx, const void* a, const void* b, void* out, uint32_t count,
               void* stream);                                            /* Evaluator::add */
-int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count,
+int lb_ct_mul_scalar(lb_context* cx, const void* a, int64_t scalar, void* out, uint32_t count,
                      void* stream);                                     /* Evaluator::mul_scalar */
-int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt_mul, uint64_t* out, uint32_t count,
+int lb_ct_mul_plain(lb_context* cx, const void* a, const void* pt_mul, void* out, uint32_t count,
                     void* stream);                                      /* Evaluator::mul_plain / mask */
-int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt_add, uint64_t* out, uint32_t count,
+int lb_ct_add_plain(lb_context* cx, const void* a, const void* pt_add, void* out, uint32_t count,
                     void* stream);                                      /* Evaluator::add_plain */
 /* automorphism x -> x^galois + key switch (galois_apply ring.cpp:155-171 with
  * Evaluator::rotate_columns / rotate_rows / rotate_bundle, evaluator.cpp:260-332) */
-int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count,
-                 void* stream);
+int lb_ct_rotate(lb_context* cx, const void* a, uint64_t galois, void* out, uint32_t count, void* stream);
 /* tensor + relinearization (Evaluator::mul, evaluator.cpp:178-202) */
-int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count,
-              void* stream);
+int lb_ct_mul(lb_context* cx, const void* a, const void* b, void* out, uint32_t count, void* stream);
 
 /* key material: key_id 0 = relinearization (s^2), odd g = Galois key x->x^g.
- * lb_key_pointer returns the device key [dnum][2][L+K][n] (NTT domain). */
+ * lb_key_pointer returns the device key [dnum][2][L+K][n] u64 (NTT domain). */
 int lb_keygen(lb_context* cx, uint64_t key_id, void* stream);
 int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out);
-/* raw pieces: NTT-domain automorphism over [polys][limbs][n] (limb l uses
- * prime l) and key switch of [count][L][n] NTT-domain polys. */
-int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
-                    uint64_t galois, void* stream);
-int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
-                  void* stream);
+/* raw pieces (residue buffers): NTT-domain automorphism over
+ * [polys][limbs][n] (limb l uses prime l) and key switch of [count][L][n]
+ * NTT-domain polys. */
+int lb_automorphism(lb_context* cx, const void* in, void* out, uint32_t polys, uint32_t limbs, uint64_t galois,
+                    void* stream);
+int lb_key_switch(lb_context* cx, const void* d, uint64_t key_id, void* u0, void* u1, uint32_t count, void* stream);
 /* Galois exponents of the reference (ring.cpp:173-184): right shift of both
  * slot rows by k columns, and the row swap. */
 uint64_t lb_galois_exponent_columns(uint32_t n, uint32_t k);
@@ -170,7 +175,7 @@ int lb_message_free(lb_message* m);
 /* depth, plain depth, magnitude bound (decimal) of a message */
 int lb_message_info(const lb_message* m, uint32_t* depth, uint32_t* plain_depth, char* magnitude, uint64_t cap);
 /* device pointer of the message's ciphertexts [batch][T][2][L][n] */
-int lb_message_data(const lb_message* m, const uint64_t** out);
+int lb_message_data(const lb_message* m, const void** out);
 
 /* ---- LoLa layer evaluator (proj/src/representation.cpp, kernels.cpp, plan.cpp) --
  * A network is the already-quantized integer network the reference's
@@ -227,7 +232,7 @@ int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters);
 int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device);
 /* device pointer of encrypted output message `index` ([batch][T][2][L][n])
  * and the number of output messages (either pointer may be NULL) */
-int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const uint64_t** data, uint32_t* count);
+int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const void** data, uint32_t* count);
 
 /* ---- measurement ------------------------------------------------------- */
 

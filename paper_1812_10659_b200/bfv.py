@@ -1,9 +1,12 @@
 """Ciphertext-level host API over the C-ABI (include/lola_b200.h, §BFV).
 
-Tensors are torch int64 CUDA tensors (all residues < 2^62):
+Ciphertexts and plaintext operands are torch CUDA tensors of the context's
+residue word (`BfvContext.res_dtype`): int32 when every ciphertext and
+special prime is below 2^30 (the 32-bit word kernels), else int64:
     ciphertext batch   [count][2][L][n]  (count = B * T, message-major)
     message batch      [B][T][2][L][n]
     plaintext operand  [T][L][n]
+Slot values, decrypted residues and keys are int64.
 Every method raises on a nonzero C-ABI status; there is no CPU path.
 """
 from __future__ import annotations
@@ -25,9 +28,9 @@ class _DevPtr:
                                          "strides": None}
 
 
-def _ptr(t: torch.Tensor) -> int:
-    if not (t.is_cuda and t.is_contiguous() and t.dtype == torch.int64):
-        raise ValueError("expected a contiguous int64 CUDA tensor")
+def _ptr(t: torch.Tensor, dtype=torch.int64) -> int:
+    if not (t.is_cuda and t.is_contiguous() and t.dtype == dtype):
+        raise ValueError(f"expected a contiguous {dtype} CUDA tensor")
     return t.data_ptr()
 
 
@@ -37,13 +40,20 @@ class BfvContext(Context):
         self.L, self.K, self.T = len(params.q), len(params.p), len(params.t)
         self.M = len(params.b)
         self.dnum = params.dnum or self.L
+        rb = C.c_uint32()
+        nat.call("lb_context_residue_bytes", self.handle, C.byref(rb))
+        self.res_dtype = torch.int32 if rb.value == 4 else torch.int64
 
     # ---- shapes ---------------------------------------------------------------
     def ct_shape(self, count: int) -> tuple:
         return (count, 2, self.L, self.n)
 
     def empty_cts(self, count: int) -> torch.Tensor:
-        return torch.empty(self.ct_shape(count), dtype=torch.int64, device="cuda")
+        return torch.empty(self.ct_shape(count), dtype=self.res_dtype, device="cuda")
+
+    def _r(self, t: torch.Tensor) -> int:
+        """Device pointer of a residue tensor (ciphertexts, plaintext operands)."""
+        return _ptr(t, self.res_dtype)
 
     def _count(self, ct: torch.Tensor) -> int:
         per = 2 * self.L * self.n
@@ -55,27 +65,27 @@ class BfvContext(Context):
     def encrypt_slots(self, values: torch.Tensor, id_base: int = 0, stream=None) -> torch.Tensor:
         values = values.reshape(-1, self.n).contiguous()
         B = values.shape[0]
-        out = torch.empty((B, self.T, 2, self.L, self.n), dtype=torch.int64, device="cuda")
-        nat.call("lb_encrypt_slots", self.handle, _ptr(values), B, id_base, _ptr(out), _stream_ptr(stream))
+        out = torch.empty((B, self.T, 2, self.L, self.n), dtype=self.res_dtype, device="cuda")
+        nat.call("lb_encrypt_slots", self.handle, _ptr(values), B, id_base, self._r(out), _stream_ptr(stream))
         return out
 
     def decrypt_slots(self, ct: torch.Tensor, stream=None) -> torch.Tensor:
         B = self._count(ct) // self.T
         out = torch.empty((B, self.T, self.n), dtype=torch.int64, device="cuda")
-        nat.call("lb_decrypt_slots", self.handle, _ptr(ct), B, _ptr(out), _stream_ptr(stream))
+        nat.call("lb_decrypt_slots", self.handle, self._r(ct), B, _ptr(out), _stream_ptr(stream))
         return out
 
     def decrypt_coeffs(self, ct: torch.Tensor, stream=None) -> torch.Tensor:
         B = self._count(ct) // self.T
         out = torch.empty((B, self.T, self.n), dtype=torch.int64, device="cuda")
-        nat.call("lb_decrypt_coeffs", self.handle, _ptr(ct), B, _ptr(out), _stream_ptr(stream))
+        nat.call("lb_decrypt_coeffs", self.handle, self._r(ct), B, _ptr(out), _stream_ptr(stream))
         return out
 
     def encode_plain(self, values: torch.Tensor, mul: bool = True, add: bool = True, stream=None):
         values = values.reshape(self.n).contiguous()
         shape = (self.T, self.L, self.n)
-        pm = torch.empty(shape, dtype=torch.int64, device="cuda") if mul else None
-        pa = torch.empty(shape, dtype=torch.int64, device="cuda") if add else None
+        pm = torch.empty(shape, dtype=self.res_dtype, device="cuda") if mul else None
+        pa = torch.empty(shape, dtype=self.res_dtype, device="cuda") if add else None
         nat.call("lb_encode_plain", self.handle, _ptr(values), pm.data_ptr() if mul else None,
                  pa.data_ptr() if add else None, _stream_ptr(stream))
         return pm, pa
@@ -83,29 +93,29 @@ class BfvContext(Context):
     # ---- ciphertext ops --------------------------------------------------------
     def _unary(self, name, a, *extra, out=None, stream=None):
         out = torch.empty_like(a) if out is None else out
-        nat.call(name, self.handle, _ptr(a), *extra, _ptr(out), self._count(a), _stream_ptr(stream))
+        nat.call(name, self.handle, self._r(a), *extra, self._r(out), self._count(a), _stream_ptr(stream))
         return out
 
     def add(self, a, b, out=None, stream=None):
         out = torch.empty_like(a) if out is None else out
-        nat.call("lb_ct_add", self.handle, _ptr(a), _ptr(b), _ptr(out), self._count(a), _stream_ptr(stream))
+        nat.call("lb_ct_add", self.handle, self._r(a), self._r(b), self._r(out), self._count(a), _stream_ptr(stream))
         return out
 
     def mul_scalar(self, a, s: int, out=None, stream=None):
         return self._unary("lb_ct_mul_scalar", a, int(s), out=out, stream=stream)
 
     def mul_plain(self, a, pt_mul, out=None, stream=None):
-        return self._unary("lb_ct_mul_plain", a, _ptr(pt_mul), out=out, stream=stream)
+        return self._unary("lb_ct_mul_plain", a, self._r(pt_mul), out=out, stream=stream)
 
     def add_plain(self, a, pt_add, out=None, stream=None):
-        return self._unary("lb_ct_add_plain", a, _ptr(pt_add), out=out, stream=stream)
+        return self._unary("lb_ct_add_plain", a, self._r(pt_add), out=out, stream=stream)
 
     def rotate(self, a, galois: int, out=None, stream=None):
         return self._unary("lb_ct_rotate", a, int(galois), out=out, stream=stream)
 
     def mul(self, a, b, out=None, stream=None):
         out = torch.empty_like(a) if out is None else out
-        nat.call("lb_ct_mul", self.handle, _ptr(a), _ptr(b), _ptr(out), self._count(a), _stream_ptr(stream))
+        nat.call("lb_ct_mul", self.handle, self._r(a), self._r(b), self._r(out), self._count(a), _stream_ptr(stream))
         return out
 
     # ---- keys / raw pieces ------------------------------------------------------
@@ -122,13 +132,14 @@ class BfvContext(Context):
     def automorphism(self, a: torch.Tensor, galois: int, limbs: int, stream=None) -> torch.Tensor:
         out = torch.empty_like(a)
         polys = a.numel() // (limbs * self.n)
-        nat.call("lb_automorphism", self.handle, _ptr(a), _ptr(out), polys, limbs, galois, _stream_ptr(stream))
+        nat.call("lb_automorphism", self.handle, self._r(a), self._r(out), polys, limbs, galois, _stream_ptr(stream))
         return out
 
     def key_switch(self, d: torch.Tensor, key_id: int, stream=None):
         count = d.numel() // (self.L * self.n)
         u0, u1 = torch.empty_like(d), torch.empty_like(d)
-        nat.call("lb_key_switch", self.handle, _ptr(d), key_id, _ptr(u0), _ptr(u1), count, _stream_ptr(stream))
+        nat.call("lb_key_switch", self.handle, self._r(d), key_id, self._r(u0), self._r(u1), count,
+                 _stream_ptr(stream))
         return u0, u1
 
 

@@ -58,8 +58,8 @@ __global__ void k_secret_coeffs(BfvDev d, uint64_t* out, uint32_t primes) {
 }
 
 // out[c][r][pos] = in[c][r][src(pos)]: x -> x^g on bit-reversed evaluations
-__global__ void k_automorph(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t total, uint32_t logn,
-                            uint64_t g) {
+template <class St>
+__global__ void k_automorph(const St* __restrict__ in, St* __restrict__ out, uint64_t total, uint32_t logn, uint64_t g) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= total) return;
     const uint32_t n = 1u << logn;
@@ -164,8 +164,9 @@ __device__ __forceinline__ uint64_t scaled_message(const BfvDev& d, uint32_t j, 
 // thread per coefficient: the error sample and the rounding term
 // floor(([Q]_t m + t/2) / t) (a 64-bit division) are limb-independent, so
 // they are computed once and the thread walks the L limbs.
+template <class St>
 __global__ void k_enc_coeffs(BfvDev d, const uint64_t* __restrict__ mcoef, uint32_t count, uint64_t id_base,
-                             uint64_t* __restrict__ ct) {
+                             St* __restrict__ ct) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(count) * d.n) return;
     const uint32_t k = idx % d.n;
@@ -175,18 +176,19 @@ __global__ void k_enc_coeffs(BfvDev d, const uint64_t* __restrict__ mcoef, uint3
     const uint64_t mval = mcoef[c * d.n + k];
     const uint64_t t = d.primes[d.tbase + j].q;
     const uint64_t extra = (d.q_mod_t[j] * mval + (t >> 1)) / t;
-    uint64_t* out = ct + c * 2 * d.L * d.n + k;
+    St* out = ct + c * 2 * d.L * d.n + k;
     for (uint32_t i = 0; i < d.L; ++i) {
         const Modulus qm = modulus_of(d.primes[i]);
         const uint64_t sm = add_mod(mul_mod(d.delta[j * d.L + i], mval, qm), reduce_u64(extra, qm), qm.q);
-        out[uint64_t(i) * d.n] = add_mod(reduce_signed(e, qm), sm, qm.q);
+        out[uint64_t(i) * d.n] = static_cast<St>(add_mod(reduce_signed(e, qm), sm, qm.q));
     }
 }
 
 // c1 = a (sampled in the evaluation domain), c0 = NTT(e + round(Qm/t)) - a s
 // (blocks never straddle a row: n is a multiple of the block size, so the
 // row's PRNG stream key is derived once per block)
-__global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, uint64_t* __restrict__ ct) {
+template <class St>
+__global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, St* __restrict__ ct) {
     __shared__ uint64_t key_sh;
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     const uint32_t pos = idx % d.n;
@@ -197,15 +199,15 @@ __global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, uint64_
     if (idx >= uint64_t(count) * d.L * d.n) return;
     const Modulus qm = modulus_of(d.primes[i]);
     const uint64_t a = sample_uniform(qm.q, prng_at(key_sh, pos));
-    uint64_t* c0 = ct + (c * 2 * d.L + i) * d.n;
-    uint64_t* c1 = c0 + uint64_t(d.L) * d.n;
-    c1[pos] = a;
-    c0[pos] = sub_mod(c0[pos], mul_mod(a, d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
+    St* c0 = ct + (c * 2 * d.L + i) * d.n;
+    St* c1 = c0 + uint64_t(d.L) * d.n;
+    c1[pos] = static_cast<St>(a);
+    c0[pos] = static_cast<St>(sub_mod(c0[pos], mul_mod(a, d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q));
 }
 
 // pt_mul = centered lift of m; pt_add = round(Q m / t); m: [T][n]
-__global__ void k_pt_lift(BfvDev d, const uint64_t* __restrict__ mcoef, uint64_t* __restrict__ pt_mul,
-                          uint64_t* __restrict__ pt_add) {
+template <class St>
+__global__ void k_pt_lift(BfvDev d, const uint64_t* __restrict__ mcoef, St* __restrict__ pt_mul, St* __restrict__ pt_add) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(d.T) * d.L * d.n) return;
     const uint32_t k = idx % d.n;
@@ -215,20 +217,21 @@ __global__ void k_pt_lift(BfvDev d, const uint64_t* __restrict__ mcoef, uint64_t
     const uint64_t t = d.primes[d.tbase + j].q;
     const uint64_t mv = mcoef[uint64_t(j) * d.n + k];
     const int64_t centered = mv > (t >> 1) ? static_cast<int64_t>(mv) - static_cast<int64_t>(t) : static_cast<int64_t>(mv);
-    if (pt_mul) pt_mul[idx] = reduce_signed(centered, qm);
-    if (pt_add) pt_add[idx] = scaled_message(d, j, i, mv, qm);
+    if (pt_mul) pt_mul[idx] = static_cast<St>(reduce_signed(centered, qm));
+    if (pt_add) pt_add[idx] = static_cast<St>(scaled_message(d, j, i, mv, qm));
 }
 
 // ---- decryption (§3.7) ----
-__global__ void k_phase(BfvDev d, const uint64_t* __restrict__ ct, uint32_t count, uint64_t* __restrict__ x) {
+template <class St>
+__global__ void k_phase(BfvDev d, const St* __restrict__ ct, uint32_t count, uint64_t* __restrict__ x) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(count) * d.L * d.n) return;
     const uint32_t pos = idx % d.n;
     const uint32_t i = (idx / d.n) % d.L;
     const uint64_t c = idx / (uint64_t(d.n) * d.L);
     const Modulus qm = modulus_of(d.primes[i]);
-    const uint64_t* c0 = ct + (c * 2 * d.L + i) * d.n;
-    const uint64_t* c1 = c0 + uint64_t(d.L) * d.n;
+    const St* c0 = ct + (c * 2 * d.L + i) * d.n;
+    const St* c1 = c0 + uint64_t(d.L) * d.n;
     x[idx] = add_mod(c0[pos], mul_mod(c1[pos], d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
 }
 
@@ -287,18 +290,44 @@ __device__ __forceinline__ void ew_rows(const EwShape& sh, F&& f) {
     }
 }
 
+// two consecutive residues, widened to u64 (16-byte access for u64 words,
+// 8-byte for u32)
+template <class St> __device__ __forceinline__ ulonglong2 ld2(const St* p) {
+    if constexpr (sizeof(St) == 8) {
+        return *reinterpret_cast<const ulonglong2*>(p);
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        return make_ulonglong2(v.x, v.y);
+    }
+}
+template <class St> __device__ __forceinline__ ulonglong2 ldg2(const St* p) {
+    if constexpr (sizeof(St) == 8) {
+        return __ldg(reinterpret_cast<const ulonglong2*>(p));
+    } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        return make_ulonglong2(v.x, v.y);
+    }
+}
+template <class St> __device__ __forceinline__ void st2(St* p, uint64_t a, uint64_t b) {
+    if constexpr (sizeof(St) == 8)
+        *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(a, b);
+    else
+        *reinterpret_cast<uint2*>(p) = make_uint2(static_cast<uint32_t>(a), static_cast<uint32_t>(b));
+}
+
 inline dim3 ew_grid(const EwShape& sh) {
     const uint32_t n = 1u << sh.logn;
     return dim3((n / 2 + kEwThreads - 1) / kEwThreads, std::min<uint32_t>(sh.rows, 65535u));
 }
 
-__global__ void __launch_bounds__(kEwThreads) k_add(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
-                                                    const uint64_t* __restrict__ b, uint64_t* __restrict__ out) {
+template <class St>
+__global__ void __launch_bounds__(kEwThreads) k_add(BfvDev d, EwShape sh, const St* __restrict__ a,
+                                                    const St* __restrict__ b, St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
         const uint64_t q = d.primes[i].q;
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
-        const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b + off);
-        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
+        const ulonglong2 x = ld2(a + off);
+        const ulonglong2 y = ld2(b + off);
+        st2(out + off, add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
     });
 }
 
@@ -306,51 +335,53 @@ struct ScalarTab {
     ulonglong2 v[32];  // per ciphertext prime: (s mod q_i, Shoup companion)
 };
 
-__global__ void __launch_bounds__(kEwThreads) k_mul_scalar(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
-                                                           ScalarTab s, uint64_t* __restrict__ out) {
+template <class St>
+__global__ void __launch_bounds__(kEwThreads) k_mul_scalar(BfvDev d, EwShape sh, const St* __restrict__ a, ScalarTab s,
+                                                           St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
         const uint64_t q = d.primes[i].q;
         const ulonglong2 w = s.v[i];
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
-        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(mul_shoup(x.x, w.x, w.y, q), mul_shoup(x.y, w.x, w.y, q));
+        const ulonglong2 x = ld2(a + off);
+        st2(out + off, mul_shoup(x.x, w.x, w.y, q), mul_shoup(x.y, w.x, w.y, q));
     });
 }
 
-__global__ void __launch_bounds__(kEwThreads) k_mul_scalar_add(BfvDev d, EwShape sh, const uint64_t* __restrict__ acc,
-                                                               const uint64_t* __restrict__ x, ScalarTab s,
-                                                               uint64_t* __restrict__ out) {
+template <class St>
+__global__ void __launch_bounds__(kEwThreads) k_mul_scalar_add(BfvDev d, EwShape sh, const St* __restrict__ acc,
+                                                               const St* __restrict__ x, ScalarTab s,
+                                                               St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t, uint32_t) {
         const uint64_t q = d.primes[i].q;
         const ulonglong2 w = s.v[i];
-        const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(acc + off);
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(x + off);
-        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(add_mod(u.x, mul_shoup(v.x, w.x, w.y, q), q),
-                                                                    add_mod(u.y, mul_shoup(v.y, w.x, w.y, q), q));
+        const ulonglong2 u = ld2(acc + off);
+        const ulonglong2 v = ld2(x + off);
+        st2(out + off, add_mod(u.x, mul_shoup(v.x, w.x, w.y, q), q), add_mod(u.y, mul_shoup(v.y, w.x, w.y, q), q));
     });
 }
 
 // out[c][comp][i] = a[c][comp][i] * pt[c mod T][i]
-__global__ void __launch_bounds__(kEwThreads) k_mul_plain(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
-                                                          const uint64_t* __restrict__ pt, uint64_t* __restrict__ out) {
+template <class St>
+__global__ void __launch_bounds__(kEwThreads) k_mul_plain(BfvDev d, EwShape sh, const St* __restrict__ a,
+                                                          const St* __restrict__ pt, St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t c, uint32_t k) {
         const Modulus qm = modulus_of(d.primes[i]);
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
-        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k));
-        *reinterpret_cast<ulonglong2*>(out + off) = make_ulonglong2(mul_mod(x.x, w.x, qm), mul_mod(x.y, w.y, qm));
+        const ulonglong2 x = ld2(a + off);
+        const ulonglong2 w = ldg2(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k);
+        st2(out + off, mul_mod(x.x, w.x, qm), mul_mod(x.y, w.y, qm));
     });
 }
 
-__global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, const uint64_t* __restrict__ a,
-                                                          const uint64_t* __restrict__ pt, uint64_t* __restrict__ out) {
+template <class St>
+__global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, const St* __restrict__ a,
+                                                          const St* __restrict__ pt, St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t comp, uint32_t c, uint32_t k) {
         const uint64_t q = d.primes[i].q;
-        ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + off);
+        ulonglong2 x = ld2(a + off);
         if (!comp) {
-            const ulonglong2 w =
-                __ldg(reinterpret_cast<const ulonglong2*>(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k));
+            const ulonglong2 w = ldg2(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k);
             x = make_ulonglong2(add_mod(x.x, w.x, q), add_mod(x.y, w.y, q));
         }
-        *reinterpret_cast<ulonglong2*>(out + off) = x;
+        st2(out + off, x.x, x.y);
     });
 }
 
@@ -360,11 +391,11 @@ __global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, 
 // SMALL: every F and G prime below 2^30, so y_i [F/f_i]_g < 2^60 and up to
 // 16 of them sum exactly in 64 bits (one reduction per output instead of a
 // 128-bit accumulator); y stays in registers (unrolled over the 16-prime cap).
-template <bool SMALL>
-__global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint32_t polys, uint32_t F, uint32_t fbase,
+template <bool SMALL, class Src, class Dst>
+__global__ void k_exact_extend(BfvDev d, const Src* __restrict__ src, uint32_t polys, uint32_t F, uint32_t fbase,
                                const uint64_t* __restrict__ hat_inv, const ulonglong2* __restrict__ frac,
                                const uint64_t* __restrict__ hat_mod /*[F][G]*/, const uint64_t* __restrict__ prod_mod /*[G]*/,
-                               uint32_t G, uint32_t gbase, uint64_t* __restrict__ dst) {
+                               uint32_t G, uint32_t gbase, Dst* __restrict__ dst) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(polys) * d.n) return;
     const uint32_t k = idx % d.n;
@@ -403,12 +434,13 @@ __global__ void k_exact_extend(BfvDev d, const uint64_t* __restrict__ src, uint3
             }
             s = reduce_acc(acc, gm);
         }
-        dst[(p * G + m) * d.n + k] = sub_mod(s, mul_mod(reduce_u64(v, gm), prod_mod[m], gm), gm.q);
+        dst[(p * G + m) * d.n + k] = static_cast<Dst>(sub_mod(s, mul_mod(reduce_u64(v, gm), prod_mod[m], gm), gm.q));
     }
 }
 
 // tensor over Q ∪ B in the evaluation domain: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
-__global__ void k_tensor(BfvDev d, const uint64_t* __restrict__ A, const uint64_t* __restrict__ Bc,
+template <class St>
+__global__ void k_tensor(BfvDev d, const St* __restrict__ A, const St* __restrict__ Bc,
                          const uint64_t* __restrict__ Y /*[count][4][M][n]*/, uint32_t count,
                          uint64_t* __restrict__ D /*[count][3][L+M][n]*/) {
     const uint32_t LM = d.L + d.M;
@@ -744,13 +776,22 @@ void bfv_setup(Context& cx) {
 
 // ---- key material ----------------------------------------------------------------
 
-void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
-                      uint64_t galois, cudaStream_t s) {
+template <class St>
+static void automorphism_words(Context& cx, const St* in, St* out, uint32_t polys, uint32_t limbs, uint64_t galois,
+                               cudaStream_t s) {
     if (galois % 2 == 0 || galois >= 2ull * cx.n()) throw std::invalid_argument("galois element must be odd in [1, 2n)");
     const uint64_t total = uint64_t(polys) * limbs * cx.n();
     if (!total) return;
-    k_automorph<<<grid_for(total), kBlock, 0, s>>>(in, out, total, cx.logn(), galois);
+    k_automorph<St><<<grid_for(total), kBlock, 0, s>>>(in, out, total, cx.logn(), galois);
     LB_KERNEL_DONE();
+}
+
+void automorphism_ntt(Context& cx, const void* in, void* out, uint32_t polys, uint32_t limbs, uint64_t galois,
+                      cudaStream_t s) {
+    if (cx.bfv()->dev.ks32)
+        automorphism_words(cx, static_cast<const uint32_t*>(in), static_cast<uint32_t*>(out), polys, limbs, galois, s);
+    else
+        automorphism_words(cx, static_cast<const uint64_t*>(in), static_cast<uint64_t*>(out), polys, limbs, galois, s);
 }
 
 void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
@@ -768,7 +809,7 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     if (key_id == kRelinKeyId) {
         k_square_limbs<<<grid_for(uint64_t(LK) * n), kBlock, 0, s>>>(d.s_ntt, target.get(), d, LK);
     } else {
-        automorphism_ntt(cx, d.s_ntt, target.get(), 1, LK, key_id, s);
+        automorphism_words(cx, d.s_ntt, target.get(), 1, LK, key_id, s);  // key material stays u64
     }
     LB_KERNEL_DONE();
     k_keygen_error<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get());
@@ -943,10 +984,13 @@ void dispatch_ks(int logn, const BfvDev& d, const KsInnerArgs& ka, const ModDown
 //   2. fused ModUp + NTT + key inner product over Q ∪ P   (ks_inner_kernel)
 //   3. inverse NTT of the P limbs of both accumulators
 //   4. fused P->Q conversion + NTT + ModDown epilogue     (moddown_kernel)
-void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint64_t d_galois, uint64_t key_id,
-                     uint32_t count, const uint64_t* add0, const uint64_t* add1, uint64_t add_stride,
-                     uint64_t add_galois, uint64_t* out0, uint64_t* out1, uint64_t out_stride, cudaStream_t s,
-                     const uint64_t* sum0 = nullptr, const uint64_t* sum1 = nullptr, uint64_t sum_stride = 0) {
+// All residue operands in the context's residue word St (== the kernels'
+// arithmetic word: u32 exactly when ks32); strides in elements.
+template <class St>
+void key_switch_impl(Context& cx, const St* d_ntt, uint64_t d_stride, uint64_t d_galois, uint64_t key_id,
+                     uint32_t count, const St* add0, const St* add1, uint64_t add_stride, uint64_t add_galois,
+                     St* out0, St* out1, uint64_t out_stride, cudaStream_t s, const St* sum0 = nullptr,
+                     const St* sum1 = nullptr, uint64_t sum_stride = 0) {
     if (!count) return;
     BfvState& st = *cx.bfv();
     const BfvDev& d = st.dev;
@@ -956,12 +1000,13 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     const uint32_t n = d.n, L = d.L, K = d.K, LK = L + K;
     // intermediates in the kernels' word size (u32 when ks32)
     const size_t wb = d.ks32 ? 4 : 8;
+    if (wb != sizeof(St)) throw std::logic_error("key switch: residue word does not match the context");
     DeviceBuffer dc(uint64_t(count) * L * n * wb, s);
     {
         // coefficients of d, pre-multiplied by [(D_j/q_i)^-1]_{q_i} for
         // multi-prime digits (folded into the transform's n^-1)
         LimbBatch lb{dc.get(), count, L, 0, uint64_t(L) * n};
-        lb.src = d_ntt;
+        lb.src = reinterpret_cast<const uint64_t*>(d_ntt);  // read as St words
         lb.src_stride = d_stride;
         lb.galois = d_galois;
         lb.packed32 = d.ks32;
@@ -990,17 +1035,37 @@ void key_switch_impl(Context& cx, const uint64_t* d_ntt, uint64_t d_stride, uint
     dispatch_ks(cx.logn(), d, ka, &ma, s);
 }
 
+// Runs f(St{}) with the context's residue word (uint32_t when ks32).
+template <class F>
+void with_residue(const Context& cx, F&& f) {
+    if (cx.bfv()->dev.ks32)
+        f(uint32_t{});
+    else
+        f(uint64_t{});
+}
+
+// A limb batch over residue words: packed32 when the words are u32.
+template <class St>
+LimbBatch res_batch(St* data, uint32_t polys, uint32_t limbs, uint32_t first_prime, uint64_t stride) {
+    LimbBatch b{reinterpret_cast<uint64_t*>(data), polys, limbs, first_prime, stride};
+    b.packed32 = sizeof(St) == 4;
+    return b;
+}
+
 }  // namespace
 
-void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
-                cudaStream_t s) {
+void key_switch(Context& cx, const void* d, uint64_t key_id, void* u0, void* u1, uint32_t count, cudaStream_t s) {
     const uint64_t LN = uint64_t(cx.L()) * cx.n();
-    key_switch_impl(cx, d, LN, 0, key_id, count, nullptr, nullptr, 0, 0, u0, u1, LN, s);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        key_switch_impl<St>(cx, static_cast<const St*>(d), LN, 0, key_id, count, nullptr, nullptr, 0, 0,
+                            static_cast<St*>(u0), static_cast<St*>(u1), LN, s);
+    });
 }
 
 // ---- public ciphertext operations ----------------------------------------------
 
-void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out, cudaStream_t s) {
+void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!B) return;
     const uint32_t n = d.n, T = d.T, L = d.L;
@@ -1013,26 +1078,33 @@ void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_b
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
-    k_enc_coeffs<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, id_base, out);
-    LB_KERNEL_DONE();
-    cx.ntt_forward(LimbBatch{out, count, L, 0, 2ull * L * n}, s);
-    k_enc_finish<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, count, id_base, out);
-    LB_KERNEL_DONE();
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        St* ct = static_cast<St*>(out);
+        k_enc_coeffs<St><<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, id_base, ct);
+        LB_KERNEL_DONE();
+        cx.ntt_forward(res_batch(ct, count, L, 0, 2ull * L * n), s);
+        k_enc_finish<St><<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, count, id_base, ct);
+        LB_KERNEL_DONE();
+    });
 }
 
-void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
+void decrypt_coeffs(Context& cx, const void* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!B) return;
     const uint32_t n = d.n, L = d.L, count = B * d.T;
     DeviceBuffer x(uint64_t(count) * L * n * 8, s);
-    k_phase<<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, ct, count, x.get());
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_phase<St><<<grid_for(uint64_t(count) * L * n), kBlock, 0, s>>>(d, static_cast<const St*>(ct), count, x.get());
+    });
     LB_KERNEL_DONE();
     cx.ntt_inverse(LimbBatch{x.get(), count, L, 0, uint64_t(L) * n}, s);
     k_dec_scale<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, x.get(), count, out);
     LB_KERNEL_DONE();
 }
 
-void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
+void decrypt_slots(Context& cx, const void* ct, uint32_t B, uint64_t* out, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!B) return;
     const uint32_t n = d.n, T = d.T, count = B * T;
@@ -1046,7 +1118,7 @@ void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, c
     LB_KERNEL_DONE();
 }
 
-void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, cudaStream_t s) {
+void encode_plain(Context& cx, const int64_t* values, void* pt_mul, void* pt_add, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     const uint32_t n = d.n, T = d.T, L = d.L;
     DeviceBuffer m(uint64_t(T) * n * 8, s);
@@ -1056,19 +1128,28 @@ void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
-    k_pt_lift<<<grid_for(uint64_t(T) * L * n), kBlock, 0, s>>>(d, m.get(), pt_mul, pt_add);
-    LB_KERNEL_DONE();
-    if (pt_mul) cx.ntt_forward(LimbBatch{pt_mul, T, L, 0, uint64_t(L) * n}, s);
-    if (pt_add) cx.ntt_forward(LimbBatch{pt_add, T, L, 0, uint64_t(L) * n}, s);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        St* pm = static_cast<St*>(pt_mul);
+        St* pa = static_cast<St*>(pt_add);
+        k_pt_lift<St><<<grid_for(uint64_t(T) * L * n), kBlock, 0, s>>>(d, m.get(), pm, pa);
+        LB_KERNEL_DONE();
+        if (pm) cx.ntt_forward(res_batch(pm, T, L, 0, uint64_t(L) * n), s);
+        if (pa) cx.ntt_forward(res_batch(pa, T, L, 0, uint64_t(L) * n), s);
+    });
 }
 
 static EwShape ew_shape(const BfvDev& d, uint32_t count) { return EwShape{count * 2 * d.L, d.L, d.T, d.logn}; }
 
-void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_add(Context& cx, const void* a, const void* b, void* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     const EwShape sh = ew_shape(d, count);
-    k_add<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, b, out);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_add<St><<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, static_cast<const St*>(a), static_cast<const St*>(b),
+                                                     static_cast<St*>(out));
+    });
     LB_KERNEL_DONE();
 }
 
@@ -1083,116 +1164,157 @@ static ScalarTab scalar_table(Context& cx, int64_t scalar) {
     return tab;
 }
 
-void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_mul_scalar(Context& cx, const void* a, int64_t scalar, void* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     const EwShape sh = ew_shape(d, count);
-    k_mul_scalar<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, scalar_table(cx, scalar), out);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_mul_scalar<St><<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, static_cast<const St*>(a), scalar_table(cx, scalar),
+                                                            static_cast<St*>(out));
+    });
     LB_KERNEL_DONE();
 }
 
-void ct_mul_scalar_add(Context& cx, const uint64_t* acc, const uint64_t* x, int64_t scalar, uint64_t* out,
-                       uint32_t count, cudaStream_t s) {
+void ct_mul_scalar_add(Context& cx, const void* acc, const void* x, int64_t scalar, void* out, uint32_t count,
+                       cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     const EwShape sh = ew_shape(d, count);
-    k_mul_scalar_add<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, acc, x, scalar_table(cx, scalar), out);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_mul_scalar_add<St><<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, static_cast<const St*>(acc),
+                                                                static_cast<const St*>(x), scalar_table(cx, scalar),
+                                                                static_cast<St*>(out));
+    });
     LB_KERNEL_DONE();
 }
 
-void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_mul_plain(Context& cx, const void* a, const void* pt, void* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     const EwShape sh = ew_shape(d, count);
-    k_mul_plain<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, pt, out);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_mul_plain<St><<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, static_cast<const St*>(a), static_cast<const St*>(pt),
+                                                           static_cast<St*>(out));
+    });
     LB_KERNEL_DONE();
 }
 
-void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_add_plain(Context& cx, const void* a, const void* pt, void* out, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     const EwShape sh = ew_shape(d, count);
-    k_add_plain<<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, a, pt, out);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        k_add_plain<St><<<ew_grid(sh), kEwThreads, 0, s>>>(d, sh, static_cast<const St*>(a), static_cast<const St*>(pt),
+                                                           static_cast<St*>(out));
+    });
     LB_KERNEL_DONE();
 }
 
-void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_rotate(Context& cx, const void* a_in, uint64_t galois, void* out_v, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     if (galois % 2 == 0 || galois >= 2ull * d.n) throw std::invalid_argument("galois element must be odd in [1, 2n)");
     const uint64_t LN = uint64_t(d.L) * d.n;
-    // the automorphism is folded into the key switch's loads; an in-place
-    // call needs a private copy of the input (outputs scatter by permutation)
-    DeviceBuffer copy;
-    if (out == a) {
-        copy = DeviceBuffer(uint64_t(count) * 2 * LN * 8, s);
-        LB_CUDA(cudaMemcpyAsync(copy.get(), a, uint64_t(count) * 2 * LN * 8, cudaMemcpyDeviceToDevice, s));
-        a = copy.get();
-    }
-    key_switch_impl(cx, a + LN, 2 * LN, galois, galois, count, a, nullptr, 2 * LN, galois, out, out + LN, 2 * LN, s);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        const St* a = static_cast<const St*>(a_in);
+        St* out = static_cast<St*>(out_v);
+        // the automorphism is folded into the key switch's loads; an in-place
+        // call needs a private copy of the input (outputs scatter by permutation)
+        DeviceBuffer copy;
+        if (out == a) {
+            const uint64_t bytes = uint64_t(count) * 2 * LN * sizeof(St);
+            copy = DeviceBuffer(bytes, s);
+            LB_CUDA(cudaMemcpyAsync(copy.get(), a, bytes, cudaMemcpyDeviceToDevice, s));
+            a = copy.get<St>();
+        }
+        key_switch_impl<St>(cx, a + LN, 2 * LN, galois, galois, count, a, nullptr, 2 * LN, galois, out, out + LN,
+                            2 * LN, s);
+    });
 }
 
-void ct_rotate_add(Context& cx, const uint64_t* base, const uint64_t* x, uint64_t galois, uint64_t* out,
-                   uint32_t count, cudaStream_t s) {
+void ct_rotate_add(Context& cx, const void* base_in, const void* x_in, uint64_t galois, void* out_v, uint32_t count,
+                   cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     if (galois % 2 == 0 || galois >= 2ull * d.n) throw std::invalid_argument("galois element must be odd in [1, 2n)");
     const uint64_t LN = uint64_t(d.L) * d.n;
-    DeviceBuffer copy;
-    if (out == x || out == base) {  // outputs are written while inputs are gathered
-        copy = DeviceBuffer(uint64_t(count) * 4 * LN * 8, s);
-        LB_CUDA(cudaMemcpyAsync(copy.get(), x, uint64_t(count) * 2 * LN * 8, cudaMemcpyDeviceToDevice, s));
-        LB_CUDA(cudaMemcpyAsync(copy.get() + uint64_t(count) * 2 * LN, base, uint64_t(count) * 2 * LN * 8,
-                                cudaMemcpyDeviceToDevice, s));
-        x = copy.get();
-        base = copy.get() + uint64_t(count) * 2 * LN;
-    }
-    key_switch_impl(cx, x + LN, 2 * LN, galois, galois, count, x, nullptr, 2 * LN, galois, out, out + LN, 2 * LN, s,
-                    base, base + LN, 2 * LN);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        const St* x = static_cast<const St*>(x_in);
+        const St* base = static_cast<const St*>(base_in);
+        St* out = static_cast<St*>(out_v);
+        DeviceBuffer copy;
+        if (out == x || out == base) {  // outputs are written while inputs are gathered
+            const uint64_t bytes = uint64_t(count) * 2 * LN * sizeof(St);
+            copy = DeviceBuffer(2 * bytes, s);
+            LB_CUDA(cudaMemcpyAsync(copy.get(), x, bytes, cudaMemcpyDeviceToDevice, s));
+            LB_CUDA(cudaMemcpyAsync(copy.get<uint8_t>() + bytes, base, bytes, cudaMemcpyDeviceToDevice, s));
+            x = copy.get<St>();
+            base = copy.get<St>() + uint64_t(count) * 2 * LN;
+        }
+        key_switch_impl<St>(cx, x + LN, 2 * LN, galois, galois, count, x, nullptr, 2 * LN, galois, out, out + LN,
+                            2 * LN, s, base, base + LN, 2 * LN);
+    });
 }
 
-void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s) {
+void ct_mul(Context& cx, const void* a_in, const void* b_in, void* out_v, uint32_t count, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!count) return;
     if (!cx.bfv()->mul_base_ok)
         throw std::invalid_argument("multiplication needs an auxiliary base B with log2 B >= log2 Q + log2 t + log2 n + 2");
     const uint32_t n = d.n, L = d.L, M = d.M, LM = L + M;
     const uint64_t LN = uint64_t(L) * n;
-    // (a) inputs to coefficients: X[c] = [a0 a1 b0 b1]
-    DeviceBuffer X(uint64_t(count) * 4 * LN * 8, s);
-    LB_CUDA(cudaMemcpy2DAsync(X.get(), 4 * LN * 8, a, 2 * LN * 8, 2 * LN * 8, count, cudaMemcpyDeviceToDevice, s));
-    LB_CUDA(cudaMemcpy2DAsync(X.get() + 2 * LN, 4 * LN * 8, b, 2 * LN * 8, 2 * LN * 8, count, cudaMemcpyDeviceToDevice,
-                              s));
-    cx.ntt_inverse(LimbBatch{X.get(), count * 4, L, 0, LN}, s);
-    // (b) exact Q -> B, (c) to evaluations
-    DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
-    const bool small = cx.bfv()->qb_small;
-    (small ? k_exact_extend<true> : k_exact_extend<false>)<<<grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(
-        d, X.get(), count * 4, L, 0, d.qhat_inv, d.q_frac, d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
-    LB_KERNEL_DONE();
-    cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
-    // (d) tensor over Q ∪ B
-    DeviceBuffer D(uint64_t(count) * 3 * LM * n * 8, s);
-    k_tensor<<<grid_for(uint64_t(count) * LM * n), kBlock, 0, s>>>(d, a, b, Y.get(), count, D.get());
-    LB_KERNEL_DONE();
-    // (e) back to coefficients over Q ∪ B
-    LimbBatch db{D.get(), count * 3, LM, 0, uint64_t(LM) * n};
-    db.prime_map = cx.bfv()->qb_map;
-    db.map_period = LM;
-    db.map_small = cx.bfv()->qb_small;
-    cx.ntt_inverse(db, s);
-    // (f) scale by t/Q into B, (g) exact B -> Q, (h) to evaluations
-    DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);
-    k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
-    LB_KERNEL_DONE();
-    DeviceBuffer E(uint64_t(count) * 3 * LN * 8, s);
-    (small ? k_exact_extend<true> : k_exact_extend<false>)<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
-        d, Z.get(), count * 3, M, d.bbase, d.bhat_inv, d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, E.get());
-    LB_KERNEL_DONE();
-    cx.ntt_forward(LimbBatch{E.get(), count * 3, L, 0, LN}, s);
-    // (i) relinearize e2 and add into (e0, e1)
-    key_switch_impl(cx, E.get() + 2 * LN, 3 * LN, 0, kRelinKeyId, count, E.get(), E.get() + LN, 3 * LN, 0, out,
-                    out + LN, 2 * LN, s);
+    with_residue(cx, [&](auto w) {
+        using St = decltype(w);
+        const St* a = static_cast<const St*>(a_in);
+        const St* b = static_cast<const St*>(b_in);
+        St* out = static_cast<St*>(out_v);
+        constexpr size_t W = sizeof(St);
+        // (a) inputs to coefficients: X[c] = [a0 a1 b0 b1]
+        DeviceBuffer X(uint64_t(count) * 4 * LN * W, s);
+        St* x = X.get<St>();
+        LB_CUDA(cudaMemcpy2DAsync(x, 4 * LN * W, a, 2 * LN * W, 2 * LN * W, count, cudaMemcpyDeviceToDevice, s));
+        LB_CUDA(cudaMemcpy2DAsync(x + 2 * LN, 4 * LN * W, b, 2 * LN * W, 2 * LN * W, count, cudaMemcpyDeviceToDevice,
+                                  s));
+        cx.ntt_inverse(res_batch(x, count * 4, L, 0, LN), s);
+        // (b) exact Q -> B, (c) to evaluations
+        DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
+        const bool small = cx.bfv()->qb_small;
+        (small ? k_exact_extend<true, St, uint64_t> : k_exact_extend<false, St, uint64_t>)<<<
+            grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(d, x, count * 4, L, 0, d.qhat_inv, d.q_frac,
+                                                              d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
+        LB_KERNEL_DONE();
+        cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
+        // (d) tensor over Q ∪ B
+        DeviceBuffer D(uint64_t(count) * 3 * LM * n * 8, s);
+        k_tensor<St><<<grid_for(uint64_t(count) * LM * n), kBlock, 0, s>>>(d, a, b, Y.get(), count, D.get());
+        LB_KERNEL_DONE();
+        // (e) back to coefficients over Q ∪ B
+        LimbBatch db{D.get(), count * 3, LM, 0, uint64_t(LM) * n};
+        db.prime_map = cx.bfv()->qb_map;
+        db.map_period = LM;
+        db.map_small = cx.bfv()->qb_small;
+        cx.ntt_inverse(db, s);
+        // (f) scale by t/Q into B, (g) exact B -> Q (in residue words), (h) to evaluations
+        DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);
+        k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
+        LB_KERNEL_DONE();
+        DeviceBuffer E(uint64_t(count) * 3 * LN * W, s);
+        St* e = E.get<St>();
+        (small ? k_exact_extend<true, uint64_t, St> : k_exact_extend<false, uint64_t, St>)<<<
+            grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, Z.get(), count * 3, M, d.bbase, d.bhat_inv,
+                                                              d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, e);
+        LB_KERNEL_DONE();
+        cx.ntt_forward(res_batch(e, count * 3, L, 0, LN), s);
+        // (i) relinearize e2 and add into (e0, e1)
+        key_switch_impl<St>(cx, e + 2 * LN, 3 * LN, 0, kRelinKeyId, count, e, e + LN, 3 * LN, 0, out, out + LN,
+                            2 * LN, s);
+    });
 }
 
 }  // namespace lb

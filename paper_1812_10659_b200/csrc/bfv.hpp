@@ -72,6 +72,12 @@ struct BfvDev {
     const uint2* ks_last_p32;        // [K][2]
 };
 
+// Residue word of a context's ciphertexts and plaintext operands in HBM:
+// uint32_t when every ciphertext and special prime is below 2^30 (ks32: the
+// key switch computes in 32-bit words too), else uint64_t. Key material and
+// internal extended-basis buffers stay uint64_t.
+inline size_t residue_bytes(const BfvDev& d) { return d.ks32 ? 4 : 8; }
+
 // Opaque device handle of a key-switching key.
 struct KsKey {
     DeviceBuffer buf;    // [dnum][2][L+K][n]
@@ -98,53 +104,50 @@ struct BfvState {
 constexpr uint64_t kRelinKeyId = 0;
 
 // ---- batched ciphertext operations (bfv.cu) ----------------------------------
-// `count` = number of ciphertexts; ciphertext c uses t_{c mod T}.
+// `count` = number of ciphertexts; ciphertext c uses t_{c mod T}. Ciphertext
+// and plaintext-operand buffers hold residue words (residue_bytes).
 
 // values: device int64 [B][n] slot values (one vector per message, reduced
 // mod each t_j); out: [B][T][2][L][n]; ciphertext id = id_base + c.
-void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
-                   cudaStream_t s);
+void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, cudaStream_t s);
 // out: [B][T][n] slot residues mod t_j
-void decrypt_slots(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s);
+void decrypt_slots(Context& cx, const void* ct, uint32_t B, uint64_t* out, cudaStream_t s);
 // out: [B][T][n] plaintext coefficients mod t_j (before slot decoding)
-void decrypt_coeffs(Context& cx, const uint64_t* ct, uint32_t B, uint64_t* out, cudaStream_t s);
+void decrypt_coeffs(Context& cx, const void* ct, uint32_t B, uint64_t* out, cudaStream_t s);
 
 // values: device int64 [n] (shared by every message); pt_mul / pt_add:
 // [T][L][n] NTT-domain plaintext operands (centered lift; round(Q m / t)).
-void encode_plain(Context& cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, cudaStream_t s);
+void encode_plain(Context& cx, const int64_t* values, void* pt_mul, void* pt_add, cudaStream_t s);
 
-void ct_add(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s);
-void ct_mul_scalar(Context& cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count, cudaStream_t s);
+void ct_add(Context& cx, const void* a, const void* b, void* out, uint32_t count, cudaStream_t s);
+void ct_mul_scalar(Context& cx, const void* a, int64_t scalar, void* out, uint32_t count, cudaStream_t s);
 // pt: [T][L][n], broadcast over messages
-void ct_mul_plain(Context& cx, const uint64_t* a, const uint64_t* pt_mul, uint64_t* out, uint32_t count,
-                  cudaStream_t s);
-void ct_add_plain(Context& cx, const uint64_t* a, const uint64_t* pt_add, uint64_t* out, uint32_t count,
-                  cudaStream_t s);
-void ct_rotate(Context& cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count, cudaStream_t s);
+void ct_mul_plain(Context& cx, const void* a, const void* pt_mul, void* out, uint32_t count, cudaStream_t s);
+void ct_add_plain(Context& cx, const void* a, const void* pt_add, void* out, uint32_t count, cudaStream_t s);
+void ct_rotate(Context& cx, const void* a, uint64_t galois, void* out, uint32_t count, cudaStream_t s);
 // fused forms used by the evaluator (one counted rotation / scalar product
 // plus one counted addition, one pass over memory):
 //   out = base + rotate_g(x)          out = acc + scalar * x
-void ct_rotate_add(Context& cx, const uint64_t* base, const uint64_t* x, uint64_t galois, uint64_t* out,
-                   uint32_t count, cudaStream_t s);
-void ct_mul_scalar_add(Context& cx, const uint64_t* acc, const uint64_t* x, int64_t scalar, uint64_t* out,
-                       uint32_t count, cudaStream_t s);
-void ct_mul(Context& cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, cudaStream_t s);
+void ct_rotate_add(Context& cx, const void* base, const void* x, uint64_t galois, void* out, uint32_t count,
+                   cudaStream_t s);
+void ct_mul_scalar_add(Context& cx, const void* acc, const void* x, int64_t scalar, void* out, uint32_t count,
+                       cudaStream_t s);
+void ct_mul(Context& cx, const void* a, const void* b, void* out, uint32_t count, cudaStream_t s);
 
 // key material
 void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s);
 const uint64_t* key_ptr(Context& cx, uint64_t key_id);
 // raw polynomial automorphism in the NTT domain over [polys][limbs][n]
-void automorphism_ntt(Context& cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
-                      uint64_t galois, cudaStream_t s);
+void automorphism_ntt(Context& cx, const void* in, void* out, uint32_t polys, uint32_t limbs, uint64_t galois,
+                      cudaStream_t s);
 // raw key switch of d ([count][L][n], NTT) -> u0, u1 ([count][L][n], NTT)
-void key_switch(Context& cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
-                cudaStream_t s);
+void key_switch(Context& cx, const void* d, uint64_t key_id, void* u0, void* u1, uint32_t count, cudaStream_t s);
 
 // Record-tensor dense layer (simd.cu): outs[r] = sum_i W[r][i] * xs[i] for
 // R output and F input ciphertext groups of `cts` ciphertexts each; xs, outs:
 // device arrays of device pointers; W: device int64 [R][F], |W| < 2^31
 // (small_weights: |W| < 2^15, enabling the 32-bit path when every q < 2^30).
-void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint64_t* const* outs, uint32_t R,
+void simd_weighted_sums(Context& cx, const void* const* xs, uint32_t F, void* const* outs, uint32_t R,
                         const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s);
 
 }  // namespace lb

@@ -69,6 +69,13 @@ int lb_context_prime(const lb_context* cx, uint32_t index, uint64_t* prime, uint
     });
 }
 
+int lb_context_residue_bytes(const lb_context* cx, uint32_t* bytes) {
+    return guarded([&] {
+        need(cx && bytes, "null argument");
+        *bytes = static_cast<uint32_t>(lb::residue_bytes(cx->cx.bfv()->dev));
+    });
+}
+
 int lb_sync(lb_context* cx, void* stream) {
     return guarded([&] { LB_CUDA(cudaStreamSynchronize(pick(cx, stream))); });
 }
@@ -91,8 +98,7 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
     });
 }
 
-int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, uint64_t* out,
-                     void* stream) {
+int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && values && out, "null argument");
@@ -100,7 +106,7 @@ int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t
     });
 }
 
-int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
+int lb_decrypt_slots(lb_context* cx, const void* ct, uint32_t B, uint64_t* out, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && ct && out, "null argument");
@@ -108,7 +114,7 @@ int lb_decrypt_slots(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* o
     });
 }
 
-int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* out, void* stream) {
+int lb_decrypt_coeffs(lb_context* cx, const void* ct, uint32_t B, uint64_t* out, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && ct && out, "null argument");
@@ -116,7 +122,7 @@ int lb_decrypt_coeffs(lb_context* cx, const uint64_t* ct, uint32_t B, uint64_t* 
     });
 }
 
-int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uint64_t* pt_add, void* stream) {
+int lb_encode_plain(lb_context* cx, const int64_t* values, void* pt_mul, void* pt_add, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && values && (pt_mul || pt_add), "null argument");
@@ -124,7 +130,7 @@ int lb_encode_plain(lb_context* cx, const int64_t* values, uint64_t* pt_mul, uin
     });
 }
 
-int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
+int lb_ct_add(lb_context* cx, const void* a, const void* b, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && b && out, "null argument");
@@ -132,8 +138,7 @@ int lb_ct_add(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* ou
     });
 }
 
-int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t* out, uint32_t count,
-                     void* stream) {
+int lb_ct_mul_scalar(lb_context* cx, const void* a, int64_t scalar, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && out, "null argument");
@@ -141,8 +146,7 @@ int lb_ct_mul_scalar(lb_context* cx, const uint64_t* a, int64_t scalar, uint64_t
     });
 }
 
-int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
-                    void* stream) {
+int lb_ct_mul_plain(lb_context* cx, const void* a, const void* pt, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && pt && out, "null argument");
@@ -150,8 +154,7 @@ int lb_ct_mul_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint6
     });
 }
 
-int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint64_t* out, uint32_t count,
-                    void* stream) {
+int lb_ct_add_plain(lb_context* cx, const void* a, const void* pt, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && pt && out, "null argument");
@@ -159,8 +162,7 @@ int lb_ct_add_plain(lb_context* cx, const uint64_t* a, const uint64_t* pt, uint6
     });
 }
 
-int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* out, uint32_t count,
-                 void* stream) {
+int lb_ct_rotate(lb_context* cx, const void* a, uint64_t galois, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && out, "null argument");
@@ -168,7 +170,7 @@ int lb_ct_rotate(lb_context* cx, const uint64_t* a, uint64_t galois, uint64_t* o
     });
 }
 
-int lb_ct_mul(lb_context* cx, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t count, void* stream) {
+int lb_ct_mul(lb_context* cx, const void* a, const void* b, void* out, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && a && b && out, "null argument");
@@ -192,8 +194,8 @@ int lb_key_pointer(lb_context* cx, uint64_t key_id, const uint64_t** out) {
     });
 }
 
-int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t polys, uint32_t limbs,
-                    uint64_t galois, void* stream) {
+int lb_automorphism(lb_context* cx, const void* in, void* out, uint32_t polys, uint32_t limbs, uint64_t galois,
+                    void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && in && out, "null argument");
@@ -202,8 +204,7 @@ int lb_automorphism(lb_context* cx, const uint64_t* in, uint64_t* out, uint32_t 
     });
 }
 
-int lb_key_switch(lb_context* cx, const uint64_t* d, uint64_t key_id, uint64_t* u0, uint64_t* u1, uint32_t count,
-                  void* stream) {
+int lb_key_switch(lb_context* cx, const void* d, uint64_t key_id, void* u0, void* u1, uint32_t count, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && d && u0 && u1, "null argument");

@@ -154,7 +154,7 @@ int lb_message_info(const lb_message* m, uint32_t* depth, uint32_t* plain_depth,
 }
 
 // device pointer of the message's ciphertexts [batch][T][2][L][n] (tests)
-int lb_message_data(const lb_message* m, const uint64_t** out) {
+int lb_message_data(const lb_message* m, const void** out) {
     return guarded([&] {
         need(m && out, "null argument");
         *out = m->m.data();

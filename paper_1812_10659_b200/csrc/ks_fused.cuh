@@ -20,7 +20,7 @@ namespace lb {
 
 struct KsInnerArgs {
     const void* dc;          // [count][L][n] coefficients of the input (word-sized: u64 or u32)
-    const uint64_t* dn;      // input evaluations, poly stride d_stride
+    const void* dn;          // input evaluations (residue words == the kernel word), poly stride d_stride
     uint64_t d_stride;
     uint64_t d_galois;       // automorphism applied to dn reads (0 = none)
     const void* key;         // [dnum][2][L+K][n] (value, Shoup companion): PairT<W>
@@ -174,9 +174,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         if (r >= lo && r < hi) {
             // the digit already lives in this prime: use the input's evaluations
-            const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+            const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
             mac_all(j, [&](uint32_t, uint32_t x) {
-                return static_cast<W>(__ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]));
+                return __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
             });
             continue;
         }
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
     // acc_h[x] = sum_j v_j[x] * key_j[h][r][x], four elements at a time
     const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
     const uint64_t kstride_j = uint64_t(2 * LK) << LOGN, kstride_h = uint64_t(LK) << LOGN;
-    const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+    const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
     const uint32_t sbt = swb<W>(threadIdx.x);
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
     W* out1 = out0 + uint64_t(LK) * n;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
                 w1[e] = __ldg(&key[j * kstride_j + kstride_h + off]);
                 if (static_cast<int>(j) == own) {
                     const uint32_t x = xt + off;
-                    v[e] = static_cast<W>(__ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]));
+                    v[e] = __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
                 } else {
                     v[e] = reduce_4q<W>(sm_at(planes + j * S::M, sbt, off), q, two_q);
                 }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         const bool first = j == 0;
         if (r >= lo && r < hi) {
-            const uint64_t* dn = a.dn + c * a.d_stride + (uint64_t(r) << LOGN);
+            const uint64_t* dn = static_cast<const uint64_t*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
             mac_all(j, first, [&](uint32_t, uint32_t x) {
                 return __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
             });
@@ -432,15 +432,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
 
 struct ModDownArgs {
     const void* acc;          // [count][2][L+K][n]: Q limbs evaluations, P limbs coefficients (word-sized)
-    const uint64_t* add0;     // optional, poly stride add_stride
-    const uint64_t* add1;
+    // residue operands below are in the kernel word W (the context's residue word)
+    const void* add0;         // optional, poly stride add_stride
+    const void* add1;
     uint64_t add_stride;
     uint64_t add_galois;      // automorphism applied to add reads (0 = none)
-    const uint64_t* sum0;     // optional second addend (no automorphism), poly stride sum_stride
-    const uint64_t* sum1;
+    const void* sum0;         // optional second addend (no automorphism), poly stride sum_stride
+    const void* sum1;
     uint64_t sum_stride;
-    uint64_t* out0;
-    uint64_t* out1;
+    void* out0;
+    void* out1;
     uint64_t out_stride;
     const void* p_inv;        // [L] (P^-1 mod q_r, Shoup): PairT<W>
     uint32_t count;
@@ -466,11 +467,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
     fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
     const uint32_t cta_base = rank * S::M;
     const W* accq = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + r) * n;
-    const uint64_t* add = h ? a.add1 : a.add0;
+    const W* add = static_cast<const W*>(h ? a.add1 : a.add0);
     if (add) add += c * a.add_stride + (uint64_t(r) << LOGN);
-    const uint64_t* sum = h ? a.sum1 : a.sum0;
+    const W* sum = static_cast<const W*>(h ? a.sum1 : a.sum0);
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
-    uint64_t* out = (h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
+    W* out = static_cast<W*>(h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
     const uint32_t sbt = swb<W>(threadIdx.x);
     // Epilogue in two halves: issue every global load of a half (including
@@ -484,8 +485,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t x = cta_base + threadIdx.x + (part * kHalf + jj) * S::T;
             va[jj] = static_cast<W>(__ldg(&accq[x]));
-            vb[jj] = add ? static_cast<W>(__ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x])) : 0;
-            vs[jj] = sum ? static_cast<W>(__ldg(&sum[x])) : 0;
+            vb[jj] = add ? __ldg(&add[a.add_galois ? galois_src(x, a.add_galois, LOGN) : x]) : 0;
+            vs[jj] = sum ? __ldg(&sum[x]) : 0;
         }
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddow
             u = csub<W>(u, q);
             u += vs[jj];
             u = csub<W>(u, q);
-            out[cta_base + y] = static_cast<uint64_t>(u);
+            out[cta_base + y] = u;
         }
     }
 }

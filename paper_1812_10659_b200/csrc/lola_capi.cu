@@ -211,7 +211,7 @@ int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_
 
 uint64_t lb_launch_count(void) { return lb::launch_counter().load(); }
 
-int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const uint64_t** data, uint32_t* count) {
+int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const void** data, uint32_t* count) {
     return guarded([&] {
         if (count) *count = static_cast<uint32_t>(s->output.messages.size());
         if (data) {

@@ -363,7 +363,7 @@ DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t
 
 DeviceBuffer Evaluator::lower(const Message& m) const { return lower_slots(m, {}); }
 
-const uint64_t* Evaluator::plain(const std::vector<int64_t>& values, bool for_add) {
+const void* Evaluator::plain(const std::vector<int64_t>& values, bool for_add) {
     auto& table = for_add ? cache_->add : cache_->mul;
     const uint64_t h = hash_values(values);
     auto& bucket = table[h];
@@ -381,12 +381,12 @@ const uint64_t* Evaluator::plain(const std::vector<int64_t>& values, bool for_ad
     LB_CUDA(cudaMemcpyAsync(dv.get(), full.data(), uint64_t(n) * 8, cudaMemcpyHostToDevice, s));
     auto e = std::make_unique<PlainCache::Entry>();
     e->values = values;
-    e->pt = DeviceBuffer(uint64_t(dc.T()) * dc.L() * n * 8, s);
+    e->pt = DeviceBuffer(uint64_t(dc.T()) * dc.L() * n * residue_bytes(dc.bfv()->dev), s);
     encode_plain(dc, dv.get<int64_t>(), for_add ? nullptr : e->pt.get(), for_add ? e->pt.get() : nullptr, s);
     e->made_on = s;
     LB_CUDA(cudaEventCreateWithFlags(&e->ready, cudaEventDisableTiming));
     LB_CUDA(cudaEventRecord(e->ready, s));
-    const uint64_t* p = e->pt.get();
+    const void* p = e->pt.get();
     bucket.push_back(std::move(e));
     return p;
 }
@@ -411,7 +411,7 @@ Message Evaluator::add_plain(const Message& a, const std::vector<int64_t>& value
     check_magnitude(mag, "add_plain");
     counters_.ops.add += 1;
     if (values.size() > cx_->n()) throw std::invalid_argument("plain operand: more values than slots");
-    const uint64_t* pt = plain(values, true);
+    const void* pt = plain(values, true);
     Message r = fresh(a.depth, a.plain_depth, mag);
     ct_add_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
@@ -434,7 +434,7 @@ Message Evaluator::mul_plain(const Message& a, const std::vector<int64_t>& value
     check_magnitude(mag, "mul_plain");
     counters_.ops.ct_plain_mul += 1;
     if (values.size() > cx_->n()) throw std::invalid_argument("plain operand: more values than slots");
-    const uint64_t* pt = plain(values, false);
+    const void* pt = plain(values, false);
     Message r = fresh(a.depth, a.plain_depth + 1, mag);
     ct_mul_plain(cx_->device(), a.data(), pt, r.data(), static_cast<uint32_t>(cx_->cts()), stream_);
     return r;
@@ -511,8 +511,8 @@ std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, ui
     counters_.ops.add += rows * (F - 1);
     std::vector<Message> out;
     out.reserve(rows);
-    std::vector<const uint64_t*> xp(F);
-    std::vector<uint64_t*> op(rows);
+    std::vector<const void*> xp(F);
+    std::vector<void*> op(rows);
     for (uint64_t i = 0; i < F; ++i) xp[i] = xs[i].data();
     for (uint64_t r = 0; r < rows; ++r) {
         out.push_back(fresh(depth, plain_depth, mags[r]));
@@ -522,8 +522,8 @@ std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, ui
     DeviceBuffer dx(F * 8, s), dout(rows * 8, s);
     LB_CUDA(cudaMemcpyAsync(dx.get(), xp.data(), F * 8, cudaMemcpyHostToDevice, s));
     LB_CUDA(cudaMemcpyAsync(dout.get(), op.data(), rows * 8, cudaMemcpyHostToDevice, s));
-    simd_weighted_sums(cx_->device(), reinterpret_cast<const uint64_t* const*>(dx.get()), static_cast<uint32_t>(F),
-                       reinterpret_cast<uint64_t* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w, small_w,
+    simd_weighted_sums(cx_->device(), reinterpret_cast<const void* const*>(dx.get()), static_cast<uint32_t>(F),
+                       reinterpret_cast<void* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w, small_w,
                        static_cast<uint32_t>(cx_->cts()), s);
     // dx / dout are freed stream-ordered after the kernel (cudaFreeAsync on s);
     // the host arrays were staged by the pageable-memory copies already

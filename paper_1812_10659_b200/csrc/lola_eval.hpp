@@ -79,7 +79,8 @@ struct OpCounters {
     }
 };
 
-// Device payload: [B][T][2][L][n] u64, NTT domain.
+// Device payload: [B][T][2][L][n] residue words (u32 when every ciphertext
+// and special prime is below 2^30, else u64), NTT domain.
 struct Payload {
     DeviceBuffer buf;
 };
@@ -89,7 +90,7 @@ struct Message {
     uint32_t depth = 0;
     uint32_t plain_depth = 0;
     Mag magnitude;
-    uint64_t* data() const { return payload->buf.get(); }
+    void* data() const { return payload->buf.get(); }
 };
 
 // Shared execution parameters (evaluator.hpp:16-41): device context, batch
@@ -110,7 +111,7 @@ public:
     const Mag& capacity() const { return capacity_; }
     cudaStream_t stream() const { return stream_; }
     uint64_t cts() const { return uint64_t(batch_) * cx_->T(); }
-    size_t payload_bytes() const { return cts() * 2 * cx_->L() * cx_->n() * 8; }
+    size_t payload_bytes() const { return cts() * 2 * cx_->L() * cx_->n() * residue_bytes(cx_->bfv()->dev); }
     // Side streams for fanning independent op chains out (the GPU analogue
     // of the reference's thread fan-out, proj/src/kernels.cpp:161-195).
     // LB_STREAMS (default 8) sets the count; 1 disables the fan-out.
@@ -210,7 +211,7 @@ private:
 
     Message fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const;
     void check_magnitude(const Mag& m, const char* op) const;
-    const uint64_t* plain(const std::vector<int64_t>& values, bool for_add);
+    const void* plain(const std::vector<int64_t>& values, bool for_add);
     Message shift_columns(const Message& a, uint32_t right_by, const Message* base = nullptr);
 };
 

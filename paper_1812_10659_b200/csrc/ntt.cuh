@@ -49,10 +49,11 @@ struct PrimeDev {
     uint2 ninv32, inv1n32;
 };
 
-// Arithmetic word of a kernel instance. Residues are stored as u64 in HBM
-// either way; a batch whose primes are all below 2^30 is transformed with
-// 32-bit words (values < 4q < 2^32, one IMAD.HI + two IMADs per Shoup
-// product instead of the ~14-instruction 64-bit emulation).
+// Arithmetic word of a kernel instance. A batch whose primes are all below
+// 2^30 is transformed with 32-bit words (values < 4q < 2^32, one IMAD.HI +
+// two IMADs per Shoup product instead of the ~14-instruction 64-bit
+// emulation); its storage word St is u32 (ciphertexts of such a context,
+// key-switch intermediates) or u64 (the generic limb-batch API).
 template <class W> struct WordT;
 template <> struct WordT<uint64_t> { using Pair = ulonglong2; };
 template <> struct WordT<uint32_t> { using Pair = uint2; };
@@ -106,7 +107,7 @@ struct LimbBatch {
     const int16_t* prime_map = nullptr;
     uint32_t map_period = 0;
     // inverse transform only: read the input from `src` (same [poly][limb]
-    // shape, poly stride src_stride) instead of in place, optionally through
+    // shape and word as `data`, poly stride src_stride) instead of in place, optionally through
     // the automorphism x -> x^galois on the evaluations (galois 0 = none).
     const uint64_t* src = nullptr;
     uint64_t src_stride = 0;
@@ -576,7 +577,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     const uint32_t sbt = swb<W>(threadIdx.x);
     if (b.src) {
         const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
-        const uint64_t* in = b.src + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
+        // src holds words of the batch's storage type (the key switch reads its
+        // input ciphertext, stored in the context's residue word)
+        const St* in = reinterpret_cast<const St*>(b.src) + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;

@@ -22,8 +22,9 @@ constexpr int kRowTile = 8;     // rows per thread
 constexpr int kColThreads = 256;
 constexpr int kChunk = 256;     // weights staged in smem per tile row and pass
 
-__global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const uint64_t* const* __restrict__ xs,
-                                                                  uint32_t F, uint64_t* const* __restrict__ outs,
+template <class St>
+__global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const St* const* __restrict__ xs,
+                                                                  uint32_t F, St* const* __restrict__ outs,
                                                                   uint32_t R, const int64_t* __restrict__ W,
                                                                   uint64_t cols) {
     __shared__ int64_t wsh[kRowTile][kChunk];
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const u
         __syncthreads();
         if (!live) continue;
         for (uint32_t ff = 0; ff < fc; ++ff) {
-            const uint64_t x = __ldg(&xs[f0 + ff][c]);
+            const uint64_t x = __ldg(&xs[f0 + ff][c]);  // widened
 #pragma unroll
             for (int rr = 0; rr < kRowTile; ++rr) {
                 const int64_t w = wsh[rr][ff];
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const u
         if (r0 + rr >= R) break;
         const uint64_t p = barrett_reduce_128(phi[rr], plo[rr], m);
         const uint64_t q = barrett_reduce_128(nhi[rr], nlo[rr], m);
-        outs[r0 + rr][c] = sub_mod(p, q, m.q);
+        outs[r0 + rr][c] = static_cast<St>(sub_mod(p, q, m.q));
     }
 }
 
@@ -74,9 +75,9 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums(BfvDev d, const u
 // signed 64-bit accumulator (|sum| < 2^17 * 2^15 * 2^30 = 2^62), one
 // IMAD.WIDE per term; up to 16 rows per thread divide the x loads per
 // product (fewer when R is small: the conv layers have 5 maps).
-template <int kRowTile32>
-__global__ void __launch_bounds__(kColThreads) k_weighted_sums32(BfvDev d, const uint64_t* const* __restrict__ xs,
-                                                                    uint32_t F, uint64_t* const* __restrict__ outs,
+template <int kRowTile32, class St>
+__global__ void __launch_bounds__(kColThreads) k_weighted_sums32(BfvDev d, const St* const* __restrict__ xs,
+                                                                    uint32_t F, St* const* __restrict__ outs,
                                                                     uint32_t R, const int64_t* __restrict__ W,
                                                                     uint64_t cols) {
     __shared__ int32_t wsh[kChunk][kRowTile32];
@@ -108,16 +109,15 @@ __global__ void __launch_bounds__(kColThreads) k_weighted_sums32(BfvDev d, const
         if (r0 + rr >= R) break;
         const int64_t v = acc[rr];
         const uint64_t a = reduce_u64(static_cast<uint64_t>(v < 0 ? -v : v), m);
-        outs[r0 + rr][c] = v < 0 ? neg_mod(a, m.q) : a;
+        outs[r0 + rr][c] = static_cast<St>(v < 0 ? neg_mod(a, m.q) : a);
     }
 }
 
 }  // namespace
 
-void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint64_t* const* outs, uint32_t R,
-                        const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s) {
-    if (!F || !R) return;
-    if (F >= (1u << 17)) throw std::invalid_argument("weighted sums: fan-in above 2^17");
+template <class St>
+static void weighted_sums_words(Context& cx, const St* const* xs, uint32_t F, St* const* outs, uint32_t R,
+                                const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     const uint64_t cols = uint64_t(cts) * 2 * d.L * d.n;
     if (small_weights && cx.primes_small(0, d.L)) {
@@ -125,17 +125,30 @@ void simd_weighted_sums(Context& cx, const uint64_t* const* xs, uint32_t F, uint
         const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + tile - 1) / tile);
         if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
         if (tile == 4)
-            k_weighted_sums32<4><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+            k_weighted_sums32<4, St><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
         else if (tile == 8)
-            k_weighted_sums32<8><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+            k_weighted_sums32<8, St><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
         else
-            k_weighted_sums32<16><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+            k_weighted_sums32<16, St><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
     } else {
         const dim3 grid(static_cast<unsigned>((cols + kColThreads - 1) / kColThreads), (R + kRowTile - 1) / kRowTile);
         if (grid.y > 65535) throw std::invalid_argument("weighted sums: too many rows");
-        k_weighted_sums<<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
+        k_weighted_sums<St><<<grid, kColThreads, 0, s>>>(d, xs, F, outs, R, W, cols);
     }
     LB_KERNEL_DONE();
+}
+
+void simd_weighted_sums(Context& cx, const void* const* xs, uint32_t F, void* const* outs, uint32_t R,
+                        const int64_t* W, bool small_weights, uint32_t cts, cudaStream_t s) {
+    if (!F || !R) return;
+    if (F >= (1u << 17)) throw std::invalid_argument("weighted sums: fan-in above 2^17");
+    // xs / outs: device arrays of device pointers to residue words
+    if (cx.bfv()->dev.ks32)
+        weighted_sums_words(cx, reinterpret_cast<const uint32_t* const*>(xs), F, reinterpret_cast<uint32_t* const*>(outs),
+                            R, W, small_weights, cts, s);
+    else
+        weighted_sums_words(cx, reinterpret_cast<const uint64_t* const*>(xs), F, reinterpret_cast<uint64_t* const*>(outs),
+                            R, W, small_weights, cts, s);
 }
 
 }  // namespace lb

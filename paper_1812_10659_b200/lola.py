@@ -157,7 +157,8 @@ class Session:
         p, cnt = vp(), C.c_uint32()
         nat.call("lb_lola_session_output", self.handle, index, C.byref(p), C.byref(cnt))
         shape = (self.batch, len(self.cx.params.t), 2, len(self.cx.params.q), self.cx.n)
-        return torch.as_tensor(_DevPtr(p.value, shape), device="cuda").clone()
+        typestr = "<i4" if self.cx.res_dtype == torch.int32 else "<i8"
+        return torch.as_tensor(_DevPtr(p.value, shape, typestr), device="cuda").clone()
 
     def run(self, images: np.ndarray):
         """Host images [batch][input_values] -> (scores [batch][outputs] Python

@@ -16,11 +16,13 @@ pytestmark = pytest.mark.gpu
 
 
 # 60-bit primes run the 64-bit word kernels; 30-bit primes (< 2^30) the
-# 32-bit word NTT / key-switch kernels, with 1-, 3- and 4-prime digits.
+# 32-bit word NTT / key-switch kernels with u32 residue storage, with 1-, 3-,
+# 4- and 5-prime digits (the last: the lola-mnist default digit structure).
 @pytest.fixture(scope="module", params=[(4096, 3, 2, 1, 0, 60), (8192, 4, 1, 1, 0, 60), (4096, 5, 2, 2, 3, 60),
-                                        (4096, 6, 2, 3, 2, 30), (8192, 10, 2, 4, 3, 30), (4096, 4, 1, 1, 4, 30)],
+                                        (4096, 6, 2, 3, 2, 30), (8192, 10, 2, 4, 3, 30), (4096, 4, 1, 1, 4, 30),
+                                        (8192, 10, 2, 5, 2, 29)],
                 ids=["n4096_L3_T2", "n8192_L4_T1", "n4096_L5_K2_dnum3", "w32_n4096_L6_K3_dnum2",
-                     "w32_n8192_L10_K4_dnum3", "w32_n4096_L4_K1"])
+                     "w32_n8192_L10_K4_dnum3", "w32_n4096_L4_K1", "w32_n8192_L10_K5_dnum2"])
 def env(request):
     n, L, T, K, dnum, bits = request.param
     prm = make_params(n, L=L, T=T, K=K, dnum=dnum, bits=bits, seed=11)
@@ -31,7 +33,7 @@ def env(request):
 
 def coeffs(cx, ct: torch.Tensor) -> np.ndarray:
     """Device ciphertexts (evaluation domain) -> coefficient numpy [count][2][L][n]."""
-    x = ct.reshape(-1, 2, cx.L, cx.n).clone()
+    x = ct.reshape(-1, 2, cx.L, cx.n).to(torch.int64, copy=True)  # residue words -> the NTT engine's u64 limbs
     cx.ntt_inverse(x, limbs=cx.L)
     torch.cuda.synchronize()
     return x.cpu().numpy().astype(np.uint64)

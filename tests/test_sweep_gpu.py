@@ -23,7 +23,7 @@ SWEEP32 = [(4096, 12), (16384, 14), (32768, 6)]
 
 
 def coeffs(cx, ct):
-    x = ct.reshape(-1, 2, cx.L, cx.n).clone()
+    x = ct.reshape(-1, 2, cx.L, cx.n).to(torch.int64, copy=True)  # residue words -> the NTT engine's u64 limbs
     cx.ntt_inverse(x, limbs=cx.L)
     torch.cuda.synchronize()
     return x.cpu().numpy().astype(np.uint64)

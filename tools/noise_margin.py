@@ -50,7 +50,7 @@ def main():
     while True:
         try:
             dev = sess.output_ciphertexts(outs)
-            x = dev.reshape(-1, prm.L, prm.n).contiguous()
+            x = dev.reshape(-1, prm.L, prm.n).to(torch.int64)
             cx.ntt_inverse(x, limbs=prm.L)  # evaluation -> coefficient domain (the oracle's layout)
             torch.cuda.synchronize()
             cts = x.reshape(dev.shape).cpu().numpy().astype(np.uint64)
