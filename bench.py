@@ -292,7 +292,7 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
     per_limb, src = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned long>")) \
-        if word == 32 else (None, None)
+        if word == 32 else (None, None)  # the generic limb-batch API (u64 limbs)
     return {
         "kernel": f"ntt_forward_kernel<14, u{word}> ({polys * L} limbs of n={n}, "
                   f"{max(cx.params.q).bit_length()}-bit q, {word}-bit words)",
@@ -358,9 +358,15 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     achieved = count * products / (ms * 1e-3) / 1e9
     achieved_bfly = count * bfly / (ms * 1e-3) / 1e9
     del ct, out
-    ks_names = ("ks_inner", "moddown_kernel", "ntt_inverse_kernel<14, unsigned int, unsigned int>",
-                "ntt_inverse_kernel<14, unsigned int, unsigned long>")
-    per_ct, src = ncu_traffic(lambda k: k.startswith(ks_names)) if word == 32 else (None, None)
+    per_ct, src = None, None
+    if word == 32:
+        try:
+            tj = json.loads(TRAFFIC_JSON.read_text())
+            if tj["params"]["L"] == L and tj["params"]["K"] == K:
+                per_ct = tj["key_switch_bytes_per_ciphertext"]
+                src = f"{TRAFFIC_JSON.relative_to(ROOT)}: ks_inner + moddown + the two inverse NTTs, per ciphertext"
+        except Exception:
+            pass
     return {
         "kernel": f"key switch = ntt_inverse + ks_inner_kernel + ntt_inverse(P) + moddown_kernel, u{word} words, "
                   f"{count} ciphertext rotations per launch set (n={n}, L={L}, K={K}, dnum={dnum})",

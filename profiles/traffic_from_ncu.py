@@ -33,29 +33,45 @@ def read(path):
 
 def main():
     out_path, L, K, CL = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
-    res = {"source": "ncu --set full --clock-control none, one launch per kernel inside one lola-mnist step "
+    res = {"source": "ncu --set full --clock-control none, launches inside one lola-mnist step "
                      "(tools/gpu_profile.sh); DRAM bytes = dram__bytes_read.sum + dram__bytes_write.sum",
            "params": {"L": L, "K": K, "cluster": CL}, "kernels": {}}
+    acc = {}
     for path in sys.argv[5:]:
         for name, grid, rd, wr, dur in read(path):
-            base = name.split("(")[0]
+            base = name.split("(")[0].replace("void ", "").replace("lb::", "").strip()
             if "ks_inner" in base:
-                unit, per = "ciphertext", grid // ((L + K) * CL)
+                unit, per, launches = "ciphertext", grid // ((L + K) * CL), 1
             elif "moddown" in base:
-                unit, per = "ciphertext", grid // (2 * L * CL)
-            elif "ntt_inverse_kernel" in base and "unsigned int, unsigned int" in base:
-                unit, per = "ciphertext (2K P limbs)", grid // (2 * K * CL)
-            elif "ntt_inverse_kernel" in base and "unsigned int, unsigned long" in base:
-                unit, per = "ciphertext (L input limbs)", grid // (L * CL)
+                unit, per, launches = "ciphertext", grid // (2 * L * CL), 1
+            elif "ntt_inverse_kernel" in base and base.endswith("unsigned int, unsigned int>"):
+                # the key switch's two inverse transforms (input: L limbs, P limbs of
+                # both accumulators: 2K limbs) share this instance
+                unit, per, launches = "limb", grid // CL, None
             elif "ntt_" in base:
-                unit, per = "limb", grid // CL
+                unit, per, launches = "limb", grid // CL, None
             else:
-                unit, per = "launch", 1
-            res["kernels"][base] = {"unit": unit, "units_in_launch": per, "dram_read_mb": rd, "dram_write_mb": wr,
-                                    "bytes_per_unit": (rd + wr) * 1e6 / per, "duration_us": dur}
+                unit, per, launches = "launch", 1, None
+            a = acc.setdefault(base, {"unit": unit, "units": 0, "bytes": 0.0, "us": 0.0, "n": 0})
+            a["units"] += per
+            a["bytes"] += (rd + wr) * 1e6
+            a["us"] += dur
+            a["n"] += 1
+    for base, a in acc.items():
+        res["kernels"][base] = {"unit": a["unit"], "launches_captured": a["n"], "units_captured": a["units"],
+                                "bytes_per_unit": a["bytes"] / a["units"], "mean_duration_us": a["us"] / a["n"]}
+    # composite: DRAM bytes of one key switch per ciphertext
+    per_ct = 0.0
+    for base, v in res["kernels"].items():
+        if "ks_inner" in base or "moddown" in base:
+            per_ct += v["bytes_per_unit"]
+        elif "ntt_inverse_kernel" in base and base.endswith("unsigned int, unsigned int>"):
+            per_ct += v["bytes_per_unit"] * (L + 2 * K)
+    res["key_switch_bytes_per_ciphertext"] = per_ct
     json.dump(res, open(out_path, "w"), indent=1)
     for k, v in res["kernels"].items():
-        print(f"{k:60s} {v['units_in_launch']:5d} {v['unit']:28s} {v['bytes_per_unit'] / 1e6:8.3f} MB/unit")
+        print(f"{k:60s} {v['units_captured']:6d} {v['unit']:12s} {v['bytes_per_unit'] / 1e6:8.3f} MB/unit")
+    print(f"key switch: {per_ct / 1e6:.3f} MB per ciphertext")
 
 
 if __name__ == "__main__":
