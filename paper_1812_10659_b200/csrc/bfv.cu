@@ -177,6 +177,18 @@ __global__ void k_enc_coeffs(BfvDev d, const uint64_t* __restrict__ mcoef, uint3
     const uint64_t t = d.primes[d.tbase + j].q;
     const uint64_t extra = (d.q_mod_t[j] * mval + (t >> 1)) / t;
     St* out = ct + c * 2 * d.L * d.n + k;
+    if constexpr (sizeof(St) == 4) {
+        // every q_i < 2^30 and t < 2^32: Shoup products in 32-bit words
+        for (uint32_t i = 0; i < d.L; ++i) {
+            const uint32_t q = static_cast<uint32_t>(d.primes[i].q);
+            const uint2 dl = d.delta32[j * d.L + i], one = d.one32[i];
+            const uint32_t a = shoup_full<uint32_t>(static_cast<uint32_t>(mval), dl.x, dl.y, q);
+            const uint32_t b = shoup_full<uint32_t>(static_cast<uint32_t>(extra), 1u, one.y, q);
+            const uint32_t ee = e < 0 ? q - static_cast<uint32_t>(-e) : static_cast<uint32_t>(e);  // |e| <= 21
+            out[uint64_t(i) * d.n] = csub<uint32_t>(csub<uint32_t>(a + b, q) + ee, q);
+        }
+        return;
+    }
     for (uint32_t i = 0; i < d.L; ++i) {
         const Modulus qm = modulus_of(d.primes[i]);
         const uint64_t sm = add_mod(mul_mod(d.delta[j * d.L + i], mval, qm), reduce_u64(extra, qm), qm.q);
@@ -202,7 +214,15 @@ __global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, St* __r
     St* c0 = ct + (c * 2 * d.L + i) * d.n;
     St* c1 = c0 + uint64_t(d.L) * d.n;
     c1[pos] = static_cast<St>(a);
-    c0[pos] = static_cast<St>(sub_mod(c0[pos], mul_mod(a, d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q));
+    if constexpr (sizeof(St) == 4) {
+        const uint32_t q = static_cast<uint32_t>(qm.q);
+        const uint2 sp = d.s32[uint64_t(i) * d.n + pos];
+        const uint32_t as = shoup_full<uint32_t>(static_cast<uint32_t>(a), sp.x, sp.y, q);
+        const uint32_t v = c0[pos];
+        c0[pos] = v >= as ? v - as : v + q - as;
+    } else {
+        c0[pos] = static_cast<St>(sub_mod(c0[pos], mul_mod(a, d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q));
+    }
 }
 
 // pt_mul = centered lift of m; pt_add = round(Q m / t); m: [T][n]
@@ -232,7 +252,13 @@ __global__ void k_phase(BfvDev d, const St* __restrict__ ct, uint32_t count, uin
     const Modulus qm = modulus_of(d.primes[i]);
     const St* c0 = ct + (c * 2 * d.L + i) * d.n;
     const St* c1 = c0 + uint64_t(d.L) * d.n;
-    x[idx] = add_mod(c0[pos], mul_mod(c1[pos], d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
+    if constexpr (sizeof(St) == 4) {
+        const uint32_t q = static_cast<uint32_t>(qm.q);
+        const uint2 sp = d.s32[uint64_t(i) * d.n + pos];
+        x[idx] = csub<uint32_t>(c0[pos] + shoup_full<uint32_t>(c1[pos], sp.x, sp.y, q), q);
+    } else {
+        x[idx] = add_mod(c0[pos], mul_mod(c1[pos], d.s_ntt[uint64_t(i) * d.n + pos], qm), qm.q);
+    }
 }
 
 // m = round(t x / Q) mod t from coefficient residues x: [count][L][n]
@@ -682,8 +708,16 @@ void bfv_setup(Context& cx) {
         }
         return o;
     };
-    size_t o_pi32 = 0, o_dh32 = 0, o_ph32 = 0, o_klq32 = 0, o_klp32 = 0;
+    size_t o_pi32 = 0, o_dh32 = 0, o_ph32 = 0, o_klq32 = 0, o_klp32 = 0, o_de32 = 0, o_one32 = 0;
     if (d.ks32) {
+        std::vector<uint2> de32(size_t(T) * L), one32(L);
+        for (uint32_t j = 0; j < T; ++j)
+            for (uint32_t i = 0; i < L; ++i)
+                de32[j * L + i] = make_uint2(static_cast<uint32_t>(delta[j * L + i]),
+                                             shoup_companion32(delta[j * L + i], q[i]));
+        for (uint32_t i = 0; i < L; ++i) one32[i] = make_uint2(1u, shoup_companion32(1, q[i]));
+        o_de32 = put(de32.data(), std::max<size_t>(1, de32.size()) * 8);
+        o_one32 = put(one32.data(), one32.size() * 8);
         const auto pi32 = to32(p_inv_shoup, [&](size_t k) { return q[k]; });
         const auto dh32 = to32(dhat_mod_sh, [&](size_t k) { return qp[k % LK]; });
         const auto ph32 = to32(phat_mod_sh, [&](size_t k) { return K ? q[k % L] : 0; });
@@ -749,6 +783,8 @@ void bfv_setup(Context& cx) {
         d.phat_mod_sh32 = reinterpret_cast<const uint2*>(base + o_ph32);
         d.ks_last_q32 = reinterpret_cast<const uint2*>(base + o_klq32);
         d.ks_last_p32 = reinterpret_cast<const uint2*>(base + o_klp32);
+        d.delta32 = reinterpret_cast<const uint2*>(base + o_de32);
+        d.one32 = reinterpret_cast<const uint2*>(base + o_one32);
     }
     {
         // HPS scaling computes round(t D / Q) in base B, |D| < n Q^2 / 4
@@ -771,6 +807,14 @@ void bfv_setup(Context& cx) {
     d.s_ntt = st->secret.get();
     cx.bfv_ = std::move(st);
     cx.ntt_forward(LimbBatch{cx.bfv_->secret.get(), 1, nsec, 0, uint64_t(nsec) * n}, s);
+    if (d.ks32) {
+        BfvState& bs = *cx.bfv_;
+        bs.secret32 = DeviceBuffer(uint64_t(L) * n * 8, s);
+        k_shoup_pairs32<<<grid_for(uint64_t(L) * n), kBlock, 0, s>>>(d, d.s_ntt, bs.secret32.get<uint2>(),
+                                                                      uint64_t(L) * n, L);
+        LB_KERNEL_DONE();
+        d.s32 = bs.secret32.get<uint2>();
+    }
     LB_CUDA(cudaStreamSynchronize(s));
 }
 

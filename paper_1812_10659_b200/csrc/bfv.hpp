@@ -70,6 +70,11 @@ struct BfvDev {
     const uint2* phat_mod_sh32;      // [K][L]
     const uint2* ks_last_q32;        // [L][2]
     const uint2* ks_last_p32;        // [K][2]
+    // 32-bit encryption / decryption constants (ks32): floor(Q/t_j) mod q_i
+    // and 1 with their companions, and the secret's evaluations over Q
+    const uint2* delta32;            // [T][L]
+    const uint2* one32;              // [L] (1, floor(2^32 / q_i))
+    const uint2* s32;                // [L][n]
 };
 
 // Residue word of a context's ciphertexts and plaintext operands in HBM:
@@ -95,6 +100,7 @@ struct BfvState {
     bool mul_base_ok = false;         // B large enough for the exact tensor product
     const int16_t* ks_map = nullptr;  // [dnum][L+K]  Q∪P minus digit j's primes
     DeviceBuffer secret;
+    DeviceBuffer secret32;  // ks32: (s mod q_i, companion) over Q, uint2 [L][n]
     std::map<uint64_t, KsKey> keys;  // key id -> key (0 = relinearization)
     std::mutex mu;
 };
