@@ -116,13 +116,15 @@ namespace {
 constexpr int kBlock = 256;
 inline unsigned blocks(uint64_t work) { return static_cast<unsigned>(std::max<uint64_t>(1, (work + kBlock - 1) / kBlock)); }
 
+// out[m][b][s] = images[b * stride + map[m][s]] (0 where the map is < 0)
 __global__ void k_gather_lift(const int64_t* __restrict__ images, uint64_t stride, const int32_t* __restrict__ map,
-                              uint32_t n, uint32_t B, int64_t* __restrict__ out) {
+                              uint32_t n, uint32_t B, uint32_t maps, int64_t* __restrict__ out) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (idx >= uint64_t(B) * n) return;
+    if (idx >= uint64_t(maps) * B * n) return;
     const uint32_t s = idx % n;
-    const uint64_t b = idx / n;
-    const int32_t src = map[s];
+    const uint64_t b = (idx / n) % B;
+    const uint64_t m = idx / (uint64_t(n) * B);
+    const int32_t src = map[m * n + s];
     out[idx] = src < 0 ? 0 : images[b * stride + src];
 }
 
@@ -303,23 +305,37 @@ Message Evaluator::lift_batch(const std::vector<std::vector<int64_t>>& values) c
 
 Message Evaluator::lift_gather(const int64_t* dev_images, uint64_t stride, const std::vector<int32_t>& map,
                                int64_t max_abs) const {
+    return lift_gather_many(dev_images, stride, {map}, max_abs).front();
+}
+
+std::vector<Message> Evaluator::lift_gather_many(const int64_t* dev_images, uint64_t stride,
+                                                 const std::vector<std::vector<int32_t>>& maps,
+                                                 int64_t max_abs) const {
     const uint32_t n = cx_->n(), B = cx_->batch();
-    if (map.size() > n) throw std::invalid_argument("lift: more values than slots");
-    std::vector<int32_t> full(n, -1);
-    std::copy(map.begin(), map.end(), full.begin());
+    const uint32_t count = static_cast<uint32_t>(maps.size());
+    if (!count) return {};
+    std::vector<int32_t> full(uint64_t(count) * n, -1);
+    for (uint32_t m = 0; m < count; ++m) {
+        if (maps[m].size() > n) throw std::invalid_argument("lift: more values than slots");
+        std::copy(maps[m].begin(), maps[m].end(), full.begin() + uint64_t(m) * n);
+    }
     const Mag mag(static_cast<uint64_t>(max_abs < 0 ? -max_abs : max_abs));
     check_magnitude(mag, "lift");
     cudaStream_t s = stream_;
-    DeviceBuffer dmap(uint64_t(n) * 4, s), slots(uint64_t(B) * n * 8, s);
-    LB_CUDA(cudaMemcpyAsync(dmap.get(), full.data(), uint64_t(n) * 4, cudaMemcpyHostToDevice, s));
-    k_gather_lift<<<blocks(uint64_t(B) * n), kBlock, 0, s>>>(dev_images, stride, dmap.get<int32_t>(), n, B,
-                                                             slots.get<int64_t>());
+    DeviceBuffer dmap(full.size() * 4, s), slots(uint64_t(count) * B * n * 8, s);
+    LB_CUDA(cudaMemcpyAsync(dmap.get(), full.data(), full.size() * 4, cudaMemcpyHostToDevice, s));
+    k_gather_lift<<<blocks(uint64_t(count) * B * n), kBlock, 0, s>>>(dev_images, stride, dmap.get<int32_t>(), n, B,
+                                                                      count, slots.get<int64_t>());
     LB_KERNEL_DONE();
-    Message m = fresh(0, 0, mag);
-    const uint64_t id = *next_id_;
-    *next_id_ += cx_->cts();
-    encrypt_slots(cx_->device(), slots.get<int64_t>(), B, id, m.data(), s);
-    return m;
+    std::vector<Message> out;
+    out.reserve(count);
+    for (uint32_t m = 0; m < count; ++m) {
+        out.push_back(fresh(0, 0, mag));
+        const uint64_t id = *next_id_;
+        *next_id_ += cx_->cts();
+        encrypt_slots(cx_->device(), slots.get<int64_t>() + uint64_t(m) * B * n, B, id, out.back().data(), s);
+    }
+    return out;
 }
 
 DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t>& slots) const {

@@ -159,6 +159,11 @@ public:
     Message lift_batch(const std::vector<std::vector<int64_t>>& values) const;
     Message lift_gather(const int64_t* dev_images, uint64_t stride, const std::vector<int32_t>& map,
                         int64_t max_abs) const;
+    // lift_gather for several maps at once (one upload of the maps, one
+    // gather, then the messages' encryptions back to back with no host sync);
+    // messages and ciphertext ids in map order, as repeated lift_gather calls
+    std::vector<Message> lift_gather_many(const int64_t* dev_images, uint64_t stride,
+                                          const std::vector<std::vector<int32_t>>& maps, int64_t max_abs) const;
     // Decrypt + CRT + center every slot: device [B][n] signed 256-bit
     // (4 little-endian words, two's complement). lower_slots gathers only
     // the listed slots: [B][slots.size()] words.

@@ -146,14 +146,13 @@ EncodedTensor encode_convolution(Evaluator& ev, const int64_t* dev_images, uint6
     t.rep.length = positions;
     t.rep.windows = r;
     if (row_split) t.rep.slot_of = layout;
-    for (uint32_t j = 0; j < r; ++j) {
-        std::vector<int32_t> map(n, -1);
+    std::vector<std::vector<int32_t>> maps(r, std::vector<int32_t>(n, -1));
+    for (uint32_t j = 0; j < r; ++j)
         for (uint32_t w = 0; w < positions; ++w) {
             auto src = g.tap(j, w);
-            if (src) map[layout[w]] = static_cast<int32_t>(*src);
+            if (src) maps[j][layout[w]] = static_cast<int32_t>(*src);
         }
-        t.messages.push_back(ev.lift_gather(dev_images, stride, map, max_abs));
-    }
+    t.messages = ev.lift_gather_many(dev_images, stride, maps, max_abs);
     return t;
 }
 
@@ -693,10 +692,16 @@ EncodedTensor encode_simd(Evaluator& ev, const int64_t* dev_images, uint64_t fea
     t.rep.kind = RepKind::Simd;
     t.rep.length = features;
     t.rep.copies = recs;
-    std::vector<int32_t> map(recs);
-    for (uint64_t j = 0; j < features; ++j) {
-        for (uint32_t r = 0; r < recs; ++r) map[r] = static_cast<int32_t>(uint64_t(r) * features + j);
-        t.messages.push_back(ev.lift_gather(dev_images, features, map, max_abs));
+    // in groups (the gathered slot values of a group are staged at once)
+    constexpr uint64_t kGroup = 64;
+    for (uint64_t j0 = 0; j0 < features; j0 += kGroup) {
+        std::vector<std::vector<int32_t>> maps;
+        for (uint64_t j = j0; j < std::min(features, j0 + kGroup); ++j) {
+            std::vector<int32_t> map(recs);
+            for (uint32_t r = 0; r < recs; ++r) map[r] = static_cast<int32_t>(uint64_t(r) * features + j);
+            maps.push_back(std::move(map));
+        }
+        for (Message& m : ev.lift_gather_many(dev_images, features, maps, max_abs)) t.messages.push_back(std::move(m));
     }
     return t;
 }
