@@ -7,7 +7,8 @@ stays below Q/2; margin = log2(Q/2) - log2(max |[t x]_Q|) bits. Also checks
 the decrypted logits against forward_integer and times one batched step.
 
 usage: python tools/noise_margin.py L K dnum bits [batch] [workload]
-(workload lola-mnist: n = 16384, 5 plaintext primes; lola-small: n = 8192, 2)"""
+(workload lola-mnist: n = 16384, 5 plaintext primes; lola-small: n = 8192, 2;
+lola-cifar: n = 16384, 6)"""
 import math
 import sys
 import time
@@ -31,12 +32,13 @@ def main():
     from paper_1812_10659_b200.lola import Session
     from paper_1812_10659_b200.params import make_params
 
-    n, T, cfg = (16384, 5, 2) if workload == "lola-mnist" else (8192, 2, 3)
+    n, T, cfg = {"lola-mnist": (16384, 5, 2), "lola-small": (8192, 2, 3), "lola-cifar": (16384, 6, 4)}[workload]
     prm = make_params(n, L=L, T=T, K=K, dnum=dnum, bits=bits)
     print(f"L={L} K={K} dnum={dnum} bits={bits}: log2 QP = {prm.log_qp():.1f}, log2 Q = "
           f"{sum(math.log2(v) for v in prm.q):.1f}", flush=True)
     cx = BfvContext(prm)
-    net = nets.lola_mnist_net(config=2) if workload == "lola-mnist" else nets.lola_small_net(config=3)
+    net = {"lola-mnist": lambda: nets.lola_mnist_net(config=2), "lola-small": lambda: nets.lola_small_net(config=3),
+           "lola-cifar": lambda: nets.lola_cifar_net(config=4)}[workload]()
     sess = Session(cx, net, workload, batch)
     imgs = nets.images(cfg, net, batch)
     scores, _, _ = sess.run(imgs)
@@ -72,19 +74,20 @@ def main():
           f"{math.log2(Q / 2) - math.log2(worst):.1f} bits", flush=True)
     del sess
     torch.cuda.empty_cache()
-    B = 64 if workload == "lola-mnist" else 256
+    B = {"lola-mnist": 64, "lola-small": 256, "lola-cifar": 1}[workload]
     sess = Session(cx, net, workload, B)
     sess.encrypt(torch.from_numpy(nets.images(cfg, net, B)).cuda(), on_device=True)
-    for _ in range(3):
+    reps = 1 if workload == "lola-cifar" else 3
+    for _ in range(reps):
         sess.execute()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(3):
+    for _ in range(reps):
         sess.execute()
     e1.record()
     torch.cuda.synchronize()
-    print(f"throughput B={B}: {3 * B / (e0.elapsed_time(e1) / 1e3):.1f} images/s", flush=True)
+    print(f"throughput B={B}: {reps * B / (e0.elapsed_time(e1) / 1e3):.2f} images/s", flush=True)
 
 
 if __name__ == "__main__":
