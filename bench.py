@@ -52,9 +52,8 @@ def workload_objects(name: str, word: int = 64):
     if name == "lola-small":
         prm = params.lola_small_params_w32() if word == 32 else params.lola_small_params()
         return cfg, strategy, batch, nets.lola_small_net(config=3), prm
-    # config 4 stays on 60-bit primes: with u64 storage its 12-limb 30-bit
-    # chain does not fit the plan's live messages in 180 GB
-    return cfg, strategy, batch, nets.lola_cifar_net(config=4), params.lola_cifar_params()
+    prm = params.lola_cifar_params_w32() if word == 32 else params.lola_cifar_params()
+    return cfg, strategy, batch, nets.lola_cifar_net(config=4), prm
 
 
 def parse():
@@ -70,8 +69,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
     ap.add_argument("--word", type=int, default=32, choices=[32, 64],
-                    help="RNS word: 32 = 30-bit primes (32-bit word kernels, default), 64 = 60-bit primes "
-                         "(lola-cifar always 64)")
+                    help="RNS word: 32 = 29/30-bit primes (32-bit word kernels, u32 residues; default), "
+                         "64 = 54/60-bit primes")
     return ap.parse_args()
 
 

@@ -127,11 +127,12 @@ struct LimbBatch {
 };
 
 // Evaluation-domain source position of x under x -> x^g (bit-reversed order).
+// g < 2n <= 2^16 and 2k + 1 < 2n, so the product fits 32 bits.
 __device__ __forceinline__ uint32_t galois_src(uint32_t x, uint64_t g, int logn) {
     const uint32_t n = 1u << logn;
     const uint32_t k = __brev(x) >> (32 - logn);
-    const uint64_t e = (g * (2ull * k + 1)) & (2ull * n - 1);
-    return __brev(static_cast<uint32_t>((e - 1) >> 1)) >> (32 - logn);
+    const uint32_t e = (static_cast<uint32_t>(g) * (2u * k + 1u)) & (2u * n - 1u);
+    return __brev((e - 1u) >> 1) >> (32 - logn);
 }
 
 #ifndef LB_NTT_LOGE
@@ -541,6 +542,88 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     }
 }
 
+// Cross-CTA pass tail: stages 3, 2, 1 as usual; stage 0 with the scaled
+// n^-1 pairs merged (c0 for the first half, c1 = psi^-bitrev(1) n^-1 s).
+template <class W>
+__device__ __forceinline__ void inv_final(W (&r)[kE], const PairT<W>* __restrict__ tw, W q, PairT<W> c0,
+                                          PairT<W> c1) {
+    const W two_q = 2 * q;
+    inv_stages<kLogE, kLogE - 1, 1, W>(r, tw, 0, 0, q, two_q);
+    constexpr int half0 = kE / 2;
+#pragma unroll
+    for (int k = 0; k < half0; ++k) {
+        W x = r[k], y = r[k + half0];
+        W s = x + y;  // < 4q
+        W d = x - y + two_q;
+        r[k] = shoup_full<W>(s, c0.x, c0.y, q);
+        r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
+    }
+}
+
+// Push-based inverse transform core (cluster limbs, LB_NTT_MBAR). On entry
+// `sm` holds this CTA's chunk of the evaluations (swizzled, values < 2q,
+// visible to every thread: the caller synchronised); `recv` is a fresh
+// receive plane of M words and `mbar` this CTA's mbarrier for it (count =
+// threads, phase `parity`). Peers must have initialised their mbarriers
+// (start_wait: wait here on the cluster barrier the caller arrived on).
+// On return r[k] = coefficient rho + k * NE (rho = rank * T + thread), fully
+// reduced, scaled by the final-stage pairs c0 (n^-1 s) and c1.
+template <int LOGN, class W>
+__device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uint32_t parity, const PrimeDev& P,
+                                              uint32_t rank, PairT<W> c0, PairT<W> c1, bool start_wait,
+                                              W (&r)[kE]) {
+    using S = NttShape<LOGN>;
+    static_assert(S::CL > 1, "push exchange needs a cluster");
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = inv_table<W>(P);
+    const uint32_t cta_base = rank * S::M;
+    constexpr int kTail = (LOGN - kLogE) % kLogE;
+    if constexpr (kTail > 0) {
+        local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int s0 = LOGN - kTail - kLogE; s0 >= 2 * kLogE; s0 -= kLogE) {
+        local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
+        __syncthreads();
+    }
+    // stages 7..4 (s0 = kLogE, one radix-16 group per thread): block bb,
+    // offset o; element k (chunk index bb*NE + o + k*stride) belongs to
+    // CTA k / PER_CTA, thread o + (k % PER_CTA) * stride, slot
+    // (rank * PER_CTA + bb) of its receive plane
+    constexpr uint32_t stride = S::N >> (2 * kLogE);
+    static_assert(S::T % stride == 0 && S::T / stride == S::PER_CTA, "push layout");
+    const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
+    const uint32_t sb = swb<W>(bb * S::NE + o);
+#pragma unroll
+    for (int k = 0; k < kE; ++k) r[k] = sm_at(sm, sb, k * stride);
+    inv_group<kLogE>(r, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
+    if (start_wait) cluster_wait();
+    const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
+    const uint32_t lrecv = smem_addr(recv + slot);
+#pragma unroll
+    for (int dst = 0; dst < S::CL; ++dst) {
+        if (dst == static_cast<int>(rank)) {
+#pragma unroll
+            for (int i = 0; i < S::PER_CTA; ++i) recv[slot + i * stride] = r[dst * S::PER_CTA + i];
+        } else {
+            const uint32_t rb = mapa_rank(lrecv, dst), rm = mapa_rank(mbar, dst);
+#pragma unroll
+            for (int i = 0; i < S::PER_CTA; ++i)
+                st_async(rb + i * stride * static_cast<uint32_t>(sizeof(W)), r[dst * S::PER_CTA + i], rm);
+        }
+    }
+    constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+    if (threadIdx.x == 0)
+        mbar_arrive_tx(mbar, kRemoteBytes);
+    else
+        mbar_arrive(mbar);
+    mbar_wait(mbar, parity);
+#pragma unroll
+    for (int k = 0; k < kE; ++k) r[k] = recv[k * S::T + threadIdx.x];
+    inv_final<W>(r, tw, q, c0, c1);
+}
+
 // Inverse transform. With LB_NTT_MBAR the cross-CTA pass is push-based: the
 // last local pass (stages 7..4) sends its outputs straight from registers to
 // the owning CTA's receive plane (st.async + complete_tx), so the owner waits
@@ -595,58 +678,36 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         }
     }
     __syncthreads();
-    // Local passes in reverse: the last (possibly short) chunk first.
-    constexpr int kTail = (LOGN - kLogE) % kLogE;
-    if constexpr (kTail > 0) {
-        local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
-        __syncthreads();
+    PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
+    {
+        const PairT<W>* last = nullptr;
+        if constexpr (sizeof(W) == 8)
+            last = b.last_stage;
+        else
+            last = b.last_stage32;
+        if (last) {
+            const uint32_t l = limb_id % b.limbs;
+            c0 = last[2 * l];
+            c1 = last[2 * l + 1];
+        }
     }
-    constexpr int kLastLocal = kPush ? 2 * kLogE : kLogE;  // the push pass handles s0 = kLogE itself
-#pragma unroll
-    for (int s0 = LOGN - kTail - kLogE; s0 >= kLastLocal; s0 -= kLogE) {
-        local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
-        __syncthreads();
-    }
-
-    // Cross-CTA pass: stages 3..0 over the elements rho + k * NE, n^-1 folded in.
     const uint32_t rho = rank * S::T + threadIdx.x;
     W r[kE];
     if constexpr (kPush) {
-        // stages 7..4 (s0 = kLogE, one radix-16 group per thread): block bb,
-        // offset o; element k (chunk index bb*NE + o + k*stride) belongs to
-        // CTA k / PER_CTA, thread o + (k % PER_CTA) * stride, slot
-        // (rank * PER_CTA + bb) of its receive plane
-        constexpr uint32_t stride = S::N >> (2 * kLogE);
-        static_assert(S::T % stride == 0 && S::T / stride == S::PER_CTA, "push layout");
-        const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
-        const uint32_t sb = swb<W>(bb * S::NE + o);
-#pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = sm_at(sm, sb, k * stride);
-        inv_group<kLogE>(r, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
-        cluster_wait();
-        const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
-        const uint32_t lrecv = smem_addr(recv + slot);
-#pragma unroll
-        for (int dst = 0; dst < S::CL; ++dst) {
-            if (dst == static_cast<int>(rank)) {
-#pragma unroll
-                for (int i = 0; i < S::PER_CTA; ++i) recv[slot + i * stride] = r[dst * S::PER_CTA + i];
-            } else {
-                const uint32_t rb = mapa_rank(lrecv, dst), rm = mapa_rank(smem_addr(&mbar), dst);
-#pragma unroll
-                for (int i = 0; i < S::PER_CTA; ++i)
-                    st_async(rb + i * stride * static_cast<uint32_t>(sizeof(W)), r[dst * S::PER_CTA + i], rm);
-            }
-        }
-        constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
-        if (threadIdx.x == 0)
-            mbar_arrive_tx(smem_addr(&mbar), kRemoteBytes);
-        else
-            mbar_arrive(smem_addr(&mbar));
-        mbar_wait(smem_addr(&mbar), 0);
-#pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = recv[k * S::T + threadIdx.x];
+        inv_core_push<LOGN, W>(sm, recv, smem_addr(&mbar), 0, P, rank, c0, c1, true, r);
     } else {
+        // local passes in reverse: the last (possibly short) chunk first
+        constexpr int kTail = (LOGN - kLogE) % kLogE;
+        if constexpr (kTail > 0) {
+            local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int s0 = LOGN - kTail - kLogE; s0 >= kLogE; s0 -= kLogE) {
+            local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
+            __syncthreads();
+        }
+        // cross-CTA pass: stages 3..0 gathered from the owners
         if constexpr (S::CL > 1) cg::this_cluster().sync();
         const uint32_t sb = swb<W>(rho);  // rho < NE
 #pragma unroll
@@ -660,33 +721,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
                 r[k] = sm_at(sm, sb, c);
             }
         }
+        inv_final<W>(r, tw, q, c0, c1);
     }
-    {
-        // stages 3, 2, 1 as usual; stage 0 with n^-1 merged.
-        inv_stages<kLogE, kLogE - 1, 1, W>(r, tw, 0, 0, q, two_q);
-        constexpr int half0 = kE / 2;
-        PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
-        const PairT<W>* last = nullptr;
-        if constexpr (sizeof(W) == 8)
-            last = b.last_stage;
-        else
-            last = b.last_stage32;
-        if (last) {
-            const uint32_t l = limb_id % b.limbs;
-            c0 = last[2 * l];
-            c1 = last[2 * l + 1];
-        }
 #pragma unroll
-        for (int k = 0; k < half0; ++k) {
-            W x = r[k], y = r[k + half0];
-            W s = x + y;  // < 4q
-            W d = x - y + two_q;
-            r[k] = shoup_full<W>(s, c0.x, c0.y, q);
-            r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
-        }
-#pragma unroll
-        for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
-    }
+    for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
     if constexpr (S::CL > 1 && !kPush) {  // keep smem alive for peers' remote loads
         cluster_arrive_relaxed();
         cluster_wait();

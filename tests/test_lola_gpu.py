@@ -70,16 +70,17 @@ def test_lola_mnist_config0_word32():
     _check(lola_mnist_params_w32(), nets.lola_mnist_net(), "lola-mnist", batch=2, config=0)
 
 
-def test_lola_cifar_config4_single_image():
+@pytest.mark.parametrize("word", [64, 32])
+def test_lola_cifar_config4_single_image(word):
     """BASELINE config 4 (83 + 163 maps, 57,252 rotations per instance, 6
     plaintext primes): decrypted logits == forward_integer; per-step counters
     == the plan's predictions (checked inside execute) whose totals equal the
     golden trace proj/tests/golden/lola_cifar.txt:10."""
     from paper_1812_10659_b200.lola import plan_counters
-    from paper_1812_10659_b200.params import lola_cifar_params
+    from paper_1812_10659_b200.params import lola_cifar_params, lola_cifar_params_w32
 
     net = nets.lola_cifar_net()
-    prm = lola_cifar_params()
+    prm = lola_cifar_params() if word == 64 else lola_cifar_params_w32()
     cx = BfvContext(prm)
     sess = Session(cx, net, "lola-cifar", 1)
     img = nets.images(4, net, 1)

@@ -17,6 +17,7 @@ SETS = {
     "lola_small_params": P.lola_small_params,
     "lola_small_params_w32": P.lola_small_params_w32,
     "lola_cifar_params": P.lola_cifar_params,
+    "lola_cifar_params_w32": P.lola_cifar_params_w32,
 }
 
 
