@@ -416,11 +416,20 @@ def run_ours(a, world, rank, local):
         return w0.elapsed_time(w1)
 
     warm = [untimed_step() for _ in range(a.warmup)]
-    # settle: a fresh box occasionally shows one slow step right after start-up
-    # (device-side, not ours); keep warming (at most 5 more, untimed) until two
-    # consecutive steps agree within 3%
-    for _ in range(5):
-        if len(warm) >= 2 and abs(warm[-1] - warm[-2]) <= 0.03 * min(warm[-2:]):
+    # the end-to-end path allocates differently (input encryption, decryption):
+    # run it once before any timed region so the stream-ordered pool has grown
+    # to the footprint of both paths
+    host_imgs = np.ascontiguousarray(imgs)
+    scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
+    sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)
+    sess.encrypt(dev_imgs, on_device=True)
+    # settle: a fresh box occasionally shows slow steps right after start-up
+    # (pool growth, lazy module loads); keep warming (at most 8 more, untimed)
+    # until three consecutive steps agree within 3%
+    warm.append(untimed_step())
+    for _ in range(8):
+        last = warm[-3:]
+        if len(last) == 3 and max(last) - min(last) <= 0.03 * min(last):
             break
         warm.append(untimed_step())
 
@@ -444,8 +453,6 @@ def run_ours(a, world, rank, local):
     value = world * B * a.steps / elapsed
 
     # ---- e2e: host images -> encrypt -> HE steps -> decrypt -> host scores ----
-    host_imgs = np.ascontiguousarray(imgs)
-    scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
     sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)  # warm
     barrier(world)
     torch.cuda.synchronize()
