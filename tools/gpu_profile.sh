@@ -11,7 +11,7 @@ i=0
 for k in $KS; do
   i=$((i+1))
   timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:$k" -s 2 -c ${NCU_COUNT:-1} -o /tmp/prof_$i $CMD > gpurun_out/ncu_full_$i.log 2>&1; echo "ncu $k rc=$?"
+    -k "regex:$k" -s ${NCU_SKIP:-2} -c ${NCU_COUNT:-1} -o /tmp/prof_$i $CMD > gpurun_out/ncu_full_$i.log 2>&1; echo "ncu $k rc=$?"
   ncu -i /tmp/prof_$i.ncu-rep --page raw --csv > gpurun_out/full_$i.csv
   ncu -i /tmp/prof_$i.ncu-rep --page source --csv > gpurun_out/source_$i.csv 2>/dev/null
 done
