@@ -453,7 +453,15 @@ def run_ours(a, world, rank, local):
     value = world * B * a.steps / elapsed
 
     # ---- e2e: host images -> encrypt -> HE steps -> decrypt -> host scores ----
-    sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)  # warm
+    # warm until two consecutive end-to-end runs agree within 5% (at most 4):
+    # the first runs in a fresh process grow the allocation pool
+    e2e_warm = []
+    for _ in range(4):
+        t0 = time.perf_counter()
+        sess.run_raw(host_imgs, scores, False, False, want_counters=False, want_times=False)
+        e2e_warm.append(time.perf_counter() - t0)
+        if len(e2e_warm) >= 2 and abs(e2e_warm[-1] - e2e_warm[-2]) <= 0.05 * min(e2e_warm[-2:]):
+            break
     barrier(world)
     torch.cuda.synchronize()
     e0.record(s)
