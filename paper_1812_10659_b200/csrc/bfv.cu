@@ -225,6 +225,73 @@ __global__ void k_enc_finish(BfvDev d, uint32_t count, uint64_t id_base, St* __r
     }
 }
 
+// ---- fused encryption (u32 residues) ----
+// Per coefficient of every ciphertext: the limb-independent pieces of c0's
+// coefficients, extra = floor(([Q]_t m + t/2) / t) and the error sample e.
+__global__ void k_enc_prep32(BfvDev d, const uint64_t* __restrict__ mcoef, uint32_t count, uint64_t id_base,
+                             uint32_t* __restrict__ extra, int8_t* __restrict__ err) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (idx >= uint64_t(count) * d.n) return;
+    const uint32_t k = idx % d.n;
+    const uint64_t c = idx / d.n;
+    const uint32_t j = c % d.T;
+    const uint64_t mval = mcoef[idx];
+    const uint64_t t = d.primes[d.tbase + j].q;
+    extra[idx] = static_cast<uint32_t>((d.q_mod_t[j] * mval + (t >> 1)) / t);
+    err[idx] = static_cast<int8_t>(sample_cbd21(prng_at(stream_key(d.seed, stream_enc_e(id_base + c)), k)));
+}
+
+// One cluster per (ciphertext, limb i): c0's coefficients (e + round(Q m/t))
+// mod q_i formed in the forward transform's first-pass loads, the transform,
+// then c1 = a (sampled at each evaluation position) and c0 -= a s in the
+// store: k_enc_coeffs + NTT + k_enc_finish in one pass over the limb.
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
+    k_encrypt32(BfvDev d, const uint64_t* __restrict__ mcoef, const uint32_t* __restrict__ extra,
+                const int8_t* __restrict__ err, uint64_t id_base, uint32_t* __restrict__ ct) {
+    using S = NttShape<LOGN>;
+    using W = uint32_t;
+    __shared__ __align__(16) W sm[S::M];
+    __shared__ uint64_t mbar;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t id = blockIdx.x / S::CL;
+    const uint32_t c = id / d.L, i = id % d.L, j = c % d.T;
+    const uint64_t n = 1ull << LOGN;
+    const PrimeDev& P = d.primes[i];
+    const W q = static_cast<W>(P.q);
+    const uint2 dl = d.delta32[j * d.L + i], one = d.one32[i];
+    const uint64_t* m = mcoef + uint64_t(c) * n;
+    const uint32_t* ex = extra + uint64_t(c) * n;
+    const int8_t* er = err + uint64_t(c) * n;
+    const Xchg xc = xchg_init<S::CL>(&mbar, 1);
+    fwd_core<LOGN>(
+        sm, P, rank,
+        [&](uint32_t rho, uint32_t off) {
+            const uint32_t k = rho + off;
+            const W a = shoup_full<W>(static_cast<W>(__ldg(&m[k])), dl.x, dl.y, q);
+            const W b = shoup_full<W>(__ldg(&ex[k]), 1u, one.y, q);
+            const int e = __ldg(&er[k]);
+            const W ee = e < 0 ? q - static_cast<W>(-e) : static_cast<W>(e);  // |e| <= 21
+            return csub<W>(csub<W>(a + b, q) + ee, q);
+        },
+        true, xc);
+    const uint64_t key_a = stream_key(d.seed, stream_enc_a(id_base + c, i));
+    W* c0 = ct + (uint64_t(c) * 2 * d.L + i) * n;
+    W* c1 = c0 + uint64_t(d.L) * n;
+    const uint32_t sb = swb<W>(threadIdx.x);
+    const uint2* s32 = d.s32 + uint64_t(i) * n;
+#pragma unroll 4
+    for (int jj = 0; jj < kE; ++jj) {
+        const uint32_t pos = rank * S::M + threadIdx.x + jj * S::T;
+        const W v = reduce_4q<W>(sm_at(sm, sb, jj * S::T), q, 2 * q);
+        const W au = static_cast<W>(sample_uniform(q, prng_at(key_a, pos)));
+        const uint2 sp = __ldg(&s32[pos]);
+        const W as = shoup_full<W>(au, sp.x, sp.y, q);
+        c1[pos] = au;
+        c0[pos] = v >= as ? v - as : v + q - as;
+    }
+}
+
 // pt_mul = centered lift of m; pt_add = round(Q m / t); m: [T][n]
 template <class St>
 __global__ void k_pt_lift(BfvDev d, const uint64_t* __restrict__ mcoef, St* __restrict__ pt_mul, St* __restrict__ pt_add) {
@@ -1109,6 +1176,38 @@ void key_switch(Context& cx, const void* d, uint64_t key_id, void* u0, void* u1,
 
 // ---- public ciphertext operations ----------------------------------------------
 
+namespace {
+
+// fused encryption for u32 contexts (A/B switch LB_ENC_FUSED=0)
+bool enc_fused() {
+    static const bool on = [] {
+        const char* e = std::getenv("LB_ENC_FUSED");
+        return e ? e[0] != '0' : true;
+    }();
+    return on;
+}
+
+template <int LOGN>
+void launch_encrypt32(const BfvDev& d, const uint64_t* m, const uint32_t* extra, const int8_t* err, uint32_t count,
+                      uint64_t id_base, void* out, cudaStream_t s) {
+    using S = NttShape<LOGN>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(count) * d.L * S::CL));
+    cfg.blockDim = dim3(S::T);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LB_CUDA(cudaLaunchKernelEx(&cfg, k_encrypt32<LOGN>, d, m, extra, err, id_base, static_cast<uint32_t*>(out)));
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
+}  // namespace
+
 void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, cudaStream_t s) {
     const BfvDev& d = cx.bfv()->dev;
     if (!B) return;
@@ -1122,6 +1221,20 @@ void encrypt_slots(Context& cx, const int64_t* values, uint32_t B, uint64_t id_b
     tb.prime_map = cx.bfv()->t_map;
     tb.map_period = T;
     cx.ntt_inverse(tb, s);
+    if (d.ks32 && enc_fused()) {
+        DeviceBuffer extra(uint64_t(count) * n * 4, s), err(uint64_t(count) * n, s);
+        k_enc_prep32<<<grid_for(uint64_t(count) * n), kBlock, 0, s>>>(d, m.get(), count, id_base, extra.get<uint32_t>(),
+                                                                      err.get<int8_t>());
+        LB_KERNEL_DONE();
+        switch (cx.logn()) {
+            case 12: launch_encrypt32<12>(d, m.get(), extra.get<uint32_t>(), err.get<int8_t>(), count, id_base, out, s); break;
+            case 13: launch_encrypt32<13>(d, m.get(), extra.get<uint32_t>(), err.get<int8_t>(), count, id_base, out, s); break;
+            case 14: launch_encrypt32<14>(d, m.get(), extra.get<uint32_t>(), err.get<int8_t>(), count, id_base, out, s); break;
+            case 15: launch_encrypt32<15>(d, m.get(), extra.get<uint32_t>(), err.get<int8_t>(), count, id_base, out, s); break;
+            default: throw std::invalid_argument("unsupported ring degree");
+        }
+        return;
+    }
     with_residue(cx, [&](auto w) {
         using St = decltype(w);
         St* ct = static_cast<St*>(out);
