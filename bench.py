@@ -394,6 +394,11 @@ def run_ours(a, world, rank, local):
     cfg, strategy, default_batch, net, prm = workload_objects(a.workload, a.word)
     cx = BfvContext(prm)
     B = a.batch or default_batch
+    # grow the allocation pool up front (half of the free device memory):
+    # mid-run pool growth maps and clears fresh memory, a >1 s stall
+    free, _ = torch.cuda.mem_get_info()
+    if os.environ.get("LB_POOL_RESERVE", "1") != "0":
+        nat.call("lb_pool_reserve", cx.handle, int(free * 0.5))
     sess = Session(cx, net, strategy, B)
     # images of this rank: a disjoint contiguous range of the job's image set
     from paper_1812_10659_b200.shard import shard_range

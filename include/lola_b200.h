@@ -80,6 +80,10 @@ int lb_context_prime(const lb_context* cx, uint32_t index, uint64_t* prime, uint
 /* residue word of the context's ciphertexts and plaintext operands: 4
  * (uint32_t; every ciphertext and special prime below 2^30) or 8 bytes */
 int lb_context_residue_bytes(const lb_context* cx, uint32_t* bytes);
+/* pre-grow the device's stream-ordered allocation pool by `bytes` (kept:
+ * the pool's release threshold is unbounded), so a long-running session
+ * never maps fresh device memory mid-run */
+int lb_pool_reserve(lb_context* cx, uint64_t bytes);
 int lb_sync(lb_context* cx, void* stream);
 
 /* ---- NTT engine (replaces NttTables::forward / inverse, ring.cpp:97-115) --

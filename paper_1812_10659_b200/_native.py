@@ -42,6 +42,7 @@ _SIGS: dict[str, list] = {
     "lb_context_destroy": [vp],
     "lb_context_prime": [vp, u32, P64, P64],
     "lb_context_residue_bytes": [vp, C.POINTER(u32)],
+    "lb_pool_reserve": [vp, u64],
     "lb_sync": [vp, vp],
     "lb_ntt_forward": [vp, vp, u32, u32, u32, u64, vp],
     "lb_ntt_inverse": [vp, vp, u32, u32, u32, u64, vp],

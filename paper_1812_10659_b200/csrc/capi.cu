@@ -76,6 +76,21 @@ int lb_context_residue_bytes(const lb_context* cx, uint32_t* bytes) {
     });
 }
 
+int lb_pool_reserve(lb_context* cx, uint64_t bytes) {
+    return guarded([&] {
+        need(cx != nullptr, "null context");
+        cx->cx.activate();
+        // grow the device's stream-ordered pool once (its release threshold
+        // keeps freed memory): later allocations of the working set never map
+        // fresh physical memory inside a timed region
+        cudaStream_t s = cx->cx.stream();
+        void* p = nullptr;
+        LB_CUDA(cudaMallocAsync(&p, bytes, s));
+        LB_CUDA(cudaFreeAsync(p, s));
+        LB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int lb_sync(lb_context* cx, void* stream) {
     return guarded([&] { LB_CUDA(cudaStreamSynchronize(pick(cx, stream))); });
 }

@@ -22,6 +22,9 @@ def main():
     B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     cfg, strategy, _, net, prm = bench.workload_objects("lola-mnist", 32)
     cx = BfvContext(prm)
+    from paper_1812_10659_b200 import _native as nat
+
+    nat.call("lb_pool_reserve", cx.handle, int(torch.cuda.mem_get_info()[0] * 0.5))
     sess = Session(cx, net, strategy, B)
     imgs = np.ascontiguousarray(nets.images(cfg, net, B))
     scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
