@@ -447,8 +447,13 @@ struct ModDownArgs {
     uint32_t count;
 };
 
+#ifndef LB_MODDOWN32_MINB
+#define LB_MODDOWN32_MINB LB_NTT32_MINB
+#endif
+template <class W> constexpr int moddown_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_MODDOWN32_MINB; }
+
 template <int LOGN, class W>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
+__global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
     __shared__ __align__(16) W sm[S::M];
     const uint32_t LK = d.L + d.K;
