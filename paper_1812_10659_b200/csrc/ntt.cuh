@@ -560,9 +560,37 @@ __device__ __forceinline__ void inv_final(W (&r)[kE], const PairT<W>* __restrict
     }
 }
 
+// The inverse's first (tail) pass, stages LOGN-1 .. LOGN-kTail, straight from
+// global memory: its butterfly groups are 2^kTail consecutive coefficients
+// (stride 1), so each group is one vector load (16 bytes for kTail = 2 on
+// u32), and the results go to smem once — no staging store + reload of the
+// input, and the loads overlap the groups' butterflies. load_group(y, r)
+// fills r[0 .. 2^kTail) with chunk elements y .. y + 2^kTail - 1.
+template <int LOGN, class W, class LoadGroup>
+__device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeDev& P, uint32_t cta_base, LoadGroup&& load_group) {
+    constexpr int kTail = (LOGN - kLogE) % kLogE;
+    constexpr int G = kE >> kTail;  // groups per thread
+    using S = NttShape<LOGN>;
+    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = inv_table<W>(P);
+    constexpr uint32_t s0 = LOGN - kTail;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const uint32_t g = threadIdx.x + i * S::T;
+        const uint32_t base = g << kTail;
+        W r[1 << kTail];
+        load_group(base, r);
+        inv_group<kTail>(r, tw, s0, (cta_base >> kTail) + g, q, two_q);
+        const uint32_t sb = swb<W>(base);
+#pragma unroll
+        for (int k = 0; k < (1 << kTail); ++k) sm_at(sm, sb, k) = r[k];
+    }
+}
+
 // Push-based inverse transform core (cluster limbs, LB_NTT_MBAR). On entry
-// `sm` holds this CTA's chunk of the evaluations (swizzled, values < 2q,
-// visible to every thread: the caller synchronised); `recv` is a fresh
+// `sm` holds this CTA's chunk after the tail pass (inv_tail_pass: stages
+// LOGN-1 .. LOGN-kTail, swizzled, values < 2q, visible to every thread: the
+// caller synchronised); `recv` is a fresh
 // receive plane of M words and `mbar` this CTA's mbarrier for it (count =
 // threads, phase `parity`). Peers must have initialised their mbarriers
 // (start_wait: wait here on the cluster barrier the caller arrived on).
@@ -578,10 +606,7 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     const PairT<W>* __restrict__ tw = inv_table<W>(P);
     const uint32_t cta_base = rank * S::M;
     constexpr int kTail = (LOGN - kLogE) % kLogE;
-    if constexpr (kTail > 0) {
-        local_pass<LOGN, kTail, true, W>(sm, tw, LOGN - kTail, cta_base, q, two_q);
-        __syncthreads();
-    }
+    static_assert(kTail > 0, "cluster limbs have a tail pass");
 #pragma unroll
     for (int s0 = LOGN - kTail - kLogE; s0 >= 2 * kLogE; s0 -= kLogE) {
         local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
@@ -658,7 +683,36 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     const uint32_t cta_base = rank * S::M;
 
     const uint32_t sbt = swb<W>(threadIdx.x);
-    if (b.src) {
+    if constexpr (kPush) {
+        // tail pass straight from global memory (through the automorphism
+        // when reading a key switch's input)
+        constexpr int kTail = (LOGN - kLogE) % kLogE;
+        if (b.src) {
+            const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
+            const St* in = reinterpret_cast<const St*>(b.src) + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
+            inv_tail_pass<LOGN, W>(sm, P, cta_base, [&](uint32_t y, W (&r)[1 << kTail]) {
+#pragma unroll
+                for (int k = 0; k < (1 << kTail); ++k) {
+                    const uint32_t x = cta_base + y + k;
+                    r[k] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
+                }
+            });
+        } else {
+            const St* in = a + cta_base;
+            inv_tail_pass<LOGN, W>(sm, P, cta_base, [&](uint32_t y, W (&r)[1 << kTail]) {
+                if constexpr (sizeof(St) == 4 && kTail == 2) {
+                    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in + y));
+                    r[0] = v.x;
+                    r[1] = v.y;
+                    r[2] = v.z;
+                    r[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < (1 << kTail); ++k) r[k] = static_cast<W>(__ldcs(&in[y + k]));
+                }
+            });
+        }
+    } else if (b.src) {
         const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
         // src holds words of the batch's storage type (the key switch reads its
         // input ciphertext, stored in the context's residue word)
