@@ -51,14 +51,15 @@ template <> struct KsTables<uint32_t> {
 // raw residue (< 4r: every prime of Q and P is within a factor 4 of every
 // other). A is a compile-time constant so all A loads of an element are
 // independent (a runtime loop serializes them).
-template <int A, int LOGN, class W, class St>
+template <int A, int LOGN, class W, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
-                                           const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc) {
+                                           const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc,
+                                           Last&& last = nullptr) {
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
-                       start_sync, xc);
+                       start_sync, xc, last);
     } else {
         PairT<W> ww[A];
 #pragma unroll
@@ -75,24 +76,24 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
                 acc += shoup_lazy<W>(v[i], ww[i].x, ww[i].y, q);
             }
             return acc;
-        }, start_sync, xc);
+        }, start_sync, xc, last);
     }
 }
 
-template <int LOGN, class W, class St>
+template <int LOGN, class W, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
-                                         Xchg xc = Xchg{}) {
+                                         Xchg xc = Xchg{}, Last&& last = nullptr) {
     switch (A) {
-        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break;
-        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break;
+        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break;
+        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; } }
         [[fallthrough]];
-        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc); break; } }
+        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; } }
         [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -105,7 +106,7 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
                     v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&src[i * n + x])), wi.x, wi.y, q), two_q);
                 }
                 return v;
-            }, start_sync, xc);
+            }, start_sync, xc, last);
         }
     }
 }
@@ -447,6 +448,9 @@ struct ModDownArgs {
     uint32_t count;
 };
 
+#ifndef LB_MODDOWN_DIRECT
+#define LB_MODDOWN_DIRECT 1
+#endif
 #ifndef LB_MODDOWN32_MINB
 #define LB_MODDOWN32_MINB LB_NTT32_MINB
 #endif
@@ -469,7 +473,6 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     // into the inverse transform) and the loader forms sum_l y_l [P/p_l]_{q_r}
     __shared__ uint64_t mbar;
     const Xchg xc = xchg_init<S::CL>(&mbar, 1);
-    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
     const uint32_t cta_base = rank * S::M;
     const W* accq = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + r) * n;
     const W* add = static_cast<const W*>(h ? a.add1 : a.add0);
@@ -478,6 +481,47 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     W* out = static_cast<W*>(h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
+#if LB_MODDOWN_DIRECT
+    // epilogue on the transform's last-pass groups (consecutive evaluations,
+    // in registers): 16-byte loads of the Q accumulator and the second
+    // addend and 16-byte stores of the result for radix-4 groups of u32
+    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc,
+                      [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) {
+        constexpr int C = 1 << fwd_last_radix<LOGN>();
+        const uint32_t x0 = cta_base + base;
+        W va[C], vb[C], vs[C];
+        if constexpr (sizeof(W) == 4 && C == 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(accq + x0));
+            va[0] = v.x; va[1] = v.y; va[2] = v.z; va[3] = v.w;
+            const uint4 t = sum ? __ldg(reinterpret_cast<const uint4*>(sum + x0)) : make_uint4(0, 0, 0, 0);
+            vs[0] = t.x; vs[1] = t.y; vs[2] = t.z; vs[3] = t.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                va[k] = __ldg(&accq[x0 + k]);
+                vs[k] = sum ? __ldg(&sum[x0 + k]) : 0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            vb[k] = add ? __ldg(&add[a.add_galois ? galois_src(x0 + k, a.add_galois, LOGN) : x0 + k]) : 0;
+        W u[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const W conv = reduce_4q<W>(rr[k], q, two_q);
+            W v = shoup_full<W>(va[k] + q - conv, pinv.x, pinv.y, q);
+            v = csub<W>(v + vb[k], q);
+            u[k] = csub<W>(v + vs[k], q);
+        }
+        if constexpr (sizeof(W) == 4 && C == 4) {
+            *reinterpret_cast<uint4*>(out + x0) = make_uint4(u[0], u[1], u[2], u[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k) out[x0 + k] = u[k];
+        }
+    });
+#else
+    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
     const uint32_t sbt = swb<W>(threadIdx.x);
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
@@ -505,6 +549,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
             out[cta_base + y] = u;
         }
     }
+#endif
 }
 
 }  // namespace lb

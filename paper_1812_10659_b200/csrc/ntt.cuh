@@ -26,6 +26,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "modarith.cuh"
 
@@ -431,9 +432,36 @@ __device__ __forceinline__ Xchg xchg_init(uint64_t* mbar, int count) {
 // start_sync = false skips the barrier that protects `sm` from being
 // overwritten while still being read: for callers whose transforms each write
 // a fresh smem plane after a first synchronised one.
-template <int LOGN, class W, class Load>
+// The forward transform's last local pass: stages LOGN-kLast .. LOGN-1 over
+// groups of 2^kLast consecutive evaluations (stride 1), handed to
+// last(base, r) in registers (chunk-local base, r[k] < 4q at base + k)
+// instead of going back to smem: epilogues that stream the result out skip a
+// store, a barrier and a reload.
+template <int LOGN>
+constexpr int fwd_last_radix() { return (LOGN % kLogE) == 0 ? kLogE : LOGN % kLogE; }
+
+template <int LOGN, class W, class Last>
+__device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t cta_base, W q,
+                                              W two_q, Last&& last) {
+    constexpr int C = fwd_last_radix<LOGN>();
+    constexpr int G = kE >> C;
+    constexpr uint32_t s0 = LOGN - C;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const uint32_t g = threadIdx.x + i * kThreads;
+        const uint32_t base = g << C;
+        const uint32_t sb = swb<W>(base);
+        W r[1 << C];
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
+        fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
+        last(base, r);
+    }
+}
+
+template <int LOGN, class W, class Load, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load,
-                                         bool start_sync = true, Xchg xc = Xchg{}) {
+                                         bool start_sync = true, Xchg xc = Xchg{}, Last&& last = nullptr) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
     const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -499,11 +527,14 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank
         __syncthreads();
     }
     const uint32_t cta_base = rank * S::M;
+    constexpr bool kDirect = !std::is_same_v<std::decay_t<Last>, std::nullptr_t>;
+    constexpr int kEnd = kDirect ? LOGN - fwd_last_radix<LOGN>() : LOGN;
 #pragma unroll
-    for (int s0 = kLogE; s0 < LOGN; s0 += kLogE) {
+    for (int s0 = kLogE; s0 < kEnd; s0 += kLogE) {
         local_pass_n<LOGN, false>(LOGN - s0 < kLogE ? LOGN - s0 : kLogE, sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
+    if constexpr (kDirect) fwd_last_pass<LOGN, W>(sm, tw, cta_base, q, two_q, last);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -529,17 +560,23 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
     __shared__ uint64_t mbar;
     const Xchg xc = xchg_init<S::CL>(&mbar, 1);
-    fwd_core<LOGN>(
-        sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); }, true, xc);
-    // Coalesced store of the CTA's chunk, fully reduced.
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     St* out = a + rank * S::M;
-    const uint32_t sb = swb<W>(threadIdx.x);
+    // the last pass's groups (consecutive evaluations) stored straight from
+    // registers, fully reduced (16-byte stores for radix-4 groups of u32)
+    fwd_core<LOGN>(
+        sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); }, true, xc,
+        [&](uint32_t base, W(&r)[1 << fwd_last_radix<LOGN>()]) {
+            constexpr int C = fwd_last_radix<LOGN>();
+            if constexpr (sizeof(St) == 4 && C == 2) {
+                __stcs(reinterpret_cast<uint4*>(out + base),
+                       make_uint4(reduce_4q<W>(r[0], q, two_q), reduce_4q<W>(r[1], q, two_q),
+                                  reduce_4q<W>(r[2], q, two_q), reduce_4q<W>(r[3], q, two_q)));
+            } else {
 #pragma unroll
-    for (int j = 0; j < kE; ++j) {
-        const uint32_t y = threadIdx.x + j * S::T;
-        __stcs(&out[y], static_cast<St>(reduce_4q<W>(sm_at(sm, sb, j * S::T), q, two_q)));
-    }
+                for (int k = 0; k < (1 << C); ++k) __stcs(&out[base + k], static_cast<St>(reduce_4q<W>(r[k], q, two_q)));
+            }
+        });
 }
 
 // Cross-CTA pass tail: stages 3, 2, 1 as usual; stage 0 with the scaled
