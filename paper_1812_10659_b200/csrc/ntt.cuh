@@ -572,6 +572,13 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
                 __stcs(reinterpret_cast<uint4*>(out + base),
                        make_uint4(reduce_4q<W>(r[0], q, two_q), reduce_4q<W>(r[1], q, two_q),
                                   reduce_4q<W>(r[2], q, two_q), reduce_4q<W>(r[3], q, two_q)));
+            } else if constexpr (sizeof(St) == 8 && C >= 1) {
+                // pairs of u64 as 16-byte stores (scalar 8-byte stores at a
+                // 2^C-element lane stride would split every warp store)
+#pragma unroll
+                for (int k = 0; k < (1 << C); k += 2)
+                    __stcs(reinterpret_cast<ulonglong2*>(out + base + k),
+                           make_ulonglong2(reduce_4q<W>(r[k], q, two_q), reduce_4q<W>(r[k + 1], q, two_q)));
             } else {
 #pragma unroll
                 for (int k = 0; k < (1 << C); ++k) __stcs(&out[base + k], static_cast<St>(reduce_4q<W>(r[k], q, two_q)));
