@@ -495,6 +495,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
             va[0] = v.x; va[1] = v.y; va[2] = v.z; va[3] = v.w;
             const uint4 t = sum ? __ldg(reinterpret_cast<const uint4*>(sum + x0)) : make_uint4(0, 0, 0, 0);
             vs[0] = t.x; vs[1] = t.y; vs[2] = t.z; vs[3] = t.w;
+        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {  // u64 pairs as 16-byte loads
+#pragma unroll
+            for (int k = 0; k < C; k += 2) {
+                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(accq + x0 + k));
+                va[k] = v.x;
+                va[k + 1] = v.y;
+                const ulonglong2 t = sum ? __ldg(reinterpret_cast<const ulonglong2*>(sum + x0 + k)) : make_ulonglong2(0, 0);
+                vs[k] = t.x;
+                vs[k + 1] = t.y;
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < C; ++k) {
@@ -515,6 +525,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
         }
         if constexpr (sizeof(W) == 4 && C == 4) {
             *reinterpret_cast<uint4*>(out + x0) = make_uint4(u[0], u[1], u[2], u[3]);
+        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {
+#pragma unroll
+            for (int k = 0; k < C; k += 2) *reinterpret_cast<ulonglong2*>(out + x0 + k) = make_ulonglong2(u[k], u[k + 1]);
         } else {
 #pragma unroll
             for (int k = 0; k < C; ++k) out[x0 + k] = u[k];
