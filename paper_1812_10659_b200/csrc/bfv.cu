@@ -264,6 +264,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
     const uint32_t* ex = extra + uint64_t(c) * n;
     const int8_t* er = err + uint64_t(c) * n;
     const Xchg xc = xchg_init<S::CL>(&mbar, 1);
+    const uint64_t key_a = stream_key(d.seed, stream_enc_a(id_base + c, i));
+    W* c0 = ct + (uint64_t(c) * 2 * d.L + i) * n;
+    W* c1 = c0 + uint64_t(d.L) * n;
+    const uint2* s32 = d.s32 + uint64_t(i) * n;
+    constexpr int C = 1 << fwd_last_radix<LOGN>();
     fwd_core<LOGN>(
         sm, P, rank,
         [&](uint32_t rho, uint32_t off) {
@@ -274,22 +279,31 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
             const W ee = e < 0 ? q - static_cast<W>(-e) : static_cast<W>(e);  // |e| <= 21
             return csub<W>(csub<W>(a + b, q) + ee, q);
         },
-        true, xc);
-    const uint64_t key_a = stream_key(d.seed, stream_enc_a(id_base + c, i));
-    W* c0 = ct + (uint64_t(c) * 2 * d.L + i) * n;
-    W* c1 = c0 + uint64_t(d.L) * n;
-    const uint32_t sb = swb<W>(threadIdx.x);
-    const uint2* s32 = d.s32 + uint64_t(i) * n;
-#pragma unroll 4
-    for (int jj = 0; jj < kE; ++jj) {
-        const uint32_t pos = rank * S::M + threadIdx.x + jj * S::T;
-        const W v = reduce_4q<W>(sm_at(sm, sb, jj * S::T), q, 2 * q);
-        const W au = static_cast<W>(sample_uniform(q, prng_at(key_a, pos)));
-        const uint2 sp = __ldg(&s32[pos]);
-        const W as = shoup_full<W>(au, sp.x, sp.y, q);
-        c1[pos] = au;
-        c0[pos] = v >= as ? v - as : v + q - as;
-    }
+        true, xc,
+        // the last pass's groups of consecutive evaluations, in registers
+        [&](uint32_t base, W(&rr)[C]) {
+            const uint32_t p0 = rank * S::M + base;
+            W u0[C], u1[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const W v = reduce_4q<W>(rr[k], q, 2 * q);
+                const W au = static_cast<W>(sample_uniform(q, prng_at(key_a, p0 + k)));
+                const uint2 sp = __ldg(&s32[p0 + k]);
+                const W as = shoup_full<W>(au, sp.x, sp.y, q);
+                u1[k] = au;
+                u0[k] = v >= as ? v - as : v + q - as;
+            }
+            if constexpr (C == 4) {
+                *reinterpret_cast<uint4*>(c1 + p0) = make_uint4(u1[0], u1[1], u1[2], u1[3]);
+                *reinterpret_cast<uint4*>(c0 + p0) = make_uint4(u0[0], u0[1], u0[2], u0[3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    c1[p0 + k] = u1[k];
+                    c0[p0 + k] = u0[k];
+                }
+            }
+        });
 }
 
 // pt_mul = centered lift of m; pt_add = round(Q m / t); m: [T][n]
