@@ -498,11 +498,22 @@ __global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, 
 // SMALL: every F and G prime below 2^30, so y_i [F/f_i]_g < 2^60 and up to
 // 16 of them sum exactly in 64 bits (one reduction per output instead of a
 // 128-bit accumulator); y stays in registers (unrolled over the 16-prime cap).
+// v < 2^64 with v >> 32 < 2^32 -> v mod r for r < 2^30: hi * [2^32]_r and lo
+// by Shoup (each [0, 2r)), two conditional subtractions.
+__device__ __forceinline__ uint32_t reduce64_32(uint64_t v, uint32_t r, uint4 red) {
+    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+    const uint32_t t = shoup_lazy<uint32_t>(hi, red.x, red.y, r) + shoup_lazy<uint32_t>(lo, 1u, red.z, r);
+    return csub<uint32_t>(csub<uint32_t>(t, 2 * r), r);
+}
+
+// SMALL (every F and G prime below 2^30): Shoup products in 32-bit words
+// (hat_inv32, prod32) and one 64 -> 32-bit reduction per output.
 template <bool SMALL, class Src, class Dst>
 __global__ void k_exact_extend(BfvDev d, const Src* __restrict__ src, uint32_t polys, uint32_t F, uint32_t fbase,
                                const uint64_t* __restrict__ hat_inv, const ulonglong2* __restrict__ frac,
                                const uint64_t* __restrict__ hat_mod /*[F][G]*/, const uint64_t* __restrict__ prod_mod /*[G]*/,
-                               uint32_t G, uint32_t gbase, Dst* __restrict__ dst) {
+                               uint32_t G, uint32_t gbase, Dst* __restrict__ dst, const uint2* __restrict__ hat_inv32,
+                               const uint2* __restrict__ prod32) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(polys) * d.n) return;
     const uint32_t k = idx % d.n;
@@ -513,8 +524,14 @@ __global__ void k_exact_extend(BfvDev d, const Src* __restrict__ src, uint32_t p
 #pragma unroll
     for (int i = 0; i < kMax; ++i) {
         if (i >= F) break;
-        const Modulus fm = modulus_of(d.primes[fbase + i]);
-        y[i] = mul_mod(src[(p * F + i) * d.n + k], hat_inv[i], fm);
+        if constexpr (SMALL) {
+            const uint32_t f = static_cast<uint32_t>(d.primes[fbase + i].q);
+            const uint2 hi = hat_inv32[i];
+            y[i] = shoup_full<uint32_t>(static_cast<uint32_t>(src[(p * F + i) * d.n + k]), hi.x, hi.y, f);
+        } else {
+            const Modulus fm = modulus_of(d.primes[fbase + i]);
+            y[i] = mul_mod(src[(p * F + i) * d.n + k], hat_inv[i], fm);
+        }
         uint64_t ip, fp;
         fixmul(y[i], frac[i], ip, fp);  // ip == 0: y_i / f_i < 1
         S_lo += fp;
@@ -522,17 +539,25 @@ __global__ void k_exact_extend(BfvDev d, const Src* __restrict__ src, uint32_t p
     }
     const uint64_t v = S_hi + (S_lo >> 63);  // round(sum y_i / f_i)
     for (uint32_t m = 0; m < G; ++m) {
-        const Modulus gm = modulus_of(d.primes[gbase + m]);
-        uint64_t s;
         if constexpr (SMALL) {
+            // y_i, [F/f_i]_g < 2^30: one IMAD.WIDE.U32 per term, the F <= 16
+            // products sum below 2^64
+            const uint32_t g = static_cast<uint32_t>(d.primes[gbase + m].q);
             uint64_t acc = 0;
 #pragma unroll
             for (int i = 0; i < kMax; ++i) {
                 if (i >= F) break;
-                acc += y[i] * hat_mod[i * G + m];
+                acc += static_cast<uint64_t>(static_cast<uint32_t>(y[i])) * static_cast<uint32_t>(hat_mod[i * G + m]);
             }
-            s = reduce_u64(acc, gm);
-        } else {
+            const uint32_t s = reduce64_32(acc, g, d.red32[gbase + m]);
+            const uint2 pm = prod32[m];
+            const uint32_t vm = shoup_full<uint32_t>(static_cast<uint32_t>(v), pm.x, pm.y, g);  // v <= F < g
+            dst[(p * G + m) * d.n + k] = static_cast<Dst>(s >= vm ? s - vm : s + g - vm);
+            continue;
+        }
+        const Modulus gm = modulus_of(d.primes[gbase + m]);
+        uint64_t s;
+        {
             Acc128 acc;
 #pragma unroll
             for (int i = 0; i < kMax; ++i) {
@@ -710,6 +735,30 @@ void bfv_setup(Context& cx) {
     const size_t o_bfrac = put(b_frac.data(), b_frac.size() * 16);
     const size_t o_bhmq = put(bhat_mod_q.data(), bhat_mod_q.size() * 8);
     const size_t o_bmq = put(b_mod_q.data(), b_mod_q.size() * 8);
+    d.qb32 = Context::word32_enabled() && cx.primes_small(0, L) && cx.primes_small(L + K, M);
+    size_t o_qhi32 = 0, o_bhi32 = 0, o_qmb32 = 0, o_bmq32 = 0, o_red32 = 0;
+    if (d.qb32) {
+        auto pairs = [](const std::vector<uint64_t>& v, const std::vector<uint64_t>& mods, size_t count) {
+            std::vector<uint2> o(std::max<size_t>(1, count));
+            for (size_t k = 0; k < count; ++k)
+                o[k] = make_uint2(static_cast<uint32_t>(v[k]), shoup_companion32(v[k], mods[k]));
+            return o;
+        };
+        const auto qhi32 = pairs(qhat_inv, q, L), bhi32 = pairs(bhat_inv, b, M);
+        const auto qmb32 = pairs(q_mod_b, b, M), bmq32 = pairs(b_mod_q, q, L);
+        o_qhi32 = put(qhi32.data(), qhi32.size() * 8);
+        o_bhi32 = put(bhi32.data(), bhi32.size() * 8);
+        o_qmb32 = put(qmb32.data(), qmb32.size() * 8);
+        o_bmq32 = put(bmq32.data(), bmq32.size() * 8);
+        std::vector<uint4> red(size_t(L) + K + M);
+        for (uint32_t r = 0; r < L + K + M; ++r) {
+            const uint64_t pr = cx.prime(r);
+            if (pr >= (uint64_t{1} << 30)) continue;
+            const uint64_t w = (uint64_t{1} << 32) % pr;
+            red[r] = make_uint4(static_cast<uint32_t>(w), shoup_companion32(w, pr), shoup_companion32(1, pr), 0u);
+        }
+        o_red32 = put(red.data(), red.size() * 16);
+    }
 
     std::vector<ulonglong2> theta(T * L);
     std::vector<uint64_t> w_mod_b(std::max<size_t>(1, size_t(T) * L * M)), tqinv_b(std::max<size_t>(1, size_t(T) * M));
@@ -844,6 +893,13 @@ void bfv_setup(Context& cx) {
     d.b_frac = reinterpret_cast<const ulonglong2*>(base + o_bfrac);
     d.bhat_mod_q = reinterpret_cast<const uint64_t*>(base + o_bhmq);
     d.b_mod_q = reinterpret_cast<const uint64_t*>(base + o_bmq);
+    if (d.qb32) {
+        d.qhat_inv32 = reinterpret_cast<const uint2*>(base + o_qhi32);
+        d.bhat_inv32 = reinterpret_cast<const uint2*>(base + o_bhi32);
+        d.q_mod_b32 = reinterpret_cast<const uint2*>(base + o_qmb32);
+        d.b_mod_q32 = reinterpret_cast<const uint2*>(base + o_bmq32);
+        d.red32 = reinterpret_cast<const uint4*>(base + o_red32);
+    }
     d.theta = reinterpret_cast<const ulonglong2*>(base + o_theta);
     d.w_mod_b = reinterpret_cast<const uint64_t*>(base + o_wmb);
     d.tqinv_b = reinterpret_cast<const uint64_t*>(base + o_tqb);
@@ -1455,10 +1511,11 @@ void ct_mul(Context& cx, const void* a_in, const void* b_in, void* out_v, uint32
         cx.ntt_inverse(res_batch(x, count * 4, L, 0, LN), s);
         // (b) exact Q -> B, (c) to evaluations
         DeviceBuffer Y(uint64_t(count) * 4 * M * n * 8, s);
-        const bool small = cx.bfv()->qb_small;
+        const bool small = cx.bfv()->qb_small && d.qb32;
         (small ? k_exact_extend<true, St, uint64_t> : k_exact_extend<false, St, uint64_t>)<<<
             grid_for(uint64_t(count) * 4 * n), kBlock, 0, s>>>(d, x, count * 4, L, 0, d.qhat_inv, d.q_frac,
-                                                              d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get());
+                                                              d.qhat_mod_b, d.q_mod_b, M, d.bbase, Y.get(),
+                                                              d.qhat_inv32, d.q_mod_b32);
         LB_KERNEL_DONE();
         cx.ntt_forward(LimbBatch{Y.get(), count * 4, M, d.bbase, uint64_t(M) * n}, s);
         // (d) tensor over Q ∪ B
@@ -1479,7 +1536,8 @@ void ct_mul(Context& cx, const void* a_in, const void* b_in, void* out_v, uint32
         St* e = E.get<St>();
         (small ? k_exact_extend<true, uint64_t, St> : k_exact_extend<false, uint64_t, St>)<<<
             grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, Z.get(), count * 3, M, d.bbase, d.bhat_inv,
-                                                              d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, e);
+                                                              d.b_frac, d.bhat_mod_q, d.b_mod_q, L, 0, e,
+                                                              d.bhat_inv32, d.b_mod_q32);
         LB_KERNEL_DONE();
         cx.ntt_forward(res_batch(e, count * 3, L, 0, LN), s);
         // (i) relinearize e2 and add into (e0, e1)

@@ -75,6 +75,15 @@ struct BfvDev {
     const uint2* delta32;            // [T][L]
     const uint2* one32;              // [L] (1, floor(2^32 / q_i))
     const uint2* s32;                // [L][n]
+    // 32-bit exact base extension (every prime of Q and B below 2^30):
+    // Shoup pairs of [(Q/q_i)^-1]_{q_i}, [(B/b_m)^-1]_{b_m}, [Q]_{b_m},
+    // [B]_{q_i}, and per table prime (2^32 mod r, companion, floor(2^32/r))
+    bool qb32;
+    const uint2* qhat_inv32;         // [L]
+    const uint2* bhat_inv32;         // [M]
+    const uint2* q_mod_b32;          // [M]
+    const uint2* b_mod_q32;          // [L]
+    const uint4* red32;              // [L+K+M] (zero entries for primes >= 2^30)
 };
 
 // Residue word of a context's ciphertexts and plaintext operands in HBM:
