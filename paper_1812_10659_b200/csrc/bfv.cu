@@ -612,6 +612,10 @@ __global__ void k_tensor(BfvDev d, const St* __restrict__ A, const St* __restric
 }
 
 // Z = round(t D / Q) in base B; D: [polys][L+M][n] coeff, Z: [polys][M][n]
+// SMALL (Q and B below 2^30, L + 1 <= 15): the Q-limb values stay in
+// registers, one IMAD.WIDE.U32 per term, one 64 -> 32-bit reduction per
+// output (the rounded R < L 2^30 fits the same 64-bit sum).
+template <bool SMALL>
 __global__ void k_scale(BfvDev d, const uint64_t* __restrict__ D, uint32_t polys, uint32_t polys_per_ct,
                         uint64_t* __restrict__ Z) {
     const uint32_t LM = d.L + d.M;
@@ -629,6 +633,25 @@ __global__ void k_scale(BfvDev d, const uint64_t* __restrict__ D, uint32_t polys
         H += ip + (Lo < fp ? 1 : 0);
     }
     const uint64_t R = H + (Lo >> 63);
+    if constexpr (SMALL) {
+        constexpr int kMax = 14;
+        uint32_t x[kMax];
+#pragma unroll
+        for (int i = 0; i < kMax; ++i) x[i] = i < static_cast<int>(d.L) ? static_cast<uint32_t>(src[uint64_t(i) * d.n]) : 0u;
+        for (uint32_t m = 0; m < d.M; ++m) {
+            const uint64_t* w = d.w_mod_b + uint64_t(j) * d.L * d.M + m;
+            uint64_t acc = R + static_cast<uint64_t>(static_cast<uint32_t>(src[uint64_t(d.L + m) * d.n])) *
+                                   static_cast<uint32_t>(d.tqinv_b[j * d.M + m]);
+#pragma unroll
+            for (int i = 0; i < kMax; ++i) {
+                if (i >= static_cast<int>(d.L)) break;
+                acc += static_cast<uint64_t>(x[i]) * static_cast<uint32_t>(w[uint64_t(i) * d.M]);
+            }
+            Z[(p * d.M + m) * d.n + k] =
+                reduce64_32(acc, static_cast<uint32_t>(d.primes[d.bbase + m].q), d.red32[d.bbase + m]);
+        }
+        return;
+    }
     for (uint32_t m = 0; m < d.M; ++m) {
         const Modulus bm = modulus_of(d.primes[d.bbase + m]);
         Acc128 acc;
@@ -1530,7 +1553,8 @@ void ct_mul(Context& cx, const void* a_in, const void* b_in, void* out_v, uint32
         cx.ntt_inverse(db, s);
         // (f) scale by t/Q into B, (g) exact B -> Q (in residue words), (h) to evaluations
         DeviceBuffer Z(uint64_t(count) * 3 * M * n * 8, s);
-        k_scale<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(d, D.get(), count * 3, 3, Z.get());
+        (small && L + 1 <= 15 ? k_scale<true> : k_scale<false>)<<<grid_for(uint64_t(count) * 3 * n), kBlock, 0, s>>>(
+            d, D.get(), count * 3, 3, Z.get());
         LB_KERNEL_DONE();
         DeviceBuffer E(uint64_t(count) * 3 * LN * W, s);
         St* e = E.get<St>();
