@@ -48,6 +48,15 @@ ulonglong2 frac128(uint64_t num, uint64_t d) {
 
 // ---- device kernels ------------------------------------------------------------
 
+// v < 2^64 with v >> 32 < 2^32 -> v mod r for r < 2^30: hi * [2^32]_r and lo
+// by Shoup (each [0, 2r)), two conditional subtractions.
+__device__ __forceinline__ uint32_t reduce64_32(uint64_t v, uint32_t r, uint4 red) {
+    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+    const uint32_t t = shoup_lazy<uint32_t>(hi, red.x, red.y, r) + shoup_lazy<uint32_t>(lo, 1u, red.z, r);
+    return csub<uint32_t>(csub<uint32_t>(t, 2 * r), r);
+}
+
+
 // secret s (ternary, §3.2) reduced into every prime of Q, P, B
 __global__ void k_secret_coeffs(BfvDev d, uint64_t* out, uint32_t primes) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -471,9 +480,19 @@ template <class St>
 __global__ void __launch_bounds__(kEwThreads) k_mul_plain(BfvDev d, EwShape sh, const St* __restrict__ a,
                                                           const St* __restrict__ pt, St* __restrict__ out) {
     ew_rows(sh, [&](uint64_t off, uint32_t i, uint32_t, uint32_t c, uint32_t k) {
-        const Modulus qm = modulus_of(d.primes[i]);
         const ulonglong2 x = ld2(a + off);
         const ulonglong2 w = ldg2(pt + ((uint64_t(c % sh.T) * sh.L + i) << sh.logn) + k);
+        if constexpr (sizeof(St) == 4) {
+            if (d.qb32) {  // 30-bit residues: 64-bit product, 64 -> 32-bit Shoup reduction
+                const uint32_t q = static_cast<uint32_t>(d.primes[i].q);
+                const uint4 red = d.red32[i];
+                const uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x.x)) * static_cast<uint32_t>(w.x);
+                const uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x.y)) * static_cast<uint32_t>(w.y);
+                st2(out + off, reduce64_32(p0, q, red), reduce64_32(p1, q, red));
+                return;
+            }
+        }
+        const Modulus qm = modulus_of(d.primes[i]);
         st2(out + off, mul_mod(x.x, w.x, qm), mul_mod(x.y, w.y, qm));
     });
 }
@@ -498,13 +517,6 @@ __global__ void __launch_bounds__(kEwThreads) k_add_plain(BfvDev d, EwShape sh, 
 // SMALL: every F and G prime below 2^30, so y_i [F/f_i]_g < 2^60 and up to
 // 16 of them sum exactly in 64 bits (one reduction per output instead of a
 // 128-bit accumulator); y stays in registers (unrolled over the 16-prime cap).
-// v < 2^64 with v >> 32 < 2^32 -> v mod r for r < 2^30: hi * [2^32]_r and lo
-// by Shoup (each [0, 2r)), two conditional subtractions.
-__device__ __forceinline__ uint32_t reduce64_32(uint64_t v, uint32_t r, uint4 red) {
-    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
-    const uint32_t t = shoup_lazy<uint32_t>(hi, red.x, red.y, r) + shoup_lazy<uint32_t>(lo, 1u, red.z, r);
-    return csub<uint32_t>(csub<uint32_t>(t, 2 * r), r);
-}
 
 // SMALL (every F and G prime below 2^30): Shoup products in 32-bit words
 // (hat_inv32, prod32) and one 64 -> 32-bit reduction per output.
@@ -600,9 +612,20 @@ __global__ void k_tensor(BfvDev d, const St* __restrict__ A, const St* __restric
         b0 = Y[o + 2 * st];
         b1 = Y[o + 3 * st];
     }
-    const Modulus pm = modulus_of(d.primes[pidx]);
     const uint64_t st = uint64_t(LM) * d.n;
     const uint64_t o = (c * 3 * LM + r) * d.n + pos;
+    if (d.qb32) {  // every value < 2^30: 64-bit products, 64 -> 32-bit Shoup reductions
+        const uint32_t p = static_cast<uint32_t>(d.primes[pidx].q);
+        const uint4 red = d.red32[pidx];
+        auto mul = [](uint64_t x, uint64_t y) {
+            return static_cast<uint64_t>(static_cast<uint32_t>(x)) * static_cast<uint32_t>(y);
+        };
+        D[o] = reduce64_32(mul(a0, b0), p, red);
+        D[o + st] = reduce64_32(mul(a0, b1) + mul(a1, b0), p, red);
+        D[o + 2 * st] = reduce64_32(mul(a1, b1), p, red);
+        return;
+    }
+    const Modulus pm = modulus_of(d.primes[pidx]);
     D[o] = mul_mod(a0, b0, pm);
     Acc128 s;
     s.mac(a0, b1);
