@@ -77,3 +77,15 @@ def test_aliasing_outputs(cx):
     rot = np.concatenate([np.roll(vals[:half], 3), np.roll(vals[half:], 3)])
     for j, t in enumerate(cx.params.t):
         assert np.array_equal(m[0, j], np.mod(vals + rot, t))
+
+
+def test_pool_reserve_then_ops(cx):
+    """lb_pool_reserve grows the allocation pool up front; later ops reuse it."""
+    free0, _ = torch.cuda.mem_get_info()
+    nat.call("lb_pool_reserve", cx.handle, 1 << 28)
+    ct = cx.encrypt_slots(torch.ones((1, cx.n), dtype=torch.int64, device="cuda"))
+    out = cx.add(ct, ct)
+    m = cx.decrypt_slots(out).cpu().numpy()
+    assert (m[0] == 2).all()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 <= free0  # the reserved memory stays with the pool
