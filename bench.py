@@ -357,6 +357,17 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     achieved = count * products / (ms * 1e-3) / 1e9
     achieved_bfly = count * bfly / (ms * 1e-3) / 1e9
     del ct, out
+    # HBM view: the compulsory bytes of one key switch are the input
+    # ciphertext read, the output written, and the Galois key (2*dnum*(L+K)
+    # limbs) read once per launch set (it is shared by all `count` rotations).
+    wb = word // 8
+    alg_bytes = count * 4 * L * n * wb + 2 * dnum * (L + K) * n * wb
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
     per_ct, src = None, None
     if word == 32:
         try:
@@ -379,6 +390,10 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
                        f"{mac} MAC + {moddown} ModDown products",
         "butterflies_only": {"achieved": achieved_bfly, "frac": achieved_bfly / peak_g},
         "launch_set_ms": ms, "rotations_per_s": count / (ms * 1e-3),
+        "hbm_view": {"achieved_gbs": alg_bytes / (ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                     "frac": alg_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "traffic_over_algorithmic": (per_ct * count / alg_bytes) if per_ct else None},
     }
 
 
