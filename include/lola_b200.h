@@ -204,17 +204,30 @@ typedef struct {
 
 typedef struct lb_lola_session lb_lola_session;
 
-/* build_plan (proj/src/plan.cpp:691-704) without a device: the predicted
+/* PlanOptions (proj/include/packnn/plan.hpp:35-41). The degree is the
+ * context's n (lb_plan_counters takes it explicitly), so the one free
+ * option is the interior window-stage matrix threshold (default 100000,
+ * plan.cpp:375-380). NULL options = the reference defaults. */
+typedef struct {
+    uint64_t window_matrix_threshold;
+} lb_plan_options;
+
+/* build_plan (proj/src/plan.cpp:582-595) without a device: the predicted
  * per-step counters [steps][7] = (ct.ct, ct.pt, scalar, mask, add, rot.col,
  * rot.row). Strategies: lola-mnist, lola-dense-mnist, lola-cifar,
  * lola-small, linear-features. */
 int lb_plan_counters(const lb_network* net, const char* strategy, uint32_t n, uint64_t* counters,
                      uint32_t max_steps, uint32_t* steps_out, uint32_t* depth_needed, uint64_t* predicted_peak);
+int lb_plan_counters_ex(const lb_network* net, const char* strategy, uint32_t n, const lb_plan_options* opt,
+                        uint64_t* counters, uint32_t max_steps, uint32_t* steps_out, uint32_t* depth_needed,
+                        uint64_t* predicted_peak);
 
 /* A plan bound to a device context and a batch of `batch` images; plaintext
  * weights are encoded on the device once and reused across runs. */
 int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
                            uint32_t max_depth, void* stream, lb_lola_session** out);
+int lb_lola_session_create_ex(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
+                              uint32_t max_depth, const lb_plan_options* opt, void* stream, lb_lola_session** out);
 int lb_lola_session_destroy(lb_lola_session* s);
 int lb_lola_session_info(const lb_lola_session* s, uint32_t* steps, uint64_t* outputs, uint64_t* input_values);
 /* plan.encode_input -> execute -> decode (proj/src/plan.cpp:597-633,

@@ -280,7 +280,7 @@ QuantizedNetwork make_network(const pref_net* net) {
 bool strategy_is_small(const char* name) { return std::strcmp(name, "lola-small") == 0; }
 
 // LoLa-Small (BASELINE config 3) has no reference preset (the three-stage
-// check at proj/src/plan.cpp:247-254 rejects it). This chains the reference's
+// check at proj/src/plan.cpp:138-145 rejects it). This chains the reference's
 // own kernels in the order the paper describes: convolution representation,
 // weighted window sums, combine the maps into one message, bias, square,
 // one row-major product per output, bias.
@@ -418,7 +418,7 @@ int pref_run_plan(const pref_net* net, const char* strategy, uint32_t n, const u
             EncodedTensor input = plan.encode_input(ev, xv);
             auto t1 = std::chrono::steady_clock::now();
             // execute() decodes internally; time the HE steps by running the
-            // same step closures, then decode, as proj/src/plan.cpp:718-740.
+            // same step closures, then decode, as proj/src/plan.cpp:609-631.
             ExecutionResult res = execute(plan, input, q, ev);
             auto t2 = std::chrono::steady_clock::now();
             scores = std::move(res.scores);
@@ -436,7 +436,7 @@ int pref_run_plan(const pref_net* net, const char* strategy, uint32_t n, const u
 }
 
 // Per-step HE timing without decode: runs each plan step closure directly
-// (mirrors execute's loop, proj/src/plan.cpp:719-735) and reports seconds per
+// (mirrors execute's loop, proj/src/plan.cpp:610-626) and reports seconds per
 // step in step_times (max_steps entries). Used as the CPU baseline.
 int pref_time_plan_steps(const pref_net* net, const char* strategy, uint32_t n, const uint64_t* primes,
                          uint32_t nprimes, int backend, uint32_t threads, const int64_t* x,

@@ -113,15 +113,28 @@ void phase_decrypt(lb_lola_session* s, uint64_t* scores, int on_device) {
     LB_CUDA(cudaStreamSynchronize(st));
 }
 
+lb::lola::PlanOptions plan_options(const lb_plan_options* opt) {
+    lb::lola::PlanOptions o;
+    if (opt) o.window_matrix_threshold = opt->window_matrix_threshold;
+    return o;
+}
+
 }  // namespace
 
 extern "C" {
 
 int lb_plan_counters(const lb_network* net, const char* strategy, uint32_t n, uint64_t* counters, uint32_t max_steps,
                      uint32_t* steps_out, uint32_t* depth_needed, uint64_t* predicted_peak) {
+    return lb_plan_counters_ex(net, strategy, n, nullptr, counters, max_steps, steps_out, depth_needed,
+                               predicted_peak);
+}
+
+int lb_plan_counters_ex(const lb_network* net, const char* strategy, uint32_t n, const lb_plan_options* opt,
+                        uint64_t* counters, uint32_t max_steps, uint32_t* steps_out, uint32_t* depth_needed,
+                        uint64_t* predicted_peak) {
     return guarded([&] {
         auto nw = to_network(net);
-        auto plan = lb::lola::build_plan(nw, lb::lola::strategy_from_name(strategy), n);
+        auto plan = lb::lola::build_plan(nw, lb::lola::strategy_from_name(strategy), n, plan_options(opt));
         if (plan.steps.size() > max_steps) throw std::invalid_argument("too many steps for buffer");
         for (size_t i = 0; i < plan.steps.size(); ++i) put_counters(plan.steps[i].predicted, counters + 7 * i);
         if (steps_out) *steps_out = static_cast<uint32_t>(plan.steps.size());
@@ -132,13 +145,18 @@ int lb_plan_counters(const lb_network* net, const char* strategy, uint32_t n, ui
 
 int lb_lola_session_create(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
                            uint32_t max_depth, void* stream, lb_lola_session** out) {
+    return lb_lola_session_create_ex(cx, net, strategy, batch, max_depth, nullptr, stream, out);
+}
+
+int lb_lola_session_create_ex(lb_context* cx, const lb_network* net, const char* strategy, uint32_t batch,
+                              uint32_t max_depth, const lb_plan_options* opt, void* stream, lb_lola_session** out) {
     return guarded([&] {
         if (!cx || !out) throw std::invalid_argument("null argument");
         cx->cx.activate();
         auto s = std::make_unique<lb_lola_session>();
         s->net = to_network(net);
         const lb::lola::Strategy strat = lb::lola::strategy_from_name(strategy);
-        s->plan = lb::lola::build_plan(s->net, strat, cx->cx.n());
+        s->plan = lb::lola::build_plan(s->net, strat, cx->cx.n(), plan_options(opt));
         // record tensors (cryptonets-simd) pack the images into the slots of
         // one message: one batch entry carrying `batch` records
         const bool records = strat == lb::lola::Strategy::CryptonetsSimd;

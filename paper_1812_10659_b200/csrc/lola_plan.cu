@@ -462,14 +462,14 @@ CounterDelta mask_active_cost(uint64_t m) {
     return d;
 }
 
-CounterDelta combine_cost(const std::vector<uint32_t>& offsets, bool with_bias) {  // plan.cpp:256-262
+CounterDelta combine_cost(const std::vector<uint32_t>& offsets, bool with_bias) {  // plan.cpp:147-153
     CounterDelta d;
     for (uint32_t o : offsets) d.rot_cols += o != 0;
     d.add = offsets.size() - 1 + (with_bias ? 1 : 0);
     return d;
 }
 
-CounterDelta stack_cost(uint32_t copies, bool fills_message) {  // plan.cpp:264-273
+CounterDelta stack_cost(uint32_t copies, bool fills_message) {  // plan.cpp:155-164
     CounterDelta d;
     const uint32_t steps = ctz64(copies);
     d.add = steps;
@@ -726,7 +726,7 @@ struct Probe {
     std::string rep;
 };
 
-Probe probe_of(const EncodedTensor& t) {  // plan.cpp:213-224
+Probe probe_of(const EncodedTensor& t) {  // plan.cpp:104-115
     Probe p;
     p.count = t.messages.size();
     switch (t.rep.kind) {
@@ -739,7 +739,7 @@ Probe probe_of(const EncodedTensor& t) {  // plan.cpp:213-224
     return p;
 }
 
-std::vector<int64_t> output_bias(const Stage& s) {  // plan.cpp:151-161
+std::vector<int64_t> output_bias(const Stage& s) {  // plan.cpp:42-53
     std::vector<int64_t> b(s.out_shape.values(), 0);
     if (s.bias.empty()) return b;
     if (s.is_conv) {
@@ -755,7 +755,7 @@ Weights window_rows(const Stage& s) {
     return {s.rows, s.cols, [&s](uint64_t m, uint64_t j) { return s.w(m, j); }};
 }
 
-// any stage as a flat matrix over the flattened input (plan.cpp:172-196)
+// any stage as a flat matrix over the flattened input (plan.cpp:63-87)
 Weights matrix_rows(const Stage& s) {
     if (!s.is_conv) return {s.rows, s.cols, [&s](uint64_t r, uint64_t c) { return s.w(r, c); }};
     const ConvGeometry g = s.geom;
@@ -790,7 +790,7 @@ void add_step(Plan& plan, uint64_t in_count, uint64_t in_dim, std::string in_rep
 
 std::string num(uint64_t v) { return std::to_string(v); }
 
-void require_lola_shape(const Network& net) {  // plan.cpp:247-254
+void require_lola_shape(const Network& net) {  // plan.cpp:138-145
     require(net.stages.size() == 3, "strategy expects three linear stages");
     require(net.squares_after.size() == 3, "malformed network");
     require(net.squares_after[0] == 1 && net.squares_after[1] == 1 && net.squares_after[2] == 0,
@@ -799,7 +799,7 @@ void require_lola_shape(const Network& net) {  // plan.cpp:247-254
     require(!net.stages[2].is_conv, "strategy expects a matrix final stage");
 }
 
-// shared tail of the lola-mnist presets (plan.cpp:286-347)
+// shared tail of the lola-mnist presets (plan.cpp:177-238)
 void add_lola_tail(Plan& plan, const Network& net, uint32_t n, uint64_t combined, const std::string& vec_rep,
                    bool hybrid_stack, uint64_t r1, uint64_t r2) {
     const uint64_t pad = pad_for(combined);
@@ -844,7 +844,7 @@ void add_lola_tail(Plan& plan, const Network& net, uint32_t n, uint64_t combined
              });
 }
 
-void build_lola_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:349-395
+void build_lola_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:240-286
     require_lola_shape(net);
     require(!net.stages[1].is_conv, "strategy expects a matrix second stage");
     const Stage& s0 = net.stages[0];
@@ -880,7 +880,7 @@ void build_lola_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp
     plan.live_entering.push_back(r2);
 }
 
-void build_lola_dense_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:397-471
+void build_lola_dense_mnist(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:288-362
     require_lola_shape(net);
     require(!net.stages[1].is_conv, "strategy expects a matrix second stage");
     const Stage& s0 = net.stages[0];
@@ -936,7 +936,7 @@ void build_lola_dense_mnist(Plan& plan, const Network& net, uint32_t n) {  // pl
     plan.live_entering.push_back(r2);
 }
 
-void build_lola_cifar(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:473-571
+void build_lola_cifar(Plan& plan, const Network& net, uint32_t n, const PlanOptions& opt) {  // plan.cpp:364-462
     require_lola_shape(net);
     const Stage& s0 = net.stages[0];
     const Stage& s1 = net.stages[1];
@@ -944,7 +944,7 @@ void build_lola_cifar(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp
     const uint64_t p = g.positions(), v = g.window_volume(), maps = s0.rows, combined = maps * p;
     require(p >= 2, "strategy needs at least two window positions per map");
     if (s1.is_conv)
-        require(uint64_t(s1.geom.window_volume()) * s1.rows > 100000,
+        require(uint64_t(s1.geom.window_volume()) * s1.rows > opt.window_matrix_threshold,
                 "interior window stage below the matrix threshold has no packed route");
     require(s1.is_conv ? s1.in_shape.values() == combined : s1.cols == combined,
             "second stage does not match the window outputs");
@@ -1003,7 +1003,7 @@ void build_lola_cifar(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp
 }
 
 // LoLa-Small (BASELINE config 3; the reference has no preset — the
-// three-stage check at plan.cpp:247-254 rejects two-stage nets): windows in
+// three-stage check at plan.cpp:138-145 rejects two-stage nets): windows in
 // convolution representation, weighted sums, combine the maps into one
 // message, bias, square, one row-major product per output, bias. The chain is
 // the reference's own kernels in that order (oracle/ref_shim.cpp runs the
@@ -1092,7 +1092,7 @@ void build_cryptonets_simd(Plan& plan, const Network& net) {  // plan.cpp:464-50
     plan.live_entering.push_back(net.stages.back().out_shape.values());
 }
 
-void build_linear_features(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:614-646
+void build_linear_features(Plan& plan, const Network& net, uint32_t n) {  // plan.cpp:505-539
     require(net.stages.size() == 1 && !net.stages[0].is_conv, "strategy expects a single matrix stage");
     require(net.squares_after.size() == 1 && net.squares_after[0] == 0, "strategy expects no squarings");
     const uint64_t cols = net.stages[0].cols, rows = net.stages[0].rows;
@@ -1144,7 +1144,7 @@ uint64_t Plan::predicted_peak() const {
     return peak;
 }
 
-Plan build_plan(const Network& net, Strategy s, uint32_t n) {
+Plan build_plan(const Network& net, Strategy s, uint32_t n, const PlanOptions& opt) {
     Plan plan;
     plan.strategy = s;
     plan.n = n;
@@ -1152,7 +1152,7 @@ Plan build_plan(const Network& net, Strategy s, uint32_t n) {
     switch (s) {
         case Strategy::LolaMnist: build_lola_mnist(plan, net, n); break;
         case Strategy::LolaDenseMnist: build_lola_dense_mnist(plan, net, n); break;
-        case Strategy::LolaCifar: build_lola_cifar(plan, net, n); break;
+        case Strategy::LolaCifar: build_lola_cifar(plan, net, n, opt); break;
         case Strategy::LolaSmall: build_lola_small(plan, net, n); break;
         case Strategy::CryptonetsSimd: build_cryptonets_simd(plan, net); break;
         case Strategy::LinearFeatures: build_linear_features(plan, net, n); break;
@@ -1160,7 +1160,7 @@ Plan build_plan(const Network& net, Strategy s, uint32_t n) {
     return plan;
 }
 
-ExecutionResult execute(const Plan& plan, EncodedTensor input, Evaluator& ev) {  // plan.cpp:706-742
+ExecutionResult execute(const Plan& plan, EncodedTensor input, Evaluator& ev) {  // plan.cpp:597-633
     if (plan.depth_needed > ev.context().max_depth())
         throw depth_error("plan needs depth " + std::to_string(plan.depth_needed) + " but the budget allows " +
                           std::to_string(ev.context().max_depth()));

@@ -111,9 +111,17 @@ struct Plan {
     uint64_t predicted_peak() const;
 };
 
+// PlanOptions (proj/include/packnn/plan.hpp:35-41): the degree is the
+// context's, so only the window-matrix threshold is a free option here.
+struct PlanOptions {
+    // an interior window stage is realized as a row-major matrix when
+    // window_volume * maps exceeds this; smaller ones are rejected
+    uint64_t window_matrix_threshold = 100000;
+};
+
 // Host-only: builds the step table with exact predicted counters. Throws
 // std::invalid_argument when the network does not fit the strategy.
-Plan build_plan(const Network& net, Strategy s, uint32_t n);
+Plan build_plan(const Network& net, Strategy s, uint32_t n, const PlanOptions& opt = PlanOptions{});
 
 struct ExecutionResult {
     EncodedTensor output;
@@ -124,7 +132,7 @@ struct ExecutionResult {
 };
 
 // Runs the plan; std::logic_error when a step's counters deviate from the
-// prediction (proj/src/plan.cpp:719-735).
+// prediction (proj/src/plan.cpp:610-626).
 ExecutionResult execute(const Plan& plan, EncodedTensor input, Evaluator& ev);
 
 // Output scores of a sparse/dense result: device [B][values][4] words.

@@ -31,10 +31,28 @@ class lb_network(C.Structure):
                 ("stages", C.POINTER(lb_stage)), ("input_bound", i64)]
 
 
+class lb_plan_options(C.Structure):
+    """PlanOptions (proj/include/packnn/plan.hpp:35-41) minus the degree,
+    which is the context's."""
+    _fields_ = [("window_matrix_threshold", u64)]
+
+
+DEFAULT_WINDOW_MATRIX_THRESHOLD = 100000
+
+
+def _options(window_matrix_threshold: int):
+    return C.byref(lb_plan_options(window_matrix_threshold))
+
+
 _SIGS = {
     "lb_plan_counters": [C.POINTER(lb_network), C.c_char_p, u32, C.POINTER(C.c_uint64), u32,
                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)],
+    "lb_plan_counters_ex": [C.POINTER(lb_network), C.c_char_p, u32, C.POINTER(lb_plan_options),
+                            C.POINTER(C.c_uint64), u32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                            C.POINTER(C.c_uint64)],
     "lb_lola_session_create": [vp, C.POINTER(lb_network), C.c_char_p, u32, u32, vp, C.POINTER(vp)],
+    "lb_lola_session_create_ex": [vp, C.POINTER(lb_network), C.c_char_p, u32, u32, C.POINTER(lb_plan_options), vp,
+                                  C.POINTER(vp)],
     "lb_lola_session_destroy": [vp],
     "lb_lola_session_info": [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "lb_lola_session_run": [vp, vp, C.c_int, vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double)],
@@ -73,13 +91,14 @@ class NetStruct:
         return C.byref(self.s)
 
 
-def plan_counters(net: Network, strategy: str, n: int):
+def plan_counters(net: Network, strategy: str, n: int,
+                  window_matrix_threshold: int = DEFAULT_WINDOW_MATRIX_THRESHOLD):
     """Predicted per-step counters [steps][7], depth needed, predicted peak."""
     ns = NetStruct(net)
     buf = (C.c_uint64 * (7 * 64))()
     steps, depth, peak = C.c_uint32(), C.c_uint32(), C.c_uint64()
-    nat.call("lb_plan_counters", ns.ptr(), strategy.encode(), n, buf, 64, C.byref(steps), C.byref(depth),
-             C.byref(peak))
+    nat.call("lb_plan_counters_ex", ns.ptr(), strategy.encode(), n, _options(window_matrix_threshold), buf, 64,
+             C.byref(steps), C.byref(depth), C.byref(peak))
     arr = np.frombuffer(buf, dtype=np.uint64)[: 7 * steps.value].reshape(-1, 7).astype(np.int64)
     return arr, depth.value, peak.value
 
@@ -93,7 +112,8 @@ def words_to_int(w) -> int:
 class Session:
     """A plan bound to a BfvContext and a fixed batch of images."""
 
-    def __init__(self, cx, net: Network, strategy: str, batch: int, max_depth: int = 8, stream=None):
+    def __init__(self, cx, net: Network, strategy: str, batch: int, max_depth: int = 8, stream=None,
+                 window_matrix_threshold: int = DEFAULT_WINDOW_MATRIX_THRESHOLD):
         import torch
 
         self.cx, self.net, self.strategy, self.batch = cx, net, strategy, batch
@@ -101,8 +121,8 @@ class Session:
         s = torch.cuda.current_stream() if stream is None else stream
         self.stream = s
         h = vp()
-        nat.call("lb_lola_session_create", cx.handle, self._ns.ptr(), strategy.encode(), batch, max_depth,
-                 int(s.cuda_stream) or None, C.byref(h))
+        nat.call("lb_lola_session_create_ex", cx.handle, self._ns.ptr(), strategy.encode(), batch, max_depth,
+                 _options(window_matrix_threshold), int(s.cuda_stream) or None, C.byref(h))
         self.handle = h
         steps, outs, ins = C.c_uint32(), C.c_uint64(), C.c_uint64()
         nat.call("lb_lola_session_info", h, C.byref(steps), C.byref(outs), C.byref(ins))

@@ -31,6 +31,7 @@ def test_every_declared_symbol_is_exported():
 
 def test_python_binding_covers_the_header():
     bound = set(nat.declared_symbols())
+    import paper_1812_10659_b200.evaluator  # registers the Evaluator signatures  # noqa: F401
     import paper_1812_10659_b200.lola  # registers the LoLa signatures  # noqa: F401
 
     bound |= set(nat.declared_symbols())
@@ -59,3 +60,15 @@ def test_plan_rejects_bad_networks():
         plan_counters(net, "no-such-strategy", 16384)
     with pytest.raises(ValueError):
         plan_counters(net, "lola-mnist", 1024)  # 845 combined values do not fit slot row 0
+
+
+def test_window_matrix_threshold_option():
+    """PlanOptions.window_matrix_threshold (plan.hpp:35-41, plan.cpp:375-380):
+    lola-cifar's interior window stage (83*6*6 * 163 = 487,092 entries) is
+    accepted at the default and rejected once the threshold reaches it."""
+    net = nets.lola_cifar_net(config=4)
+    vol = 83 * 6 * 6 * 163
+    cnt, _, _ = plan_counters(net, "lola-cifar", 16384, window_matrix_threshold=vol - 1)
+    assert cnt.shape[0] == 7
+    with pytest.raises(ValueError):
+        plan_counters(net, "lola-cifar", 16384, window_matrix_threshold=vol)
