@@ -56,6 +56,20 @@ def workload_objects(name: str, word: int = 64):
     return cfg, strategy, batch, nets.lola_cifar_net(config=4), prm
 
 
+DATA = "synthetic (SplitMix64-seeded pixels and weights)"
+
+
+def workload_config(a, cfg, strategy, B, prm, world) -> dict:
+    """The `config` object of both arms (identical, so the driver compares
+    like with like)."""
+    return {"workload": f"{strategy} cfg{cfg} batched throughput", "images_per_gpu_per_step": B,
+            "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
+            "q_bits": max(prm.q).bit_length(), "residue_storage": "u32 words in HBM when every "
+            "ciphertext and special prime < 2^30, else u64",
+            "parallelism": f"images sharded over {world} GPU(s), no collective",
+            "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -68,6 +82,8 @@ def parse():
                          "cryptonets-simd = the cfg0 net in the CryptoNets representation (images in slots)")
     ap.add_argument("--cpu-sample", type=int, default=6, help="images in the single-thread CPU baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / roofline / CPU baseline legs")
+    ap.add_argument("--ref-procs", type=int, default=0,
+                    help="reference arm: worker processes (default: every host core this process may use)")
     ap.add_argument("--word", type=int, default=32, choices=[32, 64],
                     help="RNS word: 32 = 29/30-bit primes (32-bit word kernels, u32 residues; default), "
                          "64 = 54/60-bit primes")
@@ -75,6 +91,45 @@ def parse():
 
 
 # ---- distributed plumbing -----------------------------------------------------------
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_if_needed(a) -> None:
+    """`--gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N ranks (one per GPU) and exit with its status,
+    so a multi-GPU request can never silently measure one GPU. Under torchrun,
+    WORLD_SIZE must equal --gpus."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != a.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {a.gpus}")
+        return
+    if a.gpus <= 1 or a.impl == "reference":
+        return  # the reference arm runs on rank 0 only
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} requested but only {have} CUDA device(s) are visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.stderr.write("bench.py: relaunching under torch.distributed.run: " + " ".join(cmd) + "\n")
+    sys.exit(subprocess.call(cmd))
+
 
 def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -84,6 +139,9 @@ def dist_setup(n_gpus: int):
         import torch
         import torch.distributed as dist
 
+        if torch.cuda.device_count() <= local:
+            raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} "
+                             "device(s) are visible")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
@@ -167,38 +225,63 @@ class ClockSampler:
 
 
 # ---- CPU baseline (reference) ---------------------------------------------------------
+# The reference arm never loads this repo's device library: parameter sets
+# come from params.py (pure Python) and nets.py (numpy); the work runs in
+# oracle/_ref/libpackref.so (the unmodified reference compiled in place).
 
-def _ref_worker(args):
-    idx_list, = args
+_REF = {}
+
+
+def _ref_init(workload: str, word: int):
+    """Worker start-up (untimed): network, EvalContext and plan built once."""
     from oracle import refbind as R
+
+    cfg, strategy, _, net, prm = workload_objects(workload, word)
+    _REF["net"], _REF["cfg"] = net, cfg
+    _REF["session"] = R.RefSession(net, strategy, prm.n, prm.t, ring=True, threads=1)
+
+
+def _ref_image(i: int) -> float:
+    """One image of the workload's seeded set: encode + every HE step (the
+    per-image work of plan.encode_input + execute); returns its seconds."""
     from paper_1812_10659_b200 import nets
-    from paper_1812_10659_b200.params import lola_mnist_params
 
-    net = nets.lola_mnist_net()
-    prm = lola_mnist_params()
-    tot = 0.0
-    for i in idx_list:
-        x = nets.images(2, net, 1, start=i)[0]
-        enc, steps = R.time_plan_steps(net, "lola-mnist", prm.n, prm.t, x, ring=True, threads=1)
-        tot += enc + float(steps.sum())
-    return tot
+    x = nets.images(_REF["cfg"], _REF["net"], 1, start=i)[0]
+    _, t = _REF["session"].run(x)
+    return float(t[0] + t[1])
 
 
-def cpu_reference_throughput(images: int, procs: int) -> tuple[float, float]:
-    """Reference ring backend, encode + HE steps per image (decode excluded),
-    `procs` independent single-thread processes; returns (images/s, wall s)."""
-    import multiprocessing as mp
+def _ref_ready(_):
+    return os.getpid()
 
-    per = [list(range(p, images, procs)) for p in range(procs)]
-    per = [p for p in per if p]
-    t0 = time.perf_counter()
-    if len(per) == 1:
-        _ref_worker((per[0],))
-    else:
-        with mp.get_context("spawn").Pool(len(per)) as pool:
-            pool.map(_ref_worker, [(p,) for p in per])
-    wall = time.perf_counter() - t0
-    return images / wall, wall
+
+class RefPool:
+    """`procs` single-thread reference workers, created once (before warm-up)."""
+
+    def __init__(self, workload: str, word: int, procs: int):
+        import multiprocessing as mp
+
+        self.procs = procs
+        self.pool = mp.get_context("spawn").Pool(procs, initializer=_ref_init, initargs=(workload, word))
+        self.pool.map(_ref_ready, range(procs), chunksize=1)
+
+    def run(self, images: range) -> float:
+        """Wall seconds for every image of `images`, spread over the workers."""
+        t0 = time.perf_counter()
+        self.pool.map(_ref_image, list(images), chunksize=max(1, -(-len(images) // self.procs)))
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def cpu_reference_single(workload: str, word: int, images: int) -> tuple[float, float]:
+    """One thread, this process: (images/s, seconds) over `images` images."""
+    _ref_init(workload, word)
+    _ref_image(0)  # warm (page-in, first allocations)
+    t = sum(_ref_image(i) for i in range(images))
+    return images / t, t
 
 
 # ---- reference arm ----------------------------------------------------------------------
@@ -211,25 +294,29 @@ def run_reference(a, world, rank):
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpackref.so not built"}))
         return
-    cores = os.cpu_count() or 1
+    cfg, strategy, default_batch, net, prm = workload_objects(a.workload, a.word)
+    B = a.batch or default_batch
+    procs = min(a.ref_procs or host_cores(), B)
+    pool = RefPool(a.workload, a.word, procs)
+    images = range(0, B)  # rank 0's image range of our arm
     for _ in range(a.warmup):
-        cpu_reference_throughput(cores, cores)
-    t0 = time.perf_counter()
-    for _ in range(a.steps):
-        cpu_reference_throughput(cores, cores)
-    wall = time.perf_counter() - t0
-    value = a.steps * cores / wall
-    sample = (f"{cores} images per step (one per process, {cores} single-thread processes); "
-              "lola-mnist n=16384, 5 plaintext primes, ring backend, encode + HE steps (decode excluded: "
-              "the Boost stand-in BigInt is not representative)")
+        pool.run(images)
+    per_step = [pool.run(images) for _ in range(a.steps)]
+    pool.close()
+    wall = sum(per_step)
+    value = a.steps * B / wall
+    sample = (f"{B} images per step (the same seeded images as our arm's rank 0), {procs} single-thread worker "
+              f"processes created once before warm-up, each with its network, EvalContext and plan built once; "
+              f"per image: plan.encode_input + every plan step on the reference ring backend (plaintext "
+              f"semantics, no encryption); decode excluded (the Boost stand-in BigInt is not representative)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": wall / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "lola-mnist cfg2 batched throughput (reference packnn ring backend, CPU)",
-                   "images_per_step": cores, "n": 16384, "plain_primes": 5},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "vs_baseline": None, "dtype": "u64", "data": DATA,
+        "config": workload_config(a, cfg, strategy, B, prm, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms": [round(v * 1e3, 1) for v in per_step],
     }
     print(json.dumps(line))
 
@@ -253,54 +340,78 @@ def ncu_traffic(match) -> tuple[float | None, str | None]:
     return sum(v["bytes_per_unit"] for v in ks.values()), f"{TRAFFIC_JSON.relative_to(ROOT)}: " + ", ".join(sorted(ks))
 
 
-def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
-    """Dominant kernel (batched NTT at n=16384, the workload's word size)
-    timed alone with CUDA events on its launch stream, against the measured
-    integer-pipe roof of the same word size."""
-    import ctypes as C
+def _peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
 
-    import torch
+
+def butterfly_peak(q: int) -> float:
+    """Live integer roof of the word size of prime q: sustained
+    register-resident Harvey/Shoup butterflies per second (G/s)."""
+    import ctypes as C
 
     from paper_1812_10659_b200 import _native as nat
 
+    peak = C.c_double()
+    nat.call("lb_bench_butterfly_peak", q, 4, 4000, C.byref(peak))
+    return peak.value / 1e9
+
+
+def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
+    """The hot path's NTT alone: the u32-storage forward and inverse limb
+    transforms (ntt_forward_kernel / ntt_inverse_kernel<LOGN, u32, u32>, the
+    kernels the key switch launches) over the key switch's limb count at the
+    bench batch, timed with CUDA events on their launch stream, against the
+    live butterfly peak of the same word size. 64-bit contexts time the u64
+    kernels."""
+    import torch
+
     n, L = cx.n, cx.L
     polys = max(1, limbs // L)
-    data = torch.randint(0, min(cx.params.q), (polys, L, n), dtype=torch.int64, device="cuda")
     word = 32 if max(cx.params.q) < 2**30 else 64
+    dt = torch.int32 if word == 32 else torch.int64
+    data = torch.randint(0, min(cx.params.q), (polys, L, n), dtype=dt, device="cuda")
     s = torch.cuda.current_stream()
-    for _ in range(3):
-        cx.ntt_forward(data, limbs=L, stream=s)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(reps):
-        cx.ntt_forward(data, limbs=L, stream=s)
-    e1.record(s)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    res = {}
+    for name, fn in (("forward", cx.ntt_forward), ("inverse", cx.ntt_inverse)):
+        for _ in range(3):
+            fn(data, limbs=L, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(reps):
+            fn(data, limbs=L, stream=s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / reps
+    del data
     logn = n.bit_length() - 1
     bfly = polys * L * (n // 2) * logn
-    peak = C.c_double()
-    nat.call("lb_bench_butterfly_peak", cx.params.q[0], 4, 4000, C.byref(peak))
+    peak = butterfly_peak(cx.params.q[0])
+    ms = (res["forward"] + res["inverse"]) / 2
     achieved = bfly / (ms * 1e-3) / 1e9
-    hbm_bytes = polys * L * 16 * n
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
-    per_limb, src = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned long>")) \
-        if word == 32 else (None, None)  # the generic limb-batch API (u64 limbs)
+    wb = word // 8
+    hbm_bytes = polys * L * 2 * wb * n
+    hbm_peak = float(_peaks().get("hbm_gbs", 6552.6))
+    per_limb, src = (None, None)
+    if word == 32:
+        f_b, f_s = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned int>"))
+        i_b, i_s = ncu_traffic(lambda k: k.startswith("ntt_inverse_kernel<14, unsigned int, unsigned int>"))
+        if f_b and i_b:
+            per_limb, src = (f_b + i_b) / 2, f"{f_s}; {i_s}"
     return {
-        "kernel": f"ntt_forward_kernel<14, u{word}> ({polys * L} limbs of n={n}, "
-                  f"{max(cx.params.q).bit_length()}-bit q, {word}-bit words)",
-        "bound": "int", "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gbutterfly/s",
-        "frac": achieved / (peak.value / 1e9),
+        "kernel": f"ntt_forward_kernel + ntt_inverse_kernel<{logn}, u{word}, u{word}> (mean; {polys * L} limbs of "
+                  f"n={n}, {max(cx.params.q).bit_length()}-bit q, {word}-bit words, u{word} storage)",
+        "bound": "int", "achieved": achieved, "peak": peak, "unit": "Gbutterfly/s",
+        "frac": achieved / peak,
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
         "traffic": per_limb * polys * L if per_limb else None,
         "traffic_source": src,
-        "launch_ms": ms,
+        "launch_ms": ms, "forward_ms": res["forward"], "inverse_ms": res["inverse"],
+        "frac_forward": bfly / (res["forward"] * 1e-3) / 1e9 / peak,
+        "frac_inverse": bfly / (res["inverse"] * 1e-3) / 1e9 / peak,
         "limb_transforms_per_s": polys * L / (ms * 1e-3),
         "hbm_view": {"achieved_gbs": hbm_bytes / (ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                      "frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": hbm_bytes},
@@ -314,27 +425,26 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     step's device time), timed with CUDA events on its launch stream over a
     batch of `count` ciphertext rotations.
 
-    Algorithmic work = modular (Shoup) products per ciphertext: one per NTT
-    butterfly, per ModUp base-conversion term, per key MAC, per ModDown
-    conversion term and P^-1 scaling. Peak = the live butterfly
+    Algorithmic work = modular (Shoup) products per ciphertext by SURVEY
+    §8(d)'s formula: one per NTT butterfly, per ModUp and ModDown
+    base-conversion term and per key MAC. Peak = the live butterfly
     microbenchmark (one Shoup product + three ALU ops each), so the fraction
     is conservative; the butterfly-only view is reported beside it."""
-    import ctypes as C
-
     import torch
 
-    from paper_1812_10659_b200 import _native as nat
     from paper_1812_10659_b200.bfv import galois_exponent_columns
 
     n, L, K, dnum = cx.n, cx.L, cx.K, cx.dnum
     alpha = -(-L // dnum)
-    digits = [min(L, (j + 1) * alpha) - j * alpha for j in range(dnum)]
-    transforms = L + sum(L + K - a for a in digits) + 2 * K + 2 * L
+    # SURVEY §8(d): T = L + dnum (L + K - alpha) + 2K + 2L limb transforms;
+    # dnum alpha (L + K - alpha) N ModUp + 2 K L N ModDown conversion MACs;
+    # 2 dnum (L + K) N key inner-product MACs
+    transforms = L + dnum * (L + K - alpha) + 2 * K + 2 * L
     logn = n.bit_length() - 1
     bfly = transforms * (n // 2) * logn
-    modup = sum(a * (L + K - a) for a in digits if a > 1) * n
+    modup = dnum * alpha * (L + K - alpha) * n
     mac = 2 * dnum * (L + K) * n
-    moddown = ((K * 2 * L) if K > 1 else 0) * n + 2 * L * n
+    moddown = 2 * K * L * n
     products = bfly + modup + mac + moddown
     ct = torch.randint(0, min(cx.params.q), (count, 2, L, n), dtype=cx.res_dtype, device="cuda")
     out = torch.empty_like(ct)
@@ -351,9 +461,7 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     word = 32 if max(cx.params.q) < 2**30 else 64
-    peak = C.c_double()
-    nat.call("lb_bench_butterfly_peak", cx.params.q[0], 4, 4000, C.byref(peak))
-    peak_g = peak.value / 1e9
+    peak_g = butterfly_peak(cx.params.q[0])
     achieved = count * products / (ms * 1e-3) / 1e9
     achieved_bfly = count * bfly / (ms * 1e-3) / 1e9
     del ct, out
@@ -362,12 +470,7 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     # limbs) read once per launch set (it is shared by all `count` rotations).
     wb = word // 8
     alg_bytes = count * 4 * L * n * wb + 2 * dnum * (L + K) * n * wb
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6552.6))
+    hbm_peak = float(_peaks().get("hbm_gbs", 6552.6))
     per_ct, src = None, None
     if word == 32:
         try:
@@ -397,6 +500,155 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
     }
 
 
+def parity_check(net, imgs, scores, limit: int = 256) -> dict:
+    """Decrypted logits of the timed batch vs forward_integer, the
+    reference's integer oracle (proj/src/layers.cpp:560-594), run from
+    oracle/_ref as the checker (outside every timed region). Every image when
+    the batch has <= `limit`, else an even sample of `limit`."""
+    from oracle import refbind as R
+    from paper_1812_10659_b200.lola import words_to_int
+
+    B = scores.shape[0]
+    idx = list(range(B)) if B <= limit else list(range(0, B, B // limit))[:limit]
+    bad = []
+    for i in idx:
+        got = [words_to_int(scores[i, j]) for j in range(scores.shape[1])]
+        if got != R.forward_integer(net, imgs[i]):
+            bad.append(i)
+    return {"images": len(idx), "mismatches": len(bad), "first_bad": bad[:8],
+            "checker": "oracle/_ref forward_integer (proj/src/layers.cpp:560-594)"}
+
+
+def timed_steps(sess, steps: int) -> float:
+    """Device seconds of `steps` HE steps of a session (CUDA events)."""
+    import torch
+
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        sess.execute()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def value_w64(a, net, strategy, B, imgs) -> dict:
+    """The same plan on the 60-bit parameter set (64-bit Shoup words, u64
+    residues): device-timed HE steps and the decrypted logits' parity."""
+    import numpy as np
+    import torch
+
+    from paper_1812_10659_b200.bfv import BfvContext
+    from paper_1812_10659_b200.lola import Session
+    from paper_1812_10659_b200.params import lola_mnist_params
+
+    prm = lola_mnist_params()
+    cx = BfvContext(prm)
+    sess = Session(cx, net, strategy, B)
+    sess.encrypt(torch.from_numpy(imgs).cuda(), on_device=True)
+    for _ in range(2):
+        sess.execute()
+    steps = max(2, min(a.steps, 5))
+    sec = timed_steps(sess, steps)
+    scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
+    sess.run_raw(np.ascontiguousarray(imgs), scores, False, False, want_counters=False, want_times=False)
+    par = parity_check(net, imgs, scores)
+    del sess, cx
+    torch.cuda.empty_cache()
+    return {"value": B * steps / sec, "unit": UNIT, "ms_per_step": sec / steps * 1e3, "steps": steps,
+            "images_per_step": B, "dtype": "u64", "q_bits": max(prm.q).bit_length(), "L": prm.L, "K": prm.K,
+            "dnum": prm.dnum, "parity": par,
+            "butterfly_peak_gbfly_s": butterfly_peak(prm.q[0])}
+
+
+# BASELINE config 1 grid of the bench's primitive leg: (n, L, K, dnum, bits)
+PRIMITIVE_GRID = [(4096, 4, 1, 0, 60), (8192, 6, 2, 3, 60), (16384, 8, 2, 4, 60), (32768, 12, 2, 6, 60),
+                  (16384, 10, 5, 2, 29)]
+
+
+def primitives(batch: int = 64, reps: int = 10) -> list[dict]:
+    """Config 1: batches of 64 ciphertexts, NTT limb transforms/s (vs the
+    live butterfly roof), ct x pt, ct + ct, rotations and square+relin per
+    second, device-timed; with the reference's per-limb CPU times beside."""
+    import torch
+
+    from oracle import refbind as R
+    from paper_1812_10659_b200.bfv import BfvContext, galois_exponent_columns
+    from paper_1812_10659_b200.params import make_params
+
+    def timed(fn, r):
+        for _ in range(2):
+            fn()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(r):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / r * 1e-3
+
+    out = []
+    for n, L, K, dnum, bits in PRIMITIVE_GRID:
+        prm = make_params(n, L=L, T=1, K=K, dnum=dnum, bits=bits, seed=1)
+        cx = BfvContext(prm)
+        peak = butterfly_peak(prm.q[0])
+        vals = torch.randint(-1000, 1000, (batch, n), dtype=torch.int64, device="cuda")
+        ct = cx.encrypt_slots(vals, id_base=1)
+        ct2 = cx.encrypt_slots(vals, id_base=batch + 1)
+        pm, _ = cx.encode_plain(vals[0], add=False)
+        o = torch.empty_like(ct)
+        limbs = torch.randint(0, min(prm.q), (batch * 2, L, n), dtype=cx.res_dtype, device="cuda")
+        g = galois_exponent_columns(n, 1)
+        cx.keygen(g)
+        cx.keygen(0)
+        t_fwd = timed(lambda: cx.ntt_forward(limbs, limbs=L), reps)
+        t_inv = timed(lambda: cx.ntt_inverse(limbs, limbs=L), reps)
+        t_mp = timed(lambda: cx.mul_plain(ct, pm, out=o), reps)
+        t_add = timed(lambda: cx.add(ct, ct2, out=o), reps)
+        t_rot = timed(lambda: cx.rotate(ct, g, out=o), max(2, reps // 2))
+        t_sq = timed(lambda: cx.mul(ct, ct, out=o), max(2, reps // 2))
+        nl = batch * 2 * L
+        bfly = nl * (n // 2) * (n.bit_length() - 1)
+        cpu = R.time_primitives(prm.q[0], n, 3)
+        out.append({
+            "n": n, "L": L, "K": K, "dnum": prm.dnum, "q_bits": bits, "batch": batch,
+            "word": "u32" if cx.res_dtype == torch.int32 else "u64",
+            "ntt_fwd_limbs_per_s": nl / t_fwd, "ntt_inv_limbs_per_s": nl / t_inv,
+            "ntt_fwd_frac": bfly / t_fwd / 1e9 / peak, "ntt_inv_frac": bfly / t_inv / 1e9 / peak,
+            "butterfly_peak_gbfly_s": peak,
+            "ct_pt_per_s": batch / t_mp, "ct_add_per_s": batch / t_add, "rotations_per_s": batch / t_rot,
+            "square_relin_per_s": batch / t_sq,
+            "cpu_reference_per_limb_s": cpu,
+        })
+        del cx, ct, ct2, o, limbs, pm, vals
+        torch.cuda.empty_cache()
+    return out
+
+
+def cpu_bfv_baseline(prm, ks_per_image: int) -> dict:
+    """Our CPU BFV oracle (oracle/bfv_oracle.cpp, one thread) running the
+    plan's key-switch mix: seconds per rotation (automorphism + hybrid key
+    switch, key made once) x key switches per image."""
+    import numpy as np
+
+    from oracle.bfvbind import Oracle
+
+    o = Oracle.from_params(prm)
+    rng = np.random.default_rng(0)
+    ct = np.stack([np.stack([rng.integers(0, q, prm.n, dtype=np.uint64) for q in prm.q]) for _ in range(2)])
+    _, sec = o.time_rotate(ct, 3, 2)
+    per = sec / 2
+    return {"value": 1.0 / (per * ks_per_image), "unit": UNIT, "cores": 1, "kind": "port",
+            "seconds_per_key_switch": per, "key_switches_per_image": ks_per_image,
+            "sample": f"2 rotations (n={prm.n}, L={prm.L}, K={prm.K}, dnum={prm.dnum}) on the CPU BFV oracle, "
+                      f"one thread; inferences/s = 1 / (seconds per key switch x {ks_per_image} key switches per "
+                      "image), key switching only (a lower bound on a CPU BFV inference's time)"}
+
+
 def run_ours(a, world, rank, local):
     import numpy as np
     import torch
@@ -405,6 +657,7 @@ def run_ours(a, world, rank, local):
     from paper_1812_10659_b200 import nets
     from paper_1812_10659_b200.bfv import BfvContext
     from paper_1812_10659_b200.lola import Session, plan_counters
+    from paper_1812_10659_b200.shard import shard_range, sum_over_ranks
     torch.cuda.set_device(local)
     cfg, strategy, default_batch, net, prm = workload_objects(a.workload, a.word)
     cx = BfvContext(prm)
@@ -416,12 +669,11 @@ def run_ours(a, world, rank, local):
         nat.call("lb_pool_reserve", cx.handle, int(free * 0.5))
     sess = Session(cx, net, strategy, B)
     # images of this rank: a disjoint contiguous range of the job's image set
-    from paper_1812_10659_b200.shard import shard_range
-
     imgs = nets.images(cfg, net, B, start=shard_range(world * B, world, rank).start)
     dev_imgs = torch.from_numpy(imgs).cuda()
     counters, _, _ = plan_counters(net, strategy, prm.n)
     rot_per_image = int(counters[:, 5:7].sum()) * len(prm.t)
+    ks_per_image = rot_per_image + int(counters[:, 0].sum()) * len(prm.t)
     s = torch.cuda.current_stream()
 
     # warm-up: key generation, plaintext encoding, pool growth
@@ -482,6 +734,7 @@ def run_ours(a, world, rank, local):
         e2e_warm.append(time.perf_counter() - t0)
         if len(e2e_warm) >= 2 and abs(e2e_warm[-1] - e2e_warm[-2]) <= 0.05 * min(e2e_warm[-2:]):
             break
+    scores[:] = 0
     barrier(world)
     torch.cuda.synchronize()
     e0.record(s)
@@ -492,6 +745,17 @@ def run_ours(a, world, rank, local):
     barrier(world)
     e2e_elapsed = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
     e2e_value = world * B * a.steps / e2e_elapsed
+
+    # ---- parity of exactly what was timed: the last e2e step's decrypted
+    # logits of every image of this rank vs the reference's integer oracle ----
+    par = parity_check(net, imgs, scores)
+    mism = int(sum_over_ranks(float(par["mismatches"]), world))
+    checked = int(sum_over_ranks(float(par["images"]), world))
+    parity = {"images": checked, "mismatches": mism, "checker": par["checker"],
+              "of": f"decrypted logits of the last timed e2e step, {'all' if checked == world * B else 'a sample of'} "
+                    f"{world * B} images"}
+    if rank == 0 and par["first_bad"]:
+        parity["first_bad_rank0"] = par["first_bad"]
 
     extras = {}
     if rank == 0 and not a.no_extras:
@@ -525,45 +789,55 @@ def run_ours(a, world, rank, local):
         extras["roofline"] = ks_roofline(cx, 16 * len(prm.t))
         ks_limbs = B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1)
         extras["roofline_ntt"] = ntt_roofline(cx, ks_limbs)
-        # CPU baseline: the reference on this host, one thread, bounded sample
+        if a.workload == "lola-mnist" and a.word == 32:
+            del cx
+            torch.cuda.empty_cache()
+            extras["value_w64"] = value_w64(a, net, strategy, B, imgs)
+            extras["primitives"] = primitives()
+        # CPU baselines on this host: the reference (one thread, bounded
+        # sample) and our CPU BFV oracle's key switching
         try:
             from oracle import refbind as R
 
-            if R.available() and a.workload == "lola-mnist":
-                ips, wall = cpu_reference_throughput(a.cpu_sample, 1)
+            if R.available():
+                ips, sec = cpu_reference_single(a.workload, a.word, a.cpu_sample)
                 extras["cpu_baseline"] = {
                     "value": ips, "unit": UNIT, "cores": 1, "kind": "reference",
-                    "sample": f"{a.cpu_sample} images, reference packnn ring backend (plaintext semantics, no "
-                              f"encryption), encode + HE steps, decode excluded; {wall:.1f} s"}
+                    "sample": f"{a.cpu_sample} images of the workload, reference packnn ring backend (plaintext "
+                              f"semantics, no encryption), network/EvalContext/plan built once, per image "
+                              f"encode + every plan step, decode excluded; {sec:.1f} s"}
+            extras["cpu_baseline_bfv"] = cpu_bfv_baseline(prm, ks_per_image)
         except Exception as exc:  # reported, never fatal to the GPU number
-            extras["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+            extras.setdefault("cpu_baseline", {"value": None, "error": str(exc)[:200]})
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": elapsed / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32" if max(prm.q) < 2**30 else "u64",
-            "data": "synthetic (SplitMix64-seeded pixels and weights)",
-            "config": {"workload": f"{strategy} cfg{cfg} batched throughput", "images_per_gpu_per_step": B,
-                       "n": prm.n, "plain_primes": len(prm.t), "L": prm.L, "K": prm.K, "dnum": prm.dnum,
-                       "q_bits": max(prm.q).bit_length(), "residue_storage": "u32 words in HBM when every "
-                       "ciphertext and special prime < 2^30, else u64", "parallelism": f"images sharded over {world} GPU(s), no collective",
-                       "l2": "working set (encrypted batch, GBs) far larger than the 126 MB L2"},
+            "data": DATA,
+            "config": workload_config(a, cfg, strategy, B, prm, world),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes) * world,
                     "d2h_bytes_per_step": int(scores.nbytes) * world},
+            "parity": parity,
             "gpu_launches": launches,
             "step_ms": [round(v, 3) for v in step_ms],
             "warmup_ms": [round(v, 3) for v in warm],
             "clocks": clk.summary(),
             "rotations_per_s": value * rot_per_image,
-            "key_switches_per_image": rot_per_image + int(counters[:, 0].sum()) * len(prm.t),
+            "key_switches_per_image": ks_per_image,
         }
         line.update(extras)
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
+    if mism:
+        sys.stderr.write(f"bench.py: PARITY FAILURE: {mism} of {checked} images' decrypted logits differ from "
+                         "forward_integer\n")
+        sys.exit(3)
 
 
 def main():
     a = parse()
+    relaunch_if_needed(a)
     world, rank, local = dist_setup(a.gpus)
     if a.impl == "reference":
         run_reference(a, world, rank)

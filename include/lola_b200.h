@@ -93,6 +93,13 @@ int lb_ntt_forward(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
                    uint32_t first_prime, uint64_t poly_stride, void* stream);
 int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limbs,
                    uint32_t first_prime, uint64_t poly_stride, void* stream);
+/* The same on u32 residue words (the storage word of ciphertexts whose
+ * primes are all below 2^30, and of the key switch's intermediates: the
+ * transforms the hot path runs). Every limb's prime must be below 2^30. */
+int lb_ntt_forward_u32(lb_context* cx, uint32_t* data, uint32_t polys, uint32_t limbs,
+                       uint32_t first_prime, uint64_t poly_stride, void* stream);
+int lb_ntt_inverse_u32(lb_context* cx, uint32_t* data, uint32_t polys, uint32_t limbs,
+                       uint32_t first_prime, uint64_t poly_stride, void* stream);
 
 /* ---- BFV ciphertext operations ---------------------------
  * A ciphertext is [2][L][n] residue words in the evaluation (NTT) domain. A message
@@ -104,7 +111,12 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
 /* Evaluator::lift (proj/src/evaluator.cpp:67-91) + encryption: values is
  * [B][n] int64 slot values (reduced mod each t_j, slot-encoded with the
  * reference's generator-3 order, ring.cpp:138-144), out [B][T][2][L][n];
- * ciphertext c gets randomness id id_base + c. */
+ * ciphertext c gets randomness id id_base + c. id_base = LB_FRESH_IDS draws
+ * B*T fresh ids from the context's single counter (the one every evaluator
+ * and session uses), so no two encryptions share (a, e); an explicit id_base
+ * exists for coefficient parity with the CPU oracle and must not be reused
+ * outside tests. */
+#define LB_FRESH_IDS UINT64_MAX
 int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, void* stream);
 /* decryption + Evaluator::lower's slot decode (evaluator.cpp:98-118, before
  * the CRT join): out [B][T][n] slot residues mod t_j. */

@@ -4,6 +4,7 @@
 //
 // Deliberately plain: scalar loops, `unsigned __int128 %` for every modular
 // product, a textbook natural-order transform, coefficient-domain data.
+#include <chrono>
 #include "bfv_oracle.h"
 
 #include <algorithm>
@@ -602,6 +603,33 @@ int bo_rotate(bo_ctx* c, const uint64_t* ct, uint64_t g, uint64_t* out) {
             for (uint32_t k = 0; k < c->n; ++k) c0[i][k] = addm(c0[i][k], u[0][i][k], c->q[i]);
         pack(*c, c0, out);
         pack(*c, u[1], out + (size_t)L * c->n);
+    });
+}
+
+// CPU-baseline timing: `reps` rotations of one ciphertext by g with the key
+// generated once (outside the timed region): automorphism + hybrid key
+// switch + add, the same work as bo_rotate. seconds = total wall time.
+int bo_time_rotate(bo_ctx* c, const uint64_t* ct, uint64_t g, uint32_t reps, uint64_t* out, double* seconds) {
+    return guarded([&] {
+        const uint32_t L = c->L, LK = L + c->K;
+        auto sg = galois_signed(c->s, g, c->n);
+        Rns target(LK);
+        for (uint32_t r = 0; r < LK; ++r) target[r] = c->reduce_signed(sg, c->ntt_qp(r).p);
+        auto key = make_key(*c, g, target);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (uint32_t rep = 0; rep < reps; ++rep) {
+            Rns c0 = unpack(*c, ct, L), c1 = unpack(*c, ct + (size_t)L * c->n, L);
+            for (uint32_t i = 0; i < L; ++i) {
+                c0[i] = galois(c0[i], g, c->q[i], c->n);
+                c1[i] = galois(c1[i], g, c->q[i], c->n);
+            }
+            auto u = key_switch(*c, c1, key);
+            for (uint32_t i = 0; i < L; ++i)
+                for (uint32_t k = 0; k < c->n; ++k) c0[i][k] = addm(c0[i][k], u[0][i][k], c->q[i]);
+            pack(*c, c0, out);
+            pack(*c, u[1], out + (size_t)L * c->n);
+        }
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
 }
 

@@ -68,6 +68,8 @@ int bo_add(bo_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out);
 /* §3.5 key switching and rotations */
 int bo_galois_key(bo_ctx* c, uint64_t g, uint64_t* key /* [dnum][2][L+K][n] coeffs */);
 int bo_rotate(bo_ctx* c, const uint64_t* ct, uint64_t g, uint64_t* out);
+/* CPU-baseline timing: reps rotations with the key made once; total seconds */
+int bo_time_rotate(bo_ctx* c, const uint64_t* ct, uint64_t g, uint32_t reps, uint64_t* out, double* seconds);
 /* §3.6 multiplication: tensor (HPS-style exact scaling) + relinearization */
 int bo_mul(bo_ctx* c, uint32_t tj, const uint64_t* a, const uint64_t* b, uint64_t* out);
 

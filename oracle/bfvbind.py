@@ -41,6 +41,7 @@ def lib():
             "bo_add": [C.c_void_p, P64, P64, P64],
             "bo_galois_key": [C.c_void_p, u64, P64],
             "bo_rotate": [C.c_void_p, P64, u64, P64],
+            "bo_time_rotate": [C.c_void_p, P64, u64, u32, P64, C.POINTER(C.c_double)],
             "bo_mul": [C.c_void_p, u32, P64, P64, P64],
             "bo_phase": [C.c_void_p, P64, P64],
         }
@@ -155,6 +156,14 @@ class Oracle:
         out = self._ct()
         self._chk(lib().bo_rotate(self.h, _p(c), g, _p(out)))
         return out
+
+    def time_rotate(self, ct, g, reps: int = 1) -> tuple[np.ndarray, float]:
+        """(rotated ciphertext, seconds for `reps` rotations), key made once."""
+        c = _u(ct)
+        out = self._ct()
+        sec = C.c_double()
+        self._chk(lib().bo_time_rotate(self.h, _p(c), g, reps, _p(out), C.byref(sec)))
+        return out, sec.value
 
     def mul(self, tj, a, b):
         a, b = _u(a), _u(b)

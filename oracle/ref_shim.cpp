@@ -197,6 +197,36 @@ int pref_galois_apply(uint64_t p, uint32_t n, const uint64_t* in, uint64_t expon
     });
 }
 
+// Per-limb CPU timings of the reference ring primitives (tables built once,
+// outside the timed loops), seconds per call averaged over `reps`:
+// out[0] NttTables::forward, out[1] inverse (ring.cpp:97-115), out[2]
+// poly_mul_negacyclic (ring.cpp:117-122), out[3] galois_apply with the
+// column-rotation-by-1 exponent (ring.cpp:155-182).
+int pref_time_primitives(uint64_t p, uint32_t n, uint32_t reps, double* out) {
+    return guarded([&] {
+        NttTables t = NttTables::create(PrimeModulus::create(p, n));
+        std::vector<uint64_t> a(n), b(n);
+        uint64_t x = 0x9E3779B97F4A7C15ull;
+        for (uint32_t i = 0; i < n; ++i) {
+            x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+            a[i] = x % p;
+            b[i] = (x >> 7) % p;
+        }
+        volatile uint64_t sink = 0;
+        auto time = [&](auto&& f) {
+            const auto t0 = std::chrono::steady_clock::now();
+            for (uint32_t r = 0; r < reps; ++r) sink = sink + f();
+            return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+        };
+        RingElement ra{a}, rb{b};
+        const uint64_t g = galois_exponent_columns(n, 1);
+        out[0] = time([&] { return t.forward(std::span<const uint64_t>(a))[1]; });
+        out[1] = time([&] { return t.inverse(std::span<const uint64_t>(a))[1]; });
+        out[2] = time([&] { return poly_mul_negacyclic(t, ra, rb).coeffs[1]; });
+        out[3] = time([&] { return galois_apply(t, ra, g).coeffs[1]; });
+    });
+}
+
 int pref_galois_exponent_columns(uint32_t n, uint32_t k, uint64_t* out) {
     return guarded([&] { *out = galois_exponent_columns(n, k); });
 }
@@ -471,6 +501,74 @@ int pref_time_plan_steps(const pref_net* net, const char* strategy, uint32_t n, 
         }
         *steps_out = static_cast<uint32_t>(plan.steps.size());
     });
+}
+
+
+// Persistent plan session for the CPU baseline / reference arm: the network,
+// the EvalContext (NttTables per prime) and the plan are built once, so each
+// timed run is exactly the per-image work of the reference:
+// plan.encode_input, then every step closure in order (execute's loop,
+// proj/src/plan.cpp:610-626), then optionally decode
+// (representation.cpp:185-223; excluded from timings by default because the
+// Boost stand-in BigInt is not representative of Boost's speed).
+struct pref_session {
+    QuantizedNetwork net;
+    EvalContext cx;
+    InferencePlan plan;
+    bool small;
+    pref_session(QuantizedNetwork q, BackendKind kind, uint32_t n, std::vector<uint64_t> primes, bool is_small,
+                 const char* strategy)
+        : net(std::move(q)), cx(kind, n, std::move(primes)), small(is_small) {
+        if (!small) {
+            PlanOptions opt;
+            opt.n = n;
+            plan = build_plan(net, strategy_from_name(strategy), opt);
+        }
+    }
+};
+
+int pref_session_create(const pref_net* net, const char* strategy, uint32_t n, const uint64_t* primes,
+                        uint32_t nprimes, int backend, uint32_t threads, pref_session** out) {
+    return guarded([&] {
+        set_kernel_threads(threads);
+        *out = new pref_session(make_network(net), backend ? BackendKind::Ring : BackendKind::Slot, n,
+                                std::vector<uint64_t>(primes, primes + nprimes), strategy_is_small(strategy),
+                                strategy);
+    });
+}
+
+int pref_session_destroy(pref_session* s) {
+    return guarded([&] { delete s; });
+}
+
+// times: encode, HE steps, decode seconds (decode = -1 when not requested);
+// scores_out receives the decimal scores when decode != 0.
+int pref_session_run(pref_session* s, const int64_t* x, int decode_scores, char* scores_out, uint64_t scores_cap,
+                     double* times) {
+    int rc = 0;
+    int st = guarded([&] {
+        std::vector<int64_t> xv(x, x + s->net.input.values());
+        Evaluator ev(s->cx);
+        if (s->small) {
+            SmallRun r = run_lola_small(s->net, xv, ev, &times[0], &times[1], &times[2]);
+            if (decode_scores) rc = copy_string(join_bigints(r.scores), scores_out, scores_cap);
+            return;
+        }
+        auto t0 = std::chrono::steady_clock::now();
+        EncodedTensor cur = s->plan.encode_input(ev, xv);
+        auto t1 = std::chrono::steady_clock::now();
+        for (const PlanStep& step : s->plan.steps) cur = step.run(ev, s->net, cur);
+        auto t2 = std::chrono::steady_clock::now();
+        times[0] = std::chrono::duration<double>(t1 - t0).count();
+        times[1] = std::chrono::duration<double>(t2 - t1).count();
+        times[2] = -1.0;
+        if (decode_scores) {
+            std::vector<BigInt> scores = decode(ev, cur);
+            times[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+            rc = copy_string(join_bigints(scores), scores_out, scores_cap);
+        }
+    });
+    return st ? st : rc;
 }
 
 }  // extern "C"

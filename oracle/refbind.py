@@ -63,6 +63,10 @@ _SIGS = {
                       P64, u32, PU32, PF64],
     "pref_time_plan_steps": [C.POINTER(pref_net), C.c_char_p, u32, P64, u32, C.c_int, u32, PI64, PF64, u32,
                              PU32, PF64],
+    "pref_time_primitives": [u64, u32, u32, PF64],
+    "pref_session_create": [C.POINTER(pref_net), C.c_char_p, u32, P64, u32, C.c_int, u32, C.POINTER(vp)],
+    "pref_session_destroy": [vp],
+    "pref_session_run": [vp, PI64, C.c_int, C.c_char_p, u64, PF64],
 }
 
 _lib = None
@@ -133,6 +137,14 @@ def ntt_many_seconds(p: int, n: int, limbs: np.ndarray, inverse: bool = False) -
     sec = C.c_double()
     _check(lib().pref_ntt_forward_many(p, n, a.size // n, _u64(a), _u64(out), int(inverse), C.byref(sec)))
     return out.reshape(-1, n), sec.value
+
+
+def time_primitives(p: int, n: int, reps: int = 5) -> dict:
+    """Seconds per limb of the reference's forward / inverse NTT,
+    poly_mul_negacyclic and galois_apply (tables built once)."""
+    out = np.zeros(4, dtype=np.float64)
+    _check(lib().pref_time_primitives(p, n, reps, out.ctypes.data_as(PF64)))
+    return dict(zip(("ntt_forward", "ntt_inverse", "poly_mul", "galois_apply"), out.tolist()))
 
 
 def slot_to_eval(p: int, n: int) -> np.ndarray:
@@ -292,3 +304,38 @@ def time_plan_steps(net, strategy: str, n: int, primes, x, ring: bool = True, th
                                       xv.ctypes.data_as(PI64), st.ctypes.data_as(PF64), 64, C.byref(steps),
                                       C.byref(enc)))
     return enc.value, st[: steps.value]
+
+
+class RefSession:
+    """Network, EvalContext and plan built once (pref_session_create); each
+    run() is the reference's per-image work: encode_input + every plan step
+    (+ decode when asked). Returns (scores or None, [encode, steps, decode] s)."""
+
+    def __init__(self, net, strategy: str, n: int, primes, ring: bool = True, threads: int = 1):
+        self._h = NetHandle(net)
+        p = _arr(primes)
+        h = vp()
+        _check(lib().pref_session_create(self._h.ptr(), strategy.encode(), n, _u64(p), p.size, int(ring), threads,
+                                         C.byref(h)))
+        self.handle = h
+
+    def run(self, x, decode: bool = False):
+        xv = np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+        times = np.zeros(3, dtype=np.float64)
+        cap = (1 << 22) if decode else 1
+        buf = C.create_string_buffer(cap)
+        _check(lib().pref_session_run(self.handle, xv.ctypes.data_as(PI64), int(decode), buf, cap,
+                                      times.ctypes.data_as(PF64)))
+        scores = [int(v) for v in buf.value.decode().split(",")] if decode else None
+        return scores, times
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().pref_session_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -46,6 +46,8 @@ _SIGS: dict[str, list] = {
     "lb_sync": [vp, vp],
     "lb_ntt_forward": [vp, vp, u32, u32, u32, u64, vp],
     "lb_ntt_inverse": [vp, vp, u32, u32, u32, u64, vp],
+    "lb_ntt_forward_u32": [vp, vp, u32, u32, u32, u64, vp],
+    "lb_ntt_inverse_u32": [vp, vp, u32, u32, u32, u64, vp],
     "lb_bench_butterfly_peak": [u64, C.c_int, C.c_int, C.POINTER(C.c_double)],
     "lb_encrypt_slots": [vp, vp, u32, u64, vp, vp],
     "lb_decrypt_slots": [vp, vp, u32, vp, vp],

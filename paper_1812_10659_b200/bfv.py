@@ -19,6 +19,8 @@ from . import _native as nat
 from .context import Context, _stream_ptr
 from .params import BfvParams
 
+LB_FRESH_IDS = 2**64 - 1  # include/lola_b200.h
+
 
 class _DevPtr:
     """Exposes a raw device pointer through __cuda_array_interface__."""
@@ -62,7 +64,11 @@ class BfvContext(Context):
         return ct.numel() // per
 
     # ---- encode / encrypt / decrypt ------------------------------------------
-    def encrypt_slots(self, values: torch.Tensor, id_base: int = 0, stream=None) -> torch.Tensor:
+    def encrypt_slots(self, values: torch.Tensor, id_base: int | None = None, stream=None) -> torch.Tensor:
+        """id_base None: fresh randomness ids from the context's counter
+        (LB_FRESH_IDS); an explicit id_base is for oracle parity tests."""
+        if id_base is None:
+            id_base = LB_FRESH_IDS
         values = values.reshape(-1, self.n).contiguous()
         B = values.shape[0]
         out = torch.empty((B, self.T, 2, self.L, self.n), dtype=self.res_dtype, device="cuda")

@@ -97,8 +97,14 @@ class Context:
         nat.call("lb_sync", self.handle, _stream_ptr(stream))
 
     def _ntt(self, name, data, limbs, first_prime, polys, poly_stride, stream):
+        import torch
+
         if not data.is_cuda or not data.is_contiguous():
             raise ValueError("NTT operand must be a contiguous CUDA tensor")
+        if data.dtype == torch.int32:
+            name += "_u32"  # u32 residue words (primes < 2^30)
+        elif data.dtype != torch.int64:
+            raise ValueError("NTT operand must be int64 (u64 residues) or int32 (u32 residues)")
         n = self.n
         if polys is None:
             polys = data.numel() // (limbs * n)
@@ -109,7 +115,8 @@ class Context:
         nat.call(name, self.handle, data.data_ptr(), polys, limbs, first_prime, poly_stride, _stream_ptr(stream))
 
     def ntt_forward(self, data, limbs: int, first_prime: int = 0, polys=None, poly_stride=None, stream=None):
-        """In place; data is [polys][limbs][n] int64 on the device."""
+        """In place; data is [polys][limbs][n] int64 (u64 residues) or int32
+        (u32 residues, primes < 2^30) on the device."""
         self._ntt("lb_ntt_forward", data, limbs, first_prime, polys, poly_stride, stream)
 
     def ntt_inverse(self, data, limbs: int, first_prime: int = 0, polys=None, poly_stride=None, stream=None):

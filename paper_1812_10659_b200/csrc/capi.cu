@@ -113,10 +113,33 @@ int lb_ntt_inverse(lb_context* cx, uint64_t* data, uint32_t polys, uint32_t limb
     });
 }
 
+int lb_ntt_forward_u32(lb_context* cx, uint32_t* data, uint32_t polys, uint32_t limbs, uint32_t first_prime,
+                       uint64_t poly_stride, void* stream) {
+    return guarded([&] {
+        if (cx) cx->cx.activate();
+        need(cx && data, "null argument");
+        lb::LimbBatch b{reinterpret_cast<uint64_t*>(data), polys, limbs, first_prime, poly_stride};
+        b.packed32 = true;
+        cx->cx.ntt_forward(b, pick(cx, stream));
+    });
+}
+
+int lb_ntt_inverse_u32(lb_context* cx, uint32_t* data, uint32_t polys, uint32_t limbs, uint32_t first_prime,
+                       uint64_t poly_stride, void* stream) {
+    return guarded([&] {
+        if (cx) cx->cx.activate();
+        need(cx && data, "null argument");
+        lb::LimbBatch b{reinterpret_cast<uint64_t*>(data), polys, limbs, first_prime, poly_stride};
+        b.packed32 = true;
+        cx->cx.ntt_inverse(b, pick(cx, stream));
+    });
+}
+
 int lb_encrypt_slots(lb_context* cx, const int64_t* values, uint32_t B, uint64_t id_base, void* out, void* stream) {
     return guarded([&] {
         if (cx) cx->cx.activate();
         need(cx && values && out, "null argument");
+        if (id_base == UINT64_MAX) id_base = cx->cx.reserve_ciphertext_ids(uint64_t(B) * cx->cx.T());
         lb::encrypt_slots(cx->cx, values, B, id_base, out, pick(cx, stream));
     });
 }

@@ -137,6 +137,12 @@ public:
 
     BfvState* bfv() const { return bfv_.get(); }
 
+    // Ciphertext ids select the encryption randomness (the
+    // streams of a and e). They come from ONE counter per context, shared by
+    // every evaluator, fork and session on it, so no two encryptions under
+    // this context's keys reuse (a, e). Returns the first of `count` ids.
+    uint64_t reserve_ciphertext_ids(uint64_t count) const { return next_ct_id_.fetch_add(count); }
+
 private:
     Params prm_;
     uint32_t n_;
@@ -151,6 +157,7 @@ private:
     DeviceBuffer d_tables_;
     DeviceBuffer d_primes_;
     std::unique_ptr<BfvState> bfv_;
+    mutable std::atomic<uint64_t> next_ct_id_{1};
     friend struct BfvState;
     friend void bfv_setup(Context&);
 };

@@ -233,13 +233,18 @@ EvalContext::EvalContext(Context& cx, uint32_t batch, uint32_t max_depth, cudaSt
     if (cx.T() == 0 || cx.T() > 8) throw std::invalid_argument("need 1..8 plaintext primes");
     Mag comp(1);
     for (uint32_t j = 0; j < cx.T(); ++j) comp = comp * Mag(cx.prime(cx.t_index(j)));
+    // the device CRT (k_crt_center) writes centered values as 256-bit two's
+    // complement: the composite must stay below 2^255 (Mag saturates above
+    // 2^320, which this check also rejects)
+    if (comp.w[4] != 0 || (comp.w[3] >> 63) != 0)
+        throw std::invalid_argument("product of the plaintext primes must be below 2^255");
     capacity_ = comp.minus_one().half_floor();  // (composite - 1) / 2, ring.hpp:30
 }
 
 // ---- Evaluator -------------------------------------------------------------------------
 
 Evaluator::Evaluator(const EvalContext& cx)
-    : cx_(&cx), stream_(cx.stream()), cache_(std::make_shared<PlainCache>()), next_id_(std::make_shared<uint64_t>(1)) {}
+    : cx_(&cx), stream_(cx.stream()), cache_(std::make_shared<PlainCache>()) {}
 
 Evaluator Evaluator::fork() const { return fork_on(stream_); }
 
@@ -247,7 +252,6 @@ Evaluator Evaluator::fork_on(cudaStream_t s) const {
     Evaluator e(*cx_);
     e.stream_ = s;
     e.cache_ = cache_;
-    e.next_id_ = next_id_;
     return e;
 }
 
@@ -296,8 +300,7 @@ Message Evaluator::lift_batch(const std::vector<std::vector<int64_t>>& values) c
     DeviceBuffer dv(host.size() * 8, s);
     LB_CUDA(cudaMemcpyAsync(dv.get(), host.data(), host.size() * 8, cudaMemcpyHostToDevice, s));
     Message m = fresh(0, 0, mag);
-    const uint64_t id = *next_id_;
-    *next_id_ += cx_->cts();
+    const uint64_t id = cx_->device().reserve_ciphertext_ids(cx_->cts());
     encrypt_slots(cx_->device(), dv.get<int64_t>(), B, id, m.data(), s);
     LB_CUDA(cudaStreamSynchronize(s));  // `host` is pageable and local
     return m;
@@ -331,8 +334,7 @@ std::vector<Message> Evaluator::lift_gather_many(const int64_t* dev_images, uint
     out.reserve(count);
     for (uint32_t m = 0; m < count; ++m) {
         out.push_back(fresh(0, 0, mag));
-        const uint64_t id = *next_id_;
-        *next_id_ += cx_->cts();
+        const uint64_t id = cx_->device().reserve_ciphertext_ids(cx_->cts());
         encrypt_slots(cx_->device(), slots.get<int64_t>() + uint64_t(m) * B * n, B, id, out.back().data(), s);
     }
     return out;

@@ -203,7 +203,8 @@ public:
     void note_live(uint64_t live) { counters_.note_live(live); }
     Evaluator fork() const;
     void absorb(const Evaluator& child);
-    // fork whose device work goes to stream `s` (shares caches and ids)
+    // fork whose device work goes to stream `s` (shares the plaintext cache;
+    // ciphertext ids come from the context's counter)
     Evaluator fork_on(cudaStream_t s) const;
     cudaStream_t stream() const { return stream_; }
 
@@ -212,7 +213,6 @@ private:
     cudaStream_t stream_;
     OpCounters counters_;
     std::shared_ptr<PlainCache> cache_;
-    std::shared_ptr<uint64_t> next_id_;
 
     Message fresh(uint32_t depth, uint32_t plain_depth, Mag mag) const;
     void check_magnitude(const Mag& m, const char* op) const;

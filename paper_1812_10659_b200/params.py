@@ -11,7 +11,55 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from .context import find_primes
+_MR_BASES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+
+
+def is_prime_u64(v: int) -> bool:
+    """Deterministic Miller-Rabin for every u64 (the bases of
+    proj/src/modular.cpp:22-42; same routine as csrc/host_math.hpp)."""
+    if v < 2:
+        return False
+    for s in _MR_BASES:
+        if v % s == 0:
+            return v == s
+    d, r = v - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in _MR_BASES:
+        x = pow(a, d, v)
+        if x in (1, v - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % v
+            if x == v - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def find_primes(bits: int, log_mod: int, count: int, exclude=()) -> list[int]:
+    """The `count` largest primes below 2^bits that are == 1 mod 2^log_mod,
+    skipping `exclude`: the same search as lb_find_primes
+    (csrc/host_math.hpp), in pure Python so that parameter sets (and the CPU
+    reference arm of bench.py, which must not load the device library) need
+    no native code."""
+    if bits < log_mod + 2 or bits > 62:
+        raise ValueError("bad prime size")
+    step = 1 << log_mod
+    c = ((1 << bits) - 1) // step * step + 1
+    if c >= 1 << bits:
+        c -= step
+    ex = set(int(e) for e in exclude)
+    out: list[int] = []
+    while c > step and len(out) < count:
+        if c not in ex and is_prime_u64(c):
+            out.append(c)
+        c -= step
+    if len(out) < count:
+        raise ValueError("not enough primes of that shape")
+    return out
 
 # proj/src/layers.cpp:288-290 — primes == 1 mod 32768, largest first.
 SUGGESTED_PLAIN_PRIMES = [2281701377, 2149810177, 2148794369, 2148728833, 2013265921, 1004535809, 998244353]
@@ -55,7 +103,7 @@ def plain_primes(n: int, count: int) -> list[int]:
     return ok + extra
 
 
-def make_params(n: int, L: int, T: int = 1, K: int = 1, dnum: int = 0, bits: int = 60, seed: int = 1,
+def make_params(n: int, L: int, T: int = 1, K: int = 1, dnum: int = 0, bits: int = 60, seed: int | None = None,
                 plain: list[int] | None = None) -> BfvParams:
     """Ciphertext primes: the L largest `bits`-bit primes == 1 mod 2^16 (so
     one chain serves every n <= 32768); special primes and the auxiliary
@@ -69,12 +117,21 @@ def make_params(n: int, L: int, T: int = 1, K: int = 1, dnum: int = 0, bits: int
     allp = find_primes(bits, log_mod, L + K + L + extra)
     q, p, b = allp[:L], allp[L:L + K], allp[L + K:]
     t = plain if plain is not None else plain_primes(n, T)
-    return BfvParams(n=n, q=q, p=p, b=b, t=t, dnum=dnum or L, seed=seed)
+    return BfvParams(n=n, q=q, p=p, b=b, t=t, dnum=dnum or L, seed=fresh_seed() if seed is None else seed)
+
+
+def fresh_seed() -> int:
+    """Key/randomness seed from OS entropy: the default, so two contexts
+    never share a secret key. Explicit seeds are for parity tests (the CPU
+    oracle reproduces a context from its seed)."""
+    import secrets
+
+    return secrets.randbits(63) | 1
 
 
 # BASELINE.json configs --------------------------------------------------------
 
-def lola_mnist_params(seed: int = 1) -> BfvParams:
+def lola_mnist_params(seed: int | None = None) -> BfvParams:
     """Config 0/2: n = 16384, 5 plaintext primes (the runtime
     magnitude bound needs 5), L = 5 ciphertext primes of 60 bits, K = 2
     special primes, dnum = 3 digits of <= 2 primes: log2(QP) = 420 <= 438,
@@ -85,7 +142,7 @@ def lola_mnist_params(seed: int = 1) -> BfvParams:
     return make_params(16384, L=5, T=5, K=2, dnum=3, seed=seed)
 
 
-def lola_mnist_params_w32(seed: int = 1) -> BfvParams:
+def lola_mnist_params_w32(seed: int | None = None) -> BfvParams:
     """Config 0/2 on 29-bit primes (below 2^30, so every transform and key
     switch runs on 32-bit words): L = 10 ciphertext primes (Q ~ 290 bits),
     K = 5 special primes, dnum = 2 digits of 5 primes (P ~ D_j, so key
@@ -98,14 +155,14 @@ def lola_mnist_params_w32(seed: int = 1) -> BfvParams:
     return make_params(16384, L=10, T=5, K=5, dnum=2, bits=29, seed=seed)
 
 
-def lola_cifar_params(seed: int = 1) -> BfvParams:
+def lola_cifar_params(seed: int | None = None) -> BfvParams:
     """Config 4: n = 16384, 6 plaintext primes (final bound 183
     bits), L = 6 (its second window stage and 4075-value square add ~25 bits
     of noise over LoLa-MNIST), K = 1, dnum = 6: log2(QP) = 420 <= 438."""
     return make_params(16384, L=6, T=6, K=1, dnum=6, seed=seed)
 
 
-def lola_cifar_params_w32(seed: int = 1) -> BfvParams:
+def lola_cifar_params_w32(seed: int | None = None) -> BfvParams:
     """Config 4 on 29-bit primes (32-bit word kernels, u32 residues: the same
     HBM footprint per ciphertext as the 60-bit set's 6 u64 limbs): L = 11,
     K = 4, dnum = 3 digits of <= 4 primes (P ~ D_j): log2(QP) ~ 435 <= 438.
@@ -115,14 +172,14 @@ def lola_cifar_params_w32(seed: int = 1) -> BfvParams:
     return make_params(16384, L=11, T=6, K=4, dnum=3, bits=29, seed=seed)
 
 
-def lola_small_params(seed: int = 1) -> BfvParams:
+def lola_small_params(seed: int | None = None) -> BfvParams:
     """Config 3: n = 8192, 2 plaintext primes, depth 1 (one square). 54-bit
     primes so that log2(QP) = 216 <= 218, the 128-bit bound at n = 8192:
     L = 3, K = 1, dnum = 3. Measured decryption margin 29.7 bits."""
     return make_params(8192, L=3, T=2, K=1, dnum=3, bits=54, seed=seed)
 
 
-def lola_small_params_w32(seed: int = 1) -> BfvParams:
+def lola_small_params_w32(seed: int | None = None) -> BfvParams:
     """Config 3 on 30-bit primes: L = 5, K = 2, dnum = 3 digits of <= 2:
     log2(QP) = 210 <= 218. Measured decryption margin 18.4 bits (L = 6,
     K = 1, dnum = 6: 47.5 bits but 30% slower; dnum = 2 with K = 1 fails)."""

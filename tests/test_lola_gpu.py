@@ -89,3 +89,13 @@ def test_lola_cifar_config4_single_image(word):
     assert np.array_equal(counters, predicted)
     assert counters.sum(0).tolist() == [2, 8160, 15936, 4075, 81265, 53177, 4075]
     assert scores[0] == R.forward_integer(net, img[0])
+
+
+def test_lola_mnist_w32_bench_batch():
+    """Exactly the benched configuration: lola-mnist w32 (29-bit set, u32
+    residues), the config-2 network and images, batch 64 (320 ciphertexts per
+    key-switch launch). Every decrypted logit == forward_integer; counters ==
+    the reference's."""
+    from paper_1812_10659_b200.params import lola_mnist_params_w32
+
+    _check(lola_mnist_params_w32(), nets.lola_mnist_net(config=2), "lola-mnist", batch=64, config=2)

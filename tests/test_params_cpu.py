@@ -46,3 +46,17 @@ def test_prime_chain_invariants(name):
     log_b = sum(math.log2(v) for v in prm.b)
     log_q = sum(math.log2(v) for v in prm.q)
     assert log_b >= log_q + math.log2(max(prm.t)) + math.log2(prm.n) + 2
+
+
+def test_python_prime_search_matches_the_library():
+    """params.find_primes (pure Python, used by the parameter sets and the
+    reference arm) == lb_find_primes (csrc/host_math.hpp)."""
+    from paper_1812_10659_b200 import context, params
+
+    for bits, log_mod, count in ((29, 16, 24), (30, 16, 20), (54, 16, 8), (60, 16, 16), (31, 15, 6)):
+        assert params.find_primes(bits, log_mod, count) == context.find_primes(bits, log_mod, count)
+    ex = params.find_primes(60, 16, 3)
+    assert params.find_primes(60, 16, 3, exclude=ex[:2]) == context.find_primes(60, 16, 3, exclude=ex[:2])
+    from oracle import refbind as R
+
+    assert all(R.is_prime(v) for v in params.find_primes(60, 16, 4))
