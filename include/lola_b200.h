@@ -272,6 +272,12 @@ uint64_t lb_launch_count(void);
  * second (the same butterfly the NTT runs), grid = SMs x blocks_per_sm. */
 int lb_bench_butterfly_peak(uint64_t q, int blocks_per_sm, int iters, double* bfly_per_s);
 
+/* Pipe cross-check of that roof: sustained thread-level ops/s of IMAD
+ * (mad.lo.u32), IMAD.HI (mul.hi.u32), a dependent add pair (IADD3) and the
+ * min(x, x - m) conditional subtraction (VIADDMNMX), 8 independent chains
+ * per thread; ops_per_s[4]. */
+int lb_bench_int_pipes(int iters, double* ops_per_s);
+
 #ifdef __cplusplus
 }
 #endif

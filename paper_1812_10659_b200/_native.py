@@ -49,6 +49,7 @@ _SIGS: dict[str, list] = {
     "lb_ntt_forward_u32": [vp, vp, u32, u32, u32, u64, vp],
     "lb_ntt_inverse_u32": [vp, vp, u32, u32, u32, u64, vp],
     "lb_bench_butterfly_peak": [u64, C.c_int, C.c_int, C.POINTER(C.c_double)],
+    "lb_bench_int_pipes": [C.c_int, C.POINTER(C.c_double)],
     "lb_encrypt_slots": [vp, vp, u32, u64, vp, vp],
     "lb_decrypt_slots": [vp, vp, u32, vp, vp],
     "lb_decrypt_coeffs": [vp, vp, u32, vp, vp],

@@ -40,7 +40,72 @@ __global__ void __launch_bounds__(256) butterfly_peak_kernel(W q, PairT<W> w0, P
     if (acc == static_cast<W>(0x5555555555555555ull)) sink[0] = acc;
 }
 
+// Raw issue rates of the instructions a 32-bit Shoup butterfly is made of,
+// for the cross-check of the butterfly roof against the pipe limits:
+// op 0 = IMAD (mad.lo.u32), 1 = IMAD.HI (mul.hi.u32), 2 = IADD3 (3-input
+// add), 3 = VIADDMNMX (min(x, x - m)). 8 independent chains per thread.
+template <int OP>
+__global__ void __launch_bounds__(256) int_pipe_kernel(uint32_t b, uint32_t c, int iters, uint32_t* sink) {
+    uint32_t a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 2654435761u + k * 97u;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if constexpr (OP == 0) {
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+            } else if constexpr (OP == 1) {
+                asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(b));
+            } else if constexpr (OP == 2) {
+                asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+            } else {
+                a[k] = csub<uint32_t>(a[k] ^ b, c);
+            }
+        }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= a[k];
+    if (acc == 0x55555555u) sink[0] = acc;
+}
+
 }  // namespace lb
+
+extern "C" int lb_bench_int_pipes(int iters, double* ops_per_s) {
+    try {
+        int dev = 0, sms = 0;
+        LB_CUDA(cudaGetDevice(&dev));
+        LB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        uint32_t* sink = nullptr;
+        LB_CUDA(cudaMalloc(&sink, 4));
+        const int grid = sms * 8;
+        cudaEvent_t a, b;
+        LB_CUDA(cudaEventCreate(&a));
+        LB_CUDA(cudaEventCreate(&b));
+        auto run = [&](auto kernel, int it) {
+            kernel<<<grid, 256>>>(0x9E3779B9u, 0x1234567u, it / 10 + 1, sink);
+            LB_CUDA(cudaEventRecord(a));
+            kernel<<<grid, 256>>>(0x9E3779B9u, 0x1234567u, it, sink);
+            LB_CUDA(cudaEventRecord(b));
+            LB_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            LB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            return double(grid) * 256.0 * it * 8 / (ms * 1e-3);
+        };
+        ops_per_s[0] = run(lb::int_pipe_kernel<0>, iters);
+        ops_per_s[1] = run(lb::int_pipe_kernel<1>, iters);
+        // OP 2 issues two dependent adds per chain step (PTX add.u32 pairs
+        // may fuse into one IADD3): reported per chain step
+        ops_per_s[2] = run(lb::int_pipe_kernel<2>, iters);
+        ops_per_s[3] = run(lb::int_pipe_kernel<3>, iters);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(sink);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
 
 extern "C" int lb_bench_butterfly_peak(uint64_t q, int blocks_per_sm, int iters, double* bfly_per_s) {
     try {
