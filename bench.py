@@ -776,14 +776,35 @@ def run_ours(a, world, rank, local):
             torch.cuda.synchronize()
             lat.append(e0.elapsed_time(e1))
         sc1 = np.zeros((1, one.outputs, 4), dtype=np.uint64)
-        lat_e2e = []
+        lat_e2e = []  # (no graph)
         for _ in range(3):
             t0 = time.perf_counter()
             one.run_raw(np.ascontiguousarray(imgs[:1]), sc1, False, False, want_counters=False, want_times=False)
             lat_e2e.append((time.perf_counter() - t0) * 1e3)
         del one
         torch.cuda.empty_cache()
-        extras["latency_ms"] = {"he_steps": min(lat), "e2e": min(lat_e2e), "images": 1}
+        # the same with the plan replayed as one CUDA graph
+        one.set_graph(True)
+        one.encrypt(one_img, on_device=True)
+        for _ in range(3):
+            one.execute()
+        torch.cuda.synchronize()
+        lat_g = []
+        for _ in range(5):
+            e0.record(s)
+            one.execute()
+            e1.record(s)
+            torch.cuda.synchronize()
+            lat_g.append(e0.elapsed_time(e1))
+        lat_ge = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            one.run_raw(np.ascontiguousarray(imgs[:1]), sc1, False, False, want_counters=False, want_times=False)
+            lat_ge.append((time.perf_counter() - t0) * 1e3)
+        g_par = parity_check(net, imgs[:1], sc1)
+        extras["latency_ms"] = {"he_steps": min(lat_g), "e2e": min(lat_ge), "images": 1, "cuda_graph": True,
+                                "he_steps_no_graph": min(lat), "e2e_no_graph": min(lat_e2e),
+                                "graph_parity": g_par["mismatches"] == 0}
         # roofline of the dominant unit (the key switch, at a typical plan
         # launch size) and of its NTT component alone
         extras["roofline"] = ks_roofline(cx, 16 * len(prm.t))

@@ -259,6 +259,12 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
 int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int images_on_device);
 int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters);
 int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device);
+/* CUDA-graph mode (off by default). On: the next execute runs the plan once
+ * (keys, plaintext encodings), captures a second run into a graph and replays
+ * it; every later execute (and run) is one graph launch over the same input
+ * buffers (encrypt copies new ciphertexts into them). Results, counters and
+ * errors are those of the captured run. Off: frees the graph. */
+int lb_lola_session_set_graph(lb_lola_session* s, int enable);
 /* device pointer of encrypted output message `index` ([batch][T][2][L][n])
  * and the number of output messages (either pointer may be NULL) */
 int lb_lola_session_output(const lb_lola_session* s, uint32_t index, const void** data, uint32_t* count);
@@ -274,8 +280,8 @@ int lb_bench_butterfly_peak(uint64_t q, int blocks_per_sm, int iters, double* bf
 
 /* Pipe cross-check of that roof: sustained thread-level ops/s of IMAD
  * (mad.lo.u32), IMAD.HI (mul.hi.u32), a dependent add pair (IADD3) and the
- * min(x, x - m) conditional subtraction (VIADDMNMX), 8 independent chains
- * per thread; ops_per_s[4]. */
+ * min(x, x - m) conditional subtraction (VIADDMNMX), and IMAD.WIDE.U32,
+ * 8 independent chains per thread; ops_per_s[5]. */
 int lb_bench_int_pipes(int iters, double* ops_per_s);
 
 #ifdef __cplusplus

@@ -60,8 +60,10 @@ public:
             ptr_ = o.ptr_;
             bytes_ = o.bytes_;
             stream_ = o.stream_;
+            owned_ = o.owned_;
             o.ptr_ = nullptr;
             o.bytes_ = 0;
+            o.owned_ = true;
         }
         return *this;
     }
@@ -71,15 +73,23 @@ public:
     // Frees go to `s` from now on (the caller orders `s` after every use on
     // the allocating stream, e.g. through an event).
     void rebind(cudaStream_t s) { stream_ = s; }
+    // Stop owning the memory (the pointer stays valid for readers): for
+    // buffers a CUDA graph allocated, which the graph's owner frees.
+    void* disown() {
+        owned_ = false;
+        return ptr_;
+    }
+    bool owned() const { return owned_; }
 
 private:
     void release() {
-        if (ptr_) cudaFreeAsync(ptr_, stream_);
+        if (ptr_ && owned_) cudaFreeAsync(ptr_, stream_);
         ptr_ = nullptr;
     }
     void* ptr_ = nullptr;
     size_t bytes_ = 0;
     cudaStream_t stream_ = nullptr;
+    bool owned_ = true;
 };
 
 struct Params {

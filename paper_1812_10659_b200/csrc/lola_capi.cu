@@ -75,6 +75,14 @@ struct lb_lola_session {
     lb::lola::EncodedTensor input;   // encrypted input (kept by encrypt)
     lb::lola::EncodedTensor output;  // encrypted scores (kept by execute)
     std::vector<lb::lola::CounterDelta> per_step;
+    // CUDA-graph mode (lb_lola_session_set_graph): the HE steps captured once
+    // into a graph that reads `input`'s buffers and writes graph-allocated
+    // outputs (valid until the next launch), replayed by every execute
+    bool use_graph = false;
+    cudaGraphExec_t graph = nullptr;
+    uint64_t graph_kernels = 0;          // kernel launches one replay performs
+    std::vector<void*> graph_outputs;    // graph allocations the host still references
+    ~lb_lola_session();
 };
 
 namespace {
@@ -89,7 +97,23 @@ void phase_encrypt(lb_lola_session* s, const int64_t* images, int on_device) {
                                 st));
         img = dimg.get<int64_t>();
     }
-    s->input = s->plan.encode_input(*s->ev, img);
+    lb::lola::EncodedTensor fresh = s->plan.encode_input(*s->ev, img);
+    if (s->graph) {
+        // the captured graph reads the input buffers it was captured with:
+        // move the new ciphertexts into them
+        if (fresh.messages.size() != s->input.messages.size()) throw std::logic_error("input shape changed");
+        const size_t bytes = s->ecx->payload_bytes();
+        for (size_t i = 0; i < fresh.messages.size(); ++i)
+            LB_CUDA(cudaMemcpyAsync(s->input.messages[i].data(), fresh.messages[i].data(), bytes,
+                                    cudaMemcpyDeviceToDevice, st));
+        for (size_t i = 0; i < fresh.messages.size(); ++i) {
+            lb::lola::Message keep = s->input.messages[i];
+            s->input.messages[i] = std::move(fresh.messages[i]);
+            s->input.messages[i].payload = keep.payload;  // same buffers, the new depth / magnitude
+        }
+        return;
+    }
+    s->input = std::move(fresh);
 }
 
 void phase_execute(lb_lola_session* s, bool keep_input) {
@@ -100,6 +124,61 @@ void phase_execute(lb_lola_session* s, bool keep_input) {
     lb::lola::ExecutionResult res = lb::lola::execute(s->plan, std::move(in), ev);
     s->output = std::move(res.output);
     s->per_step = std::move(res.per_step);
+}
+
+void free_graph(lb_lola_session* s) {
+    cudaStream_t st = s->ecx->stream();
+    s->output = {};
+    for (void* p : s->graph_outputs) cudaFreeAsync(p, st);
+    s->graph_outputs.clear();
+    if (s->graph) {
+        cudaStreamSynchronize(st);
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+    }
+}
+
+// execute through a CUDA graph: the first call runs the steps once
+// uncaptured (key generation, plaintext encodings, side streams), then
+// captures a second run (every counted op becomes graph nodes, the side-stream
+// fan-out becomes parallel branches) and instantiates it; every call then
+// replays it with one launch. Counters are the captured run's, which the
+// plan checked step by step.
+void phase_execute_graph(lb_lola_session* s) {
+    cudaStream_t st = s->ecx->stream();
+    if (!s->graph) {
+        if (s->input.messages.empty()) throw std::invalid_argument("no encrypted input: call encrypt first");
+        phase_execute(s, true);
+        LB_CUDA(cudaDeviceSynchronize());
+        s->output = {};
+        auto& launches = lb::launch_counter();
+        const uint64_t l0 = launches.load();
+        s->ecx->set_capturing(true);
+        LB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        cudaGraph_t g = nullptr;
+        try {
+            phase_execute(s, true);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            s->ecx->set_capturing(false);
+            s->output = {};
+            throw;
+        }
+        s->ecx->set_capturing(false);
+        LB_CUDA(cudaStreamEndCapture(st, &g));
+        s->graph_kernels = launches.load() - l0;
+        launches.fetch_sub(s->graph_kernels);  // captured, not launched
+        const cudaError_t e = cudaGraphInstantiateWithFlags(&s->graph, g, cudaGraphInstantiateFlagAutoFreeOnLaunch);
+        cudaGraphDestroy(g);
+        LB_CUDA(e);
+        // the outputs live in graph allocations: AutoFreeOnLaunch frees them at
+        // the next launch, which re-creates them at the same addresses
+        for (auto& m : s->output.messages)
+            if (m.payload->buf.owned()) s->graph_outputs.push_back(m.payload->buf.disown());
+    }
+    LB_CUDA(cudaGraphLaunch(s->graph, st));
+    lb::launch_counter().fetch_add(s->graph_kernels, std::memory_order_relaxed);
 }
 
 void phase_decrypt(lb_lola_session* s, uint64_t* scores, int on_device) {
@@ -120,6 +199,13 @@ lb::lola::PlanOptions plan_options(const lb_plan_options* opt) {
 }
 
 }  // namespace
+
+lb_lola_session::~lb_lola_session() {
+    try {
+        if (ecx) free_graph(this);
+    } catch (...) {
+    }
+}
 
 extern "C" {
 
@@ -196,7 +282,10 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
         phase_encrypt(s, images, images_on_device);
         if (times) LB_CUDA(cudaStreamSynchronize(st));
         const auto t1 = clock::now();
-        phase_execute(s, false);
+        if (s->use_graph)
+            phase_execute_graph(s);
+        else
+            phase_execute(s, false);
         if (times) LB_CUDA(cudaStreamSynchronize(st));
         const auto t2 = clock::now();
         phase_decrypt(s, scores, scores_on_device);
@@ -217,9 +306,20 @@ int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int image
 
 int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters) {
     return guarded([&] {
-        phase_execute(s, true);
+        if (s->use_graph)
+            phase_execute_graph(s);
+        else
+            phase_execute(s, true);
         if (counters)
             for (size_t i = 0; i < s->per_step.size(); ++i) put_counters(s->per_step[i], counters + 7 * i);
+    });
+}
+
+int lb_lola_session_set_graph(lb_lola_session* s, int enable) {
+    return guarded([&] {
+        if (!s) throw std::invalid_argument("null session");
+        if (!enable) free_graph(s);
+        s->use_graph = enable != 0;
     });
 }
 

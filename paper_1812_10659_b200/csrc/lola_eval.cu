@@ -200,6 +200,28 @@ uint64_t hash_values(const std::vector<int64_t>& v) {
 
 }  // namespace
 
+// ---- pointer tables --------------------------------------------------------------------
+
+constexpr uint32_t kPtrChunk = 500;
+struct PtrChunk {
+    const void* p[kPtrChunk];
+};
+
+__global__ void k_put_pointers(PtrChunk c, uint32_t count, const void** dst) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) dst[i] = c.p[i];
+}
+
+void put_pointers(const void* const* host, uint64_t count, const void** dst, cudaStream_t s) {
+    for (uint64_t b = 0; b < count; b += kPtrChunk) {
+        PtrChunk c{};
+        const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(kPtrChunk, count - b));
+        std::copy(host + b, host + b + k, c.p);
+        k_put_pointers<<<(k + 127) / 128, 128, 0, s>>>(c, k, dst + b);
+        LB_KERNEL_DONE();
+    }
+}
+
 // ---- EvalContext ---------------------------------------------------------------------
 
 uint32_t EvalContext::fanout() const {
@@ -387,9 +409,12 @@ const void* Evaluator::plain(const std::vector<int64_t>& values, bool for_add) {
     auto& bucket = table[h];
     for (auto& e : bucket)
         if (e->values == values) {
-            if (e->made_on != stream_) LB_CUDA(cudaStreamWaitEvent(stream_, e->ready, 0));
+            // (entries used under graph capture were made, and synchronised,
+            // before the capture began)
+            if (e->made_on != stream_ && !cx_->capturing()) LB_CUDA(cudaStreamWaitEvent(stream_, e->ready, 0));
             return e->pt.get();
         }
+    if (cx_->capturing()) throw std::logic_error("plaintext operand first seen under graph capture");
     const uint32_t n = cx_->n();
     Context& dc = cx_->device();
     cudaStream_t s = stream_;
@@ -538,8 +563,10 @@ std::vector<Message> Evaluator::weighted_sums(const std::vector<Message>& xs, ui
     }
     cudaStream_t s = stream_;
     DeviceBuffer dx(F * 8, s), dout(rows * 8, s);
-    LB_CUDA(cudaMemcpyAsync(dx.get(), xp.data(), F * 8, cudaMemcpyHostToDevice, s));
-    LB_CUDA(cudaMemcpyAsync(dout.get(), op.data(), rows * 8, cudaMemcpyHostToDevice, s));
+    // pointer tables travel as kernel parameters (captured by value, so the
+    // sequence is also valid inside a CUDA graph)
+    put_pointers(xp.data(), F, dx.get<const void*>(), s);
+    put_pointers(const_cast<const void* const*>(op.data()), rows, dout.get<const void*>(), s);
     simd_weighted_sums(cx_->device(), reinterpret_cast<const void* const*>(dx.get()), static_cast<uint32_t>(F),
                        reinterpret_cast<void* const*>(dout.get()), static_cast<uint32_t>(rows), dev_w, small_w,
                        static_cast<uint32_t>(cx_->cts()), s);

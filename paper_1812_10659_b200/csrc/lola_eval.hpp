@@ -117,6 +117,11 @@ public:
     // LB_STREAMS (default 8) sets the count; 1 disables the fan-out.
     uint32_t fanout() const;
     cudaStream_t side_stream(uint32_t i) const;
+    // true while a session captures the plan into a CUDA graph: every op must
+    // then be stream-ordered device work (no host syncs, no pageable uploads,
+    // no waits on events recorded before the capture began)
+    bool capturing() const { return capturing_; }
+    void set_capturing(bool c) const { capturing_ = c; }
     ~EvalContext();
 
 private:
@@ -127,6 +132,7 @@ private:
     cudaStream_t stream_;
     Mag capacity_;
     mutable std::vector<cudaStream_t> side_;
+    mutable bool capturing_ = false;
 };
 
 // Shared cache of device-encoded plaintext operands keyed by value.

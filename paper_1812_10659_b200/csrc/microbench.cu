@@ -58,8 +58,12 @@ __global__ void __launch_bounds__(256) int_pipe_kernel(uint32_t b, uint32_t c, i
                 asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(b));
             } else if constexpr (OP == 2) {
                 asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
-            } else {
+            } else if constexpr (OP == 3) {
                 a[k] = csub<uint32_t>(a[k] ^ b, c);
+            } else {
+                uint64_t w;
+                asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(a[k]), "r"(b));
+                a[k] = static_cast<uint32_t>(w >> 32) ^ static_cast<uint32_t>(w);
             }
         }
     }
@@ -98,6 +102,7 @@ extern "C" int lb_bench_int_pipes(int iters, double* ops_per_s) {
         // may fuse into one IADD3): reported per chain step
         ops_per_s[2] = run(lb::int_pipe_kernel<2>, iters);
         ops_per_s[3] = run(lb::int_pipe_kernel<3>, iters);
+        ops_per_s[4] = run(lb::int_pipe_kernel<4>, iters);  // IMAD.WIDE.U32 (+ a LOP3 fold)
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         cudaFree(sink);

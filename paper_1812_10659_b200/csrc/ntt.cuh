@@ -181,19 +181,36 @@ __device__ __forceinline__ uint32_t swz_w(uint32_t y) {
     }
 }
 
+// a + b kept on the ALU pipe. The 32-bit butterflies are bound by the FMA
+// pipe (IMAD.HI issues at half the IMAD rate on B200: 32 vs 64 lanes/clk/SM,
+// tools/pipes.py), but ptxas balances pipes as if it were full rate and turns
+// 2-input adds into IMAD.IADD. A third addend it cannot see through (a zero
+// in constant memory) makes the add a 3-input IADD3, which IMAD cannot do.
+#ifndef LB_ADD_ALU
+#define LB_ADD_ALU 1
+#endif
+static __constant__ uint32_t kZero32 = 0;
+template <class W>
+__device__ __forceinline__ W add_alu(W a, W b) {
+    if constexpr (sizeof(W) == 4 && LB_ADD_ALU)
+        return a + b + kZero32;
+    else
+        return a + b;
+}
+
 // Harvey lazy CT butterfly: X, Y in [0, 4q) -> X + WY, X - WY in [0, 4q).
 template <class W, class Pr>
 __device__ __forceinline__ void ct_bfly(W& x, W& y, Pr w, W q, W two_q) {
     W xx = csub<W>(x, two_q);
     W t = shoup_lazy<W>(y, w.x, w.y, q);
-    x = xx + t;
+    x = add_alu<W>(xx, t);
     y = xx - t + two_q;
 }
 
 // Harvey lazy GS butterfly: X, Y in [0, 2q) -> X + Y, (X - Y) W in [0, 2q).
 template <class W, class Pr>
 __device__ __forceinline__ void gs_bfly(W& x, W& y, Pr w, W q, W two_q) {
-    W s = x + y;
+    W s = add_alu<W>(x, y);
     s = csub<W>(s, two_q);
     W d = x - y + two_q;
     x = s;
@@ -378,13 +395,25 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t m, uint32_t tx) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(m), "r"(tx)
                  : "memory");
 }
+#ifndef LB_MBAR_HINT
+#define LB_MBAR_HINT 0  // try_wait suspend-time hint in ns (0 = the hardware default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t parity) {
+#if LB_MBAR_HINT
+    asm volatile(
+        "{\n .reg .pred p;\n LB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra LB_WAIT_%=;\n}\n" ::"r"(m),
+        "r"(parity), "n"(LB_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\n LB_WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra LB_WAIT_%=;\n}\n" ::"r"(m),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // Bulk L2 prefetch by the TMA unit (one instruction for a whole range):
@@ -597,7 +626,7 @@ __device__ __forceinline__ void inv_final(W (&r)[kE], const PairT<W>* __restrict
 #pragma unroll
     for (int k = 0; k < half0; ++k) {
         W x = r[k], y = r[k + half0];
-        W s = x + y;  // < 4q
+        W s = add_alu<W>(x, y);  // < 4q
         W d = x - y + two_q;
         r[k] = shoup_full<W>(s, c0.x, c0.y, q);
         r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);

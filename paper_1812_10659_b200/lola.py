@@ -59,6 +59,7 @@ _SIGS = {
     "lb_lola_session_encrypt": [vp, vp, C.c_int],
     "lb_lola_session_execute": [vp, C.POINTER(C.c_uint64)],
     "lb_lola_session_decrypt": [vp, vp, C.c_int],
+    "lb_lola_session_set_graph": [vp, C.c_int],
     "lb_lola_session_output": [vp, C.c_uint32, C.POINTER(vp), C.POINTER(C.c_uint32)],
 }
 nat.register(_SIGS)
@@ -127,6 +128,10 @@ class Session:
         steps, outs, ins = C.c_uint32(), C.c_uint64(), C.c_uint64()
         nat.call("lb_lola_session_info", h, C.byref(steps), C.byref(outs), C.byref(ins))
         self.steps, self.outputs, self.input_values = steps.value, outs.value, ins.value
+
+    def set_graph(self, enable: bool = True) -> None:
+        """CUDA-graph mode: execute captures the plan once and replays it."""
+        nat.call("lb_lola_session_set_graph", self.handle, int(enable))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -99,3 +99,37 @@ def test_lola_mnist_w32_bench_batch():
     from paper_1812_10659_b200.params import lola_mnist_params_w32
 
     _check(lola_mnist_params_w32(), nets.lola_mnist_net(config=2), "lola-mnist", batch=64, config=2)
+
+
+@pytest.mark.parametrize("which", ["toy", "mnist_w32"])
+def test_cuda_graph_replay_matches(which):
+    """Graph mode (lb_lola_session_set_graph): the captured plan replayed for
+    new images (encrypt copies them into the captured input buffers) gives
+    the same logits and counters as the direct path and forward_integer."""
+    from paper_1812_10659_b200.params import lola_mnist_params_w32
+
+    if which == "toy":
+        prm, net, cfg, B = make_params(4096, L=7, T=3, K=1, seed=5), nets.toy_net(), 9, 2
+    else:
+        prm, net, cfg, B = lola_mnist_params_w32(), nets.lola_mnist_net(config=2), 2, 1
+    cx = BfvContext(prm)
+    sess = Session(cx, net, "lola-mnist", B)
+    sess.set_graph(True)
+    for start in (0, 5, 11):
+        imgs = nets.images(cfg, net, B, start=start)
+        scores, counters, _ = sess.run(imgs)
+        for b in range(B):
+            assert scores[b] == R.forward_integer(net, imgs[b]), f"images from {start}, image {b}"
+    predicted, _, _ = __import__("paper_1812_10659_b200.lola", fromlist=["plan_counters"]).plan_counters(
+        net, "lola-mnist", prm.n)
+    assert np.array_equal(counters, predicted)
+    # separate phases: encrypt once, replay execute several times
+    imgs = nets.images(cfg, net, B, start=20)
+    sess.encrypt(imgs)
+    for _ in range(3):
+        sess.execute()
+    assert sess.decrypt() == [R.forward_integer(net, x) for x in imgs]
+    sess.set_graph(False)
+    sess.encrypt(imgs)
+    sess.execute()
+    assert sess.decrypt() == [R.forward_integer(net, x) for x in imgs]
