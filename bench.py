@@ -781,8 +781,6 @@ def run_ours(a, world, rank, local):
             t0 = time.perf_counter()
             one.run_raw(np.ascontiguousarray(imgs[:1]), sc1, False, False, want_counters=False, want_times=False)
             lat_e2e.append((time.perf_counter() - t0) * 1e3)
-        del one
-        torch.cuda.empty_cache()
         # the same with the plan replayed as one CUDA graph
         one.set_graph(True)
         one.encrypt(one_img, on_device=True)
@@ -805,6 +803,8 @@ def run_ours(a, world, rank, local):
         extras["latency_ms"] = {"he_steps": min(lat_g), "e2e": min(lat_ge), "images": 1, "cuda_graph": True,
                                 "he_steps_no_graph": min(lat), "e2e_no_graph": min(lat_e2e),
                                 "graph_parity": g_par["mismatches"] == 0}
+        del one
+        torch.cuda.empty_cache()
         # roofline of the dominant unit (the key switch, at a typical plan
         # launch size) and of its NTT component alone
         extras["roofline"] = ks_roofline(cx, 16 * len(prm.t))

@@ -78,6 +78,11 @@ struct lb_lola_session {
     // CUDA-graph mode (lb_lola_session_set_graph): the HE steps captured once
     // into a graph that reads `input`'s buffers and writes graph-allocated
     // outputs (valid until the next launch), replayed by every execute
+    // the session's ops run on its own non-blocking stream (a graph cannot
+    // capture the legacy default stream); every entry point orders it after
+    // the caller's stream on entry and the caller's stream after it on exit
+    cudaStream_t caller = nullptr, own = nullptr;
+    cudaEvent_t in_ev = nullptr, out_ev = nullptr;
     bool use_graph = false;
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_kernels = 0;          // kernel launches one replay performs
@@ -205,7 +210,34 @@ lb_lola_session::~lb_lola_session() {
         if (ecx) free_graph(this);
     } catch (...) {
     }
+    output = {};
+    input = {};
+    ev.reset();
+    ecx.reset();
+    plan = lb::lola::Plan{};  // cached device operands are freed on `own`
+    if (own) {
+        cudaStreamSynchronize(own);
+        cudaStreamDestroy(own);
+    }
+    if (in_ev) cudaEventDestroy(in_ev);
+    if (out_ev) cudaEventDestroy(out_ev);
 }
+
+namespace {
+
+// caller's stream -> session stream on entry, session stream -> caller's on exit
+struct StreamBridge {
+    lb_lola_session* s;
+    explicit StreamBridge(lb_lola_session* ss) : s(ss) {
+        LB_CUDA(cudaEventRecord(s->in_ev, s->caller));
+        LB_CUDA(cudaStreamWaitEvent(s->own, s->in_ev, 0));
+    }
+    ~StreamBridge() {
+        if (cudaEventRecord(s->out_ev, s->own) == cudaSuccess) cudaStreamWaitEvent(s->caller, s->out_ev, 0);
+    }
+};
+
+}  // namespace
 
 extern "C" {
 
@@ -248,8 +280,11 @@ int lb_lola_session_create_ex(lb_context* cx, const lb_network* net, const char*
         const bool records = strat == lb::lola::Strategy::CryptonetsSimd;
         if (records && (batch == 0 || batch > cx->cx.n()))
             throw std::invalid_argument("cryptonets-simd packs at most n images per session");
-        s->ecx = std::make_unique<lb::lola::EvalContext>(cx->cx, records ? 1 : batch, max_depth,
-                                                         static_cast<cudaStream_t>(stream));
+        s->caller = static_cast<cudaStream_t>(stream);
+        LB_CUDA(cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking));
+        LB_CUDA(cudaEventCreateWithFlags(&s->in_ev, cudaEventDisableTiming));
+        LB_CUDA(cudaEventCreateWithFlags(&s->out_ev, cudaEventDisableTiming));
+        s->ecx = std::make_unique<lb::lola::EvalContext>(cx->cx, records ? 1 : batch, max_depth, s->own);
         if (records) s->ecx->set_records(batch);
         s->ev = std::make_unique<lb::lola::Evaluator>(*s->ecx);
         s->batch = batch;
@@ -277,6 +312,7 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
                         int scores_on_device, uint64_t* counters, double* times) {
     return guarded([&] {
         using clock = std::chrono::steady_clock;
+        StreamBridge bridge(s);
         cudaStream_t st = s->ecx->stream();
         const auto t0 = clock::now();
         phase_encrypt(s, images, images_on_device);
@@ -301,11 +337,15 @@ int lb_lola_session_run(lb_lola_session* s, const int64_t* images, int images_on
 }
 
 int lb_lola_session_encrypt(lb_lola_session* s, const int64_t* images, int images_on_device) {
-    return guarded([&] { phase_encrypt(s, images, images_on_device); });
+    return guarded([&] {
+        StreamBridge bridge(s);
+        phase_encrypt(s, images, images_on_device);
+    });
 }
 
 int lb_lola_session_execute(lb_lola_session* s, uint64_t* counters) {
     return guarded([&] {
+        StreamBridge bridge(s);
         if (s->use_graph)
             phase_execute_graph(s);
         else
@@ -324,7 +364,10 @@ int lb_lola_session_set_graph(lb_lola_session* s, int enable) {
 }
 
 int lb_lola_session_decrypt(lb_lola_session* s, uint64_t* scores, int scores_on_device) {
-    return guarded([&] { phase_decrypt(s, scores, scores_on_device); });
+    return guarded([&] {
+        StreamBridge bridge(s);
+        phase_decrypt(s, scores, scores_on_device);
+    });
 }
 
 uint64_t lb_launch_count(void) { return lb::launch_counter().load(); }
