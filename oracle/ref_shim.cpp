@@ -65,6 +65,17 @@ int copy_string(const std::string& s, char* out, uint64_t cap) {
     return 0;
 }
 
+// backend: 0 slot, 1 ring (the reference's two), 2 = the B200 drop-in
+// (oracle/b200_dropin/evaluator_b200.cpp), present only in libpackb200.so
+extern "C" int pb2_available(void) __attribute__((weak));
+BackendKind backend_kind(int backend) {
+    if (backend == 2) {
+        if (!pb2_available) throw std::invalid_argument("the b200 backend is not linked into this library");
+        return static_cast<BackendKind>(2);
+    }
+    return backend ? BackendKind::Ring : BackendKind::Slot;
+}
+
 std::string join_bigints(const std::vector<BigInt>& v) {
     std::string s;
     for (size_t i = 0; i < v.size(); ++i) {
@@ -265,7 +276,7 @@ int pref_schoolbook_mul(uint64_t p, uint32_t n, const uint64_t* a, const uint64_
 int pref_eval_rotate(uint64_t p, uint32_t n, int backend, const int64_t* values, int64_t k,
                      int rows, int64_t* out) {
     return guarded([&] {
-        EvalContext cx(backend ? BackendKind::Ring : BackendKind::Slot, n, {p});
+        EvalContext cx(backend_kind(backend), n, {p});
         Evaluator ev(cx);
         Message m = ev.lift(std::span<const int64_t>(values, n));
         Message r = rows ? ev.rotate_rows(m) : ev.rotate_columns(m, k);
@@ -431,7 +442,7 @@ int pref_run_plan(const pref_net* net, const char* strategy, uint32_t n, const u
         set_kernel_threads(threads);
         QuantizedNetwork q = make_network(net);
         std::vector<int64_t> xv(x, x + q.input.values());
-        EvalContext cx(backend ? BackendKind::Ring : BackendKind::Slot, n,
+        EvalContext cx(backend_kind(backend), n,
                        std::vector<uint64_t>(primes, primes + nprimes));
         Evaluator ev(cx);
         std::vector<BigInt> scores;
@@ -476,7 +487,7 @@ int pref_time_plan_steps(const pref_net* net, const char* strategy, uint32_t n, 
         set_kernel_threads(threads);
         QuantizedNetwork q = make_network(net);
         std::vector<int64_t> xv(x, x + q.input.values());
-        EvalContext cx(backend ? BackendKind::Ring : BackendKind::Slot, n,
+        EvalContext cx(backend_kind(backend), n,
                        std::vector<uint64_t>(primes, primes + nprimes));
         Evaluator ev(cx);
         if (strategy_is_small(strategy)) {
@@ -531,7 +542,7 @@ int pref_session_create(const pref_net* net, const char* strategy, uint32_t n, c
                         uint32_t nprimes, int backend, uint32_t threads, pref_session** out) {
     return guarded([&] {
         set_kernel_threads(threads);
-        *out = new pref_session(make_network(net), backend ? BackendKind::Ring : BackendKind::Slot, n,
+        *out = new pref_session(make_network(net), backend_kind(backend), n,
                                 std::vector<uint64_t>(primes, primes + nprimes), strategy_is_small(strategy),
                                 strategy);
     });

@@ -70,28 +70,69 @@ _SIGS = {
 }
 
 _lib = None
+# the drop-in proof: the reference's unmodified plan/kernels/representations
+# over the B200 evaluator (oracle/b200_dropin/evaluator_b200.cpp)
+DROPIN_LIB = HERE / "_ref" / "libpackb200.so"
+_dropin = None
 
 
 def available() -> bool:
     return REF_LIB.exists()
 
 
+def _load(path: Path):
+    if not path.exists():
+        raise RefError(-1, f"{path} not built (make -C oracle)")
+    l = C.CDLL(str(path))
+    l.pref_last_error.restype = C.c_char_p
+    l.pref_galois_exponent_rows.restype = u64
+    l.pref_galois_exponent_rows.argtypes = [u32]
+    l.pref_is_prime.argtypes = [u64]
+    for name, args in _SIGS.items():
+        f = getattr(l, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    return l
+
+
 def lib():
     global _lib
     if _lib is None:
-        if not REF_LIB.exists():
-            raise RefError(-1, f"{REF_LIB} not built (make -C oracle)")
-        l = C.CDLL(str(REF_LIB))
-        l.pref_last_error.restype = C.c_char_p
-        l.pref_galois_exponent_rows.restype = u64
-        l.pref_galois_exponent_rows.argtypes = [u32]
-        l.pref_is_prime.argtypes = [u64]
-        for name, args in _SIGS.items():
-            f = getattr(l, name)
-            f.argtypes = args
-            f.restype = C.c_int
-        _lib = l
+        _lib = _load(REF_LIB)
     return _lib
+
+
+def dropin_lib():
+    global _dropin
+    if _dropin is None:
+        l = _load(DROPIN_LIB)
+        l.pb2_set_params.argtypes = [P64, u32, P64, u32, P64, u32, u32, u64]
+        l.pb2_set_params.restype = C.c_int
+        _dropin = l
+    return _dropin
+
+
+def run_plan_b200(net, strategy: str, prm, x):
+    """The reference's own plan (build_plan + encode_input + execute +
+    decode, proj/src/plan.cpp:582-633) on the B200 evaluator backend
+    (BackendKind 2) with BFV parameters `prm`. Returns (scores, per-step
+    counters)."""
+    l = dropin_lib()
+    q, pp, b = _arr(prm.q), _arr(prm.p), _arr(prm.b)
+    l.pb2_set_params(_u64(q), q.size, _u64(pp), pp.size, _u64(b), b.size, prm.dnum, prm.seed)
+    h = NetHandle(net)
+    t = _arr(prm.t)
+    xv = np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+    buf = C.create_string_buffer(1 << 22)
+    counters = np.zeros(7 * 64, dtype=np.uint64)
+    steps = C.c_uint32()
+    times = np.zeros(3, dtype=np.float64)
+    rc = l.pref_run_plan(h.ptr(), strategy.encode(), prm.n, _u64(t), t.size, 2, 1, xv.ctypes.data_as(PI64), buf,
+                         1 << 22, _u64(counters), 64, C.byref(steps), times.ctypes.data_as(PF64))
+    if rc:
+        raise RefError(rc, l.pref_last_error().decode())
+    scores = [int(v) for v in buf.value.decode().split(",")]
+    return scores, counters[: 7 * steps.value].reshape(-1, 7).astype(np.int64)
 
 
 def _check(rc: int) -> None:
