@@ -422,6 +422,20 @@ const void* Evaluator::plain(const std::vector<int64_t>& values, bool for_add) {
     std::copy(values.begin(), values.end(), full.begin());
     DeviceBuffer dv(uint64_t(n) * 8, s);
     LB_CUDA(cudaMemcpyAsync(dv.get(), full.data(), uint64_t(n) * 8, cudaMemcpyHostToDevice, s));
+    const size_t pt_bytes = uint64_t(dc.T()) * dc.L() * n * residue_bytes(dc.bfv()->dev);
+    static const size_t budget = [] {
+        const char* e = std::getenv("LB_PLAIN_CACHE_GB");
+        return static_cast<size_t>((e ? std::atof(e) : 8.0) * (1ull << 30));
+    }();
+    if (cache_->bytes + pt_bytes > budget) {
+        DeviceBuffer t(pt_bytes, s);
+        encode_plain(dc, dv.get<int64_t>(), for_add ? nullptr : t.get(), for_add ? t.get() : nullptr, s);
+        const void* p = t.get();
+        cache_->transient.push_back(std::move(t));
+        while (cache_->transient.size() > 4) cache_->transient.pop_front();
+        return p;
+    }
+    cache_->bytes += pt_bytes;
     auto e = std::make_unique<PlainCache::Entry>();
     e->values = values;
     e->pt = DeviceBuffer(uint64_t(dc.T()) * dc.L() * n * residue_bytes(dc.bfv()->dev), s);

@@ -13,6 +13,7 @@
 
 #include <array>
 #include <cstdint>
+#include <deque>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -147,6 +148,14 @@ struct PlainCache {
         }
     };
     std::unordered_map<uint64_t, std::vector<std::unique_ptr<Entry>>> mul, add;
+    // Device bytes held by entries. Above the budget (LB_PLAIN_CACHE_GB,
+    // default 8) new operands are encoded into transient buffers instead:
+    // lola-cifar's 8,160 weight rows and 4,075 masks would otherwise pin
+    // ~53 GB, which is what bounds its batch. A transient is freed once a
+    // few newer ones exist: every op enqueues its kernel before the next
+    // plain() call, so the stream-ordered free follows its last use.
+    size_t bytes = 0;
+    std::deque<DeviceBuffer> transient;
 };
 
 class Evaluator {

@@ -23,7 +23,7 @@ def _ensure_oracles() -> None:
     ref = ROOT / "oracle" / "_ref"
     need = [ref / "libbfvoracle.so"]
     if Path("/root/reference/proj/src").exists():
-        need.append(ref / "libpackref.so")
+        need += [ref / "libpackref.so", ref / "libpackb200.so"]
     if all(p.exists() for p in need):
         return
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "-j8"], check=True)
