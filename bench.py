@@ -31,7 +31,7 @@ UNIT = "inferences/s"
 WORKLOADS = {
     "lola-mnist": (2, "lola-mnist", 64),
     "lola-small": (3, "lola-small", 256),
-    "lola-cifar": (4, "lola-cifar", 1),
+    "lola-cifar": (4, "lola-cifar", 2),  # 4,075 live messages x 35 GB per image: B=2 fits 180 GB (B=4 does not)
     # the CryptoNets baseline representation of the paper's comparison: the
     # cfg0 net with one message per value and the images in the slots
     # (n = 16384 images per step); not a BASELINE config
