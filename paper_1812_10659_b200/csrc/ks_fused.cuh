@@ -456,6 +456,79 @@ struct ModDownArgs {
 #endif
 template <class W> constexpr int moddown_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_MODDOWN32_MINB; }
 
+#ifndef LB_MD_PREFETCH
+#define LB_MD_PREFETCH 0  // 1: measured no gain (156.0 vs 156.4 images/s; 48 registers spill 60 bytes)
+#endif
+
+// ModDown's epilogue on one last-pass group of C consecutive evaluations:
+// out = (acc_q - conv) P^-1 + sigma_g(add) + sum.
+template <int LOGN, class W>
+struct MdEpilogue {
+    static constexpr int C = 1 << fwd_last_radix<LOGN>();
+    const W* accq;
+    const W* add;
+    const W* sum;
+    W* out;
+    uint32_t cta_base;
+    uint64_t galois;
+    PairT<W> pinv;
+    W q;
+    struct Ops {
+        W va[C], vb[C], vs[C];
+    };
+    __device__ __forceinline__ Ops prefetch(uint32_t base) const {
+        Ops o;
+        const uint32_t x0 = cta_base + base;
+        if constexpr (sizeof(W) == 4 && C == 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(accq + x0));
+            o.va[0] = v.x; o.va[1] = v.y; o.va[2] = v.z; o.va[3] = v.w;
+            const uint4 t = sum ? __ldg(reinterpret_cast<const uint4*>(sum + x0)) : make_uint4(0, 0, 0, 0);
+            o.vs[0] = t.x; o.vs[1] = t.y; o.vs[2] = t.z; o.vs[3] = t.w;
+        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {  // u64 pairs as 16-byte loads
+#pragma unroll
+            for (int k = 0; k < C; k += 2) {
+                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(accq + x0 + k));
+                o.va[k] = v.x;
+                o.va[k + 1] = v.y;
+                const ulonglong2 t = sum ? __ldg(reinterpret_cast<const ulonglong2*>(sum + x0 + k)) : make_ulonglong2(0, 0);
+                o.vs[k] = t.x;
+                o.vs[k + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                o.va[k] = __ldg(&accq[x0 + k]);
+                o.vs[k] = sum ? __ldg(&sum[x0 + k]) : 0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            o.vb[k] = add ? __ldg(&add[galois ? galois_src(x0 + k, galois, LOGN) : x0 + k]) : 0;
+        return o;
+    }
+    __device__ __forceinline__ void finish(uint32_t base, const W (&rr)[C], const Ops& o) const {
+        const uint32_t x0 = cta_base + base;
+        const W two_q = 2 * q;
+        W u[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const W conv = reduce_4q<W>(rr[k], q, two_q);
+            W v = shoup_full<W>(o.va[k] + q - conv, pinv.x, pinv.y, q);
+            v = csub<W>(v + o.vb[k], q);
+            u[k] = csub<W>(v + o.vs[k], q);
+        }
+        if constexpr (sizeof(W) == 4 && C == 4) {
+            *reinterpret_cast<uint4*>(out + x0) = make_uint4(u[0], u[1], u[2], u[3]);
+        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {
+#pragma unroll
+            for (int k = 0; k < C; k += 2) *reinterpret_cast<ulonglong2*>(out + x0 + k) = make_ulonglong2(u[k], u[k + 1]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k) out[x0 + k] = u[k];
+        }
+    }
+};
+
 template <int LOGN, class W>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
@@ -484,55 +557,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
 #if LB_MODDOWN_DIRECT
     // epilogue on the transform's last-pass groups (consecutive evaluations,
     // in registers): 16-byte loads of the Q accumulator and the second
-    // addend and 16-byte stores of the result for radix-4 groups of u32
+    // addend and 16-byte stores of the result for radix-4 groups of u32;
+    // with LB_MD_PREFETCH the next group's operands are in flight during the
+    // current group's butterflies
+    MdEpilogue<LOGN, W> ep{accq, add, sum, out, cta_base, a.add_galois, pinv, q};
+#if LB_MD_PREFETCH
+    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, ep);
+#else
     fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc,
-                      [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) {
-        constexpr int C = 1 << fwd_last_radix<LOGN>();
-        const uint32_t x0 = cta_base + base;
-        W va[C], vb[C], vs[C];
-        if constexpr (sizeof(W) == 4 && C == 4) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(accq + x0));
-            va[0] = v.x; va[1] = v.y; va[2] = v.z; va[3] = v.w;
-            const uint4 t = sum ? __ldg(reinterpret_cast<const uint4*>(sum + x0)) : make_uint4(0, 0, 0, 0);
-            vs[0] = t.x; vs[1] = t.y; vs[2] = t.z; vs[3] = t.w;
-        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {  // u64 pairs as 16-byte loads
-#pragma unroll
-            for (int k = 0; k < C; k += 2) {
-                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(accq + x0 + k));
-                va[k] = v.x;
-                va[k + 1] = v.y;
-                const ulonglong2 t = sum ? __ldg(reinterpret_cast<const ulonglong2*>(sum + x0 + k)) : make_ulonglong2(0, 0);
-                vs[k] = t.x;
-                vs[k + 1] = t.y;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                va[k] = __ldg(&accq[x0 + k]);
-                vs[k] = sum ? __ldg(&sum[x0 + k]) : 0;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < C; ++k)
-            vb[k] = add ? __ldg(&add[a.add_galois ? galois_src(x0 + k, a.add_galois, LOGN) : x0 + k]) : 0;
-        W u[C];
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            const W conv = reduce_4q<W>(rr[k], q, two_q);
-            W v = shoup_full<W>(va[k] + q - conv, pinv.x, pinv.y, q);
-            v = csub<W>(v + vb[k], q);
-            u[k] = csub<W>(v + vs[k], q);
-        }
-        if constexpr (sizeof(W) == 4 && C == 4) {
-            *reinterpret_cast<uint4*>(out + x0) = make_uint4(u[0], u[1], u[2], u[3]);
-        } else if constexpr (sizeof(W) == 8 && C % 2 == 0) {
-#pragma unroll
-            for (int k = 0; k < C; k += 2) *reinterpret_cast<ulonglong2*>(out + x0 + k) = make_ulonglong2(u[k], u[k + 1]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < C; ++k) out[x0 + k] = u[k];
-        }
-    });
+                      [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { ep.finish(base, rr, ep.prefetch(base)); });
+#endif
 #else
     fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
     const uint32_t sbt = swb<W>(threadIdx.x);

@@ -469,22 +469,50 @@ __device__ __forceinline__ Xchg xchg_init(uint64_t* mbar, int count) {
 template <int LOGN>
 constexpr int fwd_last_radix() { return (LOGN % kLogE) == 0 ? kLogE : LOGN % kLogE; }
 
+// An epilogue object with prefetch(base) -> Ops and finish(base, r, ops)
+// gets its global operands for group i + 1 issued before group i's
+// butterflies (one group of software pipelining), so their latency overlaps
+// compute instead of stalling the epilogue; a plain callable last(base, r)
+// loads on use.
+template <class T, class = void>
+struct has_prefetch : std::false_type {};
+template <class T>
+struct has_prefetch<T, std::void_t<decltype(&std::decay_t<T>::prefetch)>> : std::true_type {};
+
 template <int LOGN, class W, class Last>
 __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t cta_base, W q,
                                               W two_q, Last&& last) {
     constexpr int C = fwd_last_radix<LOGN>();
     constexpr int G = kE >> C;
     constexpr uint32_t s0 = LOGN - C;
+    if constexpr (has_prefetch<Last>::value) {
+        auto ops = last.prefetch(threadIdx.x << C);
 #pragma unroll
-    for (int i = 0; i < G; ++i) {
-        const uint32_t g = threadIdx.x + i * kThreads;
-        const uint32_t base = g << C;
-        const uint32_t sb = swb<W>(base);
-        W r[1 << C];
+        for (int i = 0; i < G; ++i) {
+            const uint32_t g = threadIdx.x + i * kThreads;
+            const uint32_t base = g << C;
+            decltype(ops) nxt = ops;
+            if (i + 1 < G) nxt = last.prefetch((g + kThreads) << C);
+            const uint32_t sb = swb<W>(base);
+            W r[1 << C];
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
-        fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
-        last(base, r);
+            for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
+            fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
+            last.finish(base, r, ops);
+            ops = nxt;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const uint32_t g = threadIdx.x + i * kThreads;
+            const uint32_t base = g << C;
+            const uint32_t sb = swb<W>(base);
+            W r[1 << C];
+#pragma unroll
+            for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
+            fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
+            last(base, r);
+        }
     }
 }
 
