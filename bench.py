@@ -359,6 +359,27 @@ def butterfly_peak(q: int) -> float:
     return peak.value / 1e9
 
 
+_PIPES = {}
+
+
+def pipe_check() -> dict:
+    """Cross-check of the butterfly roof against the FMA-pipe limit: measured
+    IMAD and IMAD.HI issue rates (lb_bench_int_pipes); a 32-bit Shoup
+    butterfly needs one IMAD.HI and two IMADs on that pipe."""
+    import ctypes as C
+
+    from paper_1812_10659_b200 import _native as nat
+
+    if not _PIPES:
+        ops = (C.c_double * 5)()
+        nat.call("lb_bench_int_pipes", 20000, ops)
+        imad, imad_hi = ops[0] / 1e9, ops[1] / 1e9
+        bound = 1.0 / (1.0 / imad_hi + 2.0 / imad)
+        _PIPES.update({"imad_gops": imad, "imad_hi_gops": imad_hi, "imad_wide_gops": ops[4] / 1e9,
+                       "fma_pipe_bound_gbfly_s_u32": bound})
+    return dict(_PIPES)
+
+
 def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
     """The hot path's NTT alone: the u32-storage forward and inverse limb
     transforms (ntt_forward_kernel / ntt_inverse_kernel<LOGN, u32, u32>, the
@@ -486,6 +507,7 @@ def ks_roofline(cx, count: int, reps: int = 10) -> dict:
         "bound": "int", "achieved": achieved, "peak": peak_g, "unit": "G Shoup products/s",
         "frac": achieved / peak_g,
         "peak_source": "measured live: register-resident Shoup butterfly microbenchmark (lb_bench_butterfly_peak)",
+        "peak_cross_check": pipe_check() if word == 32 else None,
         "traffic": per_ct * count if per_ct else None,
         "traffic_unit": "bytes per launch set (DRAM read + write)",
         "traffic_source": src,
@@ -555,12 +577,19 @@ def value_w64(a, net, strategy, B, imgs) -> dict:
     scores = np.zeros((B, sess.outputs, 4), dtype=np.uint64)
     sess.run_raw(np.ascontiguousarray(imgs), scores, False, False, want_counters=False, want_times=False)
     par = parity_check(net, imgs, scores)
-    del sess, cx
+    del sess
+    torch.cuda.empty_cache()
+    ks = ks_roofline(cx, 16 * len(prm.t))
+    ntt = ntt_roofline(cx, B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1))
+    del cx
     torch.cuda.empty_cache()
     return {"value": B * steps / sec, "unit": UNIT, "ms_per_step": sec / steps * 1e3, "steps": steps,
             "images_per_step": B, "dtype": "u64", "q_bits": max(prm.q).bit_length(), "L": prm.L, "K": prm.K,
             "dnum": prm.dnum, "parity": par,
-            "butterfly_peak_gbfly_s": butterfly_peak(prm.q[0])}
+            "roofline": {k: ks[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac", "launch_set_ms",
+                                             "algorithmic")},
+            "roofline_ntt": {k: ntt[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac",
+                                                 "frac_forward", "frac_inverse", "hbm_view")}}
 
 
 # BASELINE config 1 grid of the bench's primitive leg: (n, L, K, dnum, bits)
