@@ -32,6 +32,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -70,6 +71,26 @@ std::map<const EvalContext*, Backend> g_backends;
 }
 void ok(int status) {
     if (status) raise(status);
+}
+
+// Ciphertext parameters when the caller (e.g. the CLI) set none: the
+// repo's parameter sets by degree (paper_1812_10659_b200/params.py) —
+// n >= 16384: 29-bit L=10, K=5, dnum=2 (lola-mnist); n = 8192: 30-bit L=5,
+// K=2, dnum=3 (lola-small); smaller: 60-bit L=7, K=1, one prime per digit —
+// with the auxiliary base of the exact tensor product next in the chain.
+void default_params(uint32_t n) {
+    uint32_t bits = 60, L = 7, K = 1, dnum = 7;
+    if (n >= 16384) bits = 29, L = 10, K = 5, dnum = 2;
+    else if (n == 8192) bits = 30, L = 5, K = 2, dnum = 3;
+    const uint32_t M = L + (bits >= 59 ? 1 : 2);
+    std::vector<uint64_t> all(L + K + M);
+    ok(lb_find_primes(bits, 16, L + K + M, nullptr, 0, all.data()));
+    g_params.q.assign(all.begin(), all.begin() + L);
+    g_params.p.assign(all.begin() + L, all.begin() + L + K);
+    g_params.b.assign(all.begin() + L + K, all.end());
+    g_params.dnum = dnum;
+    std::random_device rd;
+    g_params.seed = ((uint64_t(rd()) << 32) | rd()) | 1;
 }
 
 Backend& backend(const EvalContext* cx) {
@@ -161,7 +182,7 @@ const char* backend_name(BackendKind k) {
 }
 
 BackendKind backend_from_name(const std::string& s) {
-    if (s == "b200") return kB200;
+    if (s == "b200" || s == "gpu") return kB200;
     throw std::invalid_argument("this build carries only the b200 backend: " + s);
 }
 
@@ -175,7 +196,7 @@ EvalContext::EvalContext(BackendKind kind, uint32_t n, const std::vector<uint64_
       corrupt_rotation_(corrupt_rotation) {
     if (kind != kB200) throw std::invalid_argument("this build carries only the b200 backend");
     if (corrupt_rotation) throw std::invalid_argument("the b200 backend has no corrupt_rotation hook");
-    if (g_params.q.empty()) throw std::invalid_argument("pb2_set_params: no ciphertext parameters");
+    if (g_params.q.empty()) default_params(n);
     lb_params prm{};
     prm.n = n;
     prm.num_q = static_cast<uint32_t>(g_params.q.size());
