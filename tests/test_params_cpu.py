@@ -60,3 +60,11 @@ def test_python_prime_search_matches_the_library():
     from oracle import refbind as R
 
     assert all(R.is_prime(v) for v in params.find_primes(60, 16, 4))
+
+
+def test_default_seeds_are_fresh():
+    from paper_1812_10659_b200 import params
+
+    seeds = {params.lola_mnist_params_w32().seed for _ in range(4)}
+    assert len(seeds) == 4 and all(s % 2 == 1 and s < 2**63 for s in seeds)
+    assert params.make_params(4096, L=2, seed=5).seed == 5
