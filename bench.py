@@ -276,6 +276,23 @@ class RefPool:
         self.pool.join()
 
 
+def cpu_reference_latency(workload: str, word: int, threads: int, images: int = 2) -> float:
+    """The reference's single-image latency with `threads` kernel threads
+    (--threads, proj/src/kernels.cpp:161-195: matvec_rowmajor's row fan-out),
+    encode + every plan step, best of `images` runs; seconds."""
+    from oracle import refbind as R
+    from paper_1812_10659_b200 import nets
+
+    cfg, strategy, _, net, prm = workload_objects(workload, word)
+    rs = R.RefSession(net, strategy, prm.n, prm.t, ring=True, threads=threads)
+    x = nets.images(cfg, net, 1)[0]
+    best = float("inf")
+    for _ in range(images):
+        _, t = rs.run(x)
+        best = min(best, float(t[0] + t[1]))
+    return best
+
+
 def cpu_reference_single(workload: str, word: int, images: int) -> tuple[float, float]:
     """One thread, this process: (images/s, seconds) over `images` images."""
     _ref_init(workload, word)
@@ -857,6 +874,13 @@ def run_ours(a, world, rank, local):
                               f"semantics, no encryption), network/EvalContext/plan built once, per image "
                               f"encode + every plan step, decode excluded; {sec:.1f} s"}
             extras["cpu_baseline_bfv"] = cpu_bfv_baseline(prm, ks_per_image)
+            if R.available():
+                cores = host_cores()
+                extras["cpu_latency_ms"] = {
+                    "threads_1": cpu_reference_latency(a.workload, a.word, 1) * 1e3,
+                    f"threads_{cores}": cpu_reference_latency(a.workload, a.word, cores) * 1e3,
+                    "what": "reference ring backend, one image, encode + every plan step, --threads 1 and "
+                            "--threads $(nproc) (kernels.cpp:161-195 fans matvec_rowmajor rows out)"}
         except Exception as exc:  # reported, never fatal to the GPU number
             extras.setdefault("cpu_baseline", {"value": None, "error": str(exc)[:200]})
 

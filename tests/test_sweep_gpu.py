@@ -70,9 +70,10 @@ def test_ntt_word32_matches_reference(n, L):
 
 
 @pytest.mark.parametrize("n,L,K,dnum,bits", [(4096, 12, 1, 0, 60), (16384, 4, 1, 0, 60), (32768, 2, 1, 0, 60),
-                                              (32768, 6, 1, 0, 60), (32768, 8, 4, 2, 29), (8192, 12, 4, 3, 29)],
-                         ids=["n4096_L12", "n16384_L4", "n32768_L2", "n32768_L6", "w32_n32768_L8_K4_dnum2",
-                              "w32_n8192_L12_K4_dnum3"])
+                                              (32768, 6, 1, 0, 60), (32768, 12, 2, 6, 60), (32768, 8, 4, 2, 29),
+                                              (8192, 12, 4, 3, 29)],
+                         ids=["n4096_L12", "n16384_L4", "n32768_L2", "n32768_L6", "n32768_L12_K2_dnum6",
+                              "w32_n32768_L8_K4_dnum2", "w32_n8192_L12_K4_dnum3"])
 def test_ciphertext_primitives_match_oracle(n, L, K, dnum, bits):
     """60-bit sets on the 64-bit kernels; 29-bit sets on the 32-bit word
     kernels with u32 residue storage (n = 32768: eight-CTA clusters)."""
