@@ -122,7 +122,7 @@ def relaunch_if_needed(a) -> None:
     import torch
 
     have = torch.cuda.device_count()
-    if have < a.gpus:
+    if have < a.gpus and not SAME_DEVICE:
         raise SystemExit(f"bench.py: --gpus {a.gpus} requested but only {have} CUDA device(s) are visible")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
@@ -131,10 +131,20 @@ def relaunch_if_needed(a) -> None:
     sys.exit(subprocess.call(cmd))
 
 
+# Functional test hook (tests/test_bench_ranks_gpu.py): LB_RANKS_ON_ONE_GPU=1
+# puts every rank on cuda:0 over gloo, to exercise the multi-rank path on a
+# one-GPU box. Its timings are meaningless (ranks share the GPU) and it is
+# never the driver's configuration.
+SAME_DEVICE = os.environ.get("LB_RANKS_ON_ONE_GPU") == "1"
+COLL_DEVICE = "cpu" if SAME_DEVICE else "cuda"
+
+
 def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SAME_DEVICE:
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -143,7 +153,10 @@ def dist_setup(n_gpus: int):
             raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} "
                              "device(s) are visible")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SAME_DEVICE:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -156,7 +169,7 @@ def barrier(world):
 def max_over_ranks(world, value: float) -> float:
     from paper_1812_10659_b200.shard import max_over_ranks as _m
 
-    return _m(value, world, device="cuda")
+    return _m(value, world, device=COLL_DEVICE)
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -795,8 +808,8 @@ def run_ours(a, world, rank, local):
     # ---- parity of exactly what was timed: the last e2e step's decrypted
     # logits of every image of this rank vs the reference's integer oracle ----
     par = parity_check(net, imgs, scores)
-    mism = int(sum_over_ranks(float(par["mismatches"]), world))
-    checked = int(sum_over_ranks(float(par["images"]), world))
+    mism = int(sum_over_ranks(float(par["mismatches"]), world, device=COLL_DEVICE))
+    checked = int(sum_over_ranks(float(par["images"]), world, device=COLL_DEVICE))
     parity = {"images": checked, "mismatches": mism, "checker": par["checker"],
               "of": f"decrypted logits of the last timed e2e step, {'all' if checked == world * B else 'a sample of'} "
                     f"{world * B} images"}
