@@ -397,7 +397,8 @@ DeviceBuffer Evaluator::lower_slots(const Message& m, const std::vector<uint32_t
     k_crt_center<<<blocks(uint64_t(B) * ns), kBlock, 0, s>>>(res.get(), n, B, slots.empty() ? nullptr : dsl.get<uint32_t>(),
                                                              ns, tab, out.get());
     LB_KERNEL_DONE();
-    LB_CUDA(cudaStreamSynchronize(s));  // `slots` may be a temporary
+    // no host sync: a pageable host-to-device cudaMemcpyAsync has staged its
+    // source before returning, so `slots` may go out of scope
     return out;
 }
 
