@@ -142,6 +142,17 @@ __global__ void k_shoup_pairs32(BfvDev d, const uint64_t* __restrict__ key, uint
     out[idx] = make_uint2(static_cast<uint32_t>(k), static_cast<uint32_t>((k << 32) / q));
 }
 
+// (key_j[0], key_j[1]) word pairs [dnum][limbs][n] for the 29-bit key switch
+// (64-bit product sums need no Shoup companions): half the key bytes
+__global__ void k_pack_key29(const uint64_t* __restrict__ key, uint2* __restrict__ out, uint32_t dnum, uint32_t limbs,
+                             uint32_t n) {
+    const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint64_t per_j = uint64_t(limbs) * n;
+    if (idx >= dnum * per_j) return;
+    const uint64_t j = idx / per_j, rx = idx % per_j;
+    out[idx] = make_uint2(static_cast<uint32_t>(key[(2 * j) * per_j + rx]), static_cast<uint32_t>(key[(2 * j + 1) * per_j + rx]));
+}
+
 __global__ void k_square_limbs(const uint64_t* __restrict__ s, uint64_t* __restrict__ out, BfvDev d, uint32_t limbs) {
     const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (idx >= uint64_t(limbs) * d.n) return;
@@ -689,6 +700,19 @@ __global__ void k_scale(BfvDev d, const uint64_t* __restrict__ D, uint32_t polys
 
 // ---- constants -----------------------------------------------------------------
 
+namespace {
+bool ks_use_planes();
+}
+
+// 29-bit fast path of the key switch (A/B switch LB_KS29=0)
+static bool ks29_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LB_KS29");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void bfv_setup(Context& cx) {
     auto st = std::make_unique<BfvState>();
     const auto& P = cx.params();
@@ -884,7 +908,15 @@ void bfv_setup(Context& cx) {
         }
         return o;
     };
-    size_t o_pi32 = 0, o_dh32 = 0, o_ph32 = 0, o_klq32 = 0, o_klp32 = 0, o_de32 = 0, o_one32 = 0;
+    size_t o_pi32 = 0, o_dh32 = 0, o_ph32 = 0, o_klq32 = 0, o_klp32 = 0, o_de32 = 0, o_one32 = 0, o_mu60 = 0;
+    d.ks29 = d.ks32 && alpha <= 8 && K <= 8 && dnum <= kMaxPlanes && ks29_enabled() && ks_use_planes();
+    for (uint32_t r = 0; r < LK && d.ks29; ++r)
+        d.ks29 = qp[r] > (uint64_t{1} << 28) && qp[r] < (uint64_t{1} << 29);
+    if (d.ks29) {
+        std::vector<uint32_t> mu(LK);
+        for (uint32_t r = 0; r < LK; ++r) mu[r] = static_cast<uint32_t>((uint64_t{1} << 60) / qp[r]);
+        o_mu60 = put(mu.data(), mu.size() * 4);
+    }
     if (d.ks32) {
         std::vector<uint2> de32(size_t(T) * L), one32(L);
         for (uint32_t j = 0; j < T; ++j)
@@ -969,6 +1001,7 @@ void bfv_setup(Context& cx) {
         d.delta32 = reinterpret_cast<const uint2*>(base + o_de32);
         d.one32 = reinterpret_cast<const uint2*>(base + o_one32);
     }
+    d.mu60 = d.ks29 ? reinterpret_cast<const uint32_t*>(base + o_mu60) : nullptr;
     {
         // HPS scaling computes round(t D / Q) in base B, |D| < n Q^2 / 4
         double lq = 0, lb = 0, lt = 0;
@@ -1045,7 +1078,10 @@ void ensure_key(Context& cx, uint64_t key_id, cudaStream_t s) {
     k_keygen_finish<<<grid_for(uint64_t(d.dnum) * LK * n), kBlock, 0, s>>>(d, key_id, err.get(), target.get(),
                                                                              d.p_mod_qp, key.buf.get());
     LB_KERNEL_DONE();
-    if (d.ks32) {
+    if (d.ks29 && LB_WIDE_MAC) {
+        key.shoup = DeviceBuffer(key_elems * 4, s);
+        k_pack_key29<<<grid_for(key_elems / 2), kBlock, 0, s>>>(key.buf.get(), key.shoup.get<uint2>(), d.dnum, LK, n);
+    } else if (d.ks32) {
         key.shoup = DeviceBuffer(key_elems * 8, s);
         k_shoup_pairs32<<<grid_for(key_elems), kBlock, 0, s>>>(d, key.buf.get(), key.shoup.get<uint2>(), key_elems, LK);
     } else {
@@ -1125,7 +1161,11 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
             const size_t smem = size_t(d.dnum) * S::M * sizeof(W);
             static bool configured32 = false;
             if (!configured32) {
-                LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN, false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kMaxPlanes * S::M * sizeof(W))));
+                LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(kMaxPlanes * S::M * sizeof(W))));
                 configured32 = true;
             }
@@ -1141,7 +1181,10 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_planes_kernel<LOGN>, d, a));
+            if (d.ks29)
+                LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_planes_kernel<LOGN, true>, d, a));
+            else
+                LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_planes_kernel<LOGN, false>, d, a));
             launch_counter().fetch_add(1, std::memory_order_relaxed);
             return;
         }
@@ -1182,7 +1225,14 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN, W>, d, a));
+    if constexpr (sizeof(W) == 4) {
+        if (d.ks29) {
+            LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN, W, true>, d, a));
+            launch_counter().fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
+    }
+    LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN, W, false>, d, a));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -70,6 +70,11 @@ struct BfvDev {
     const uint2* phat_mod_sh32;      // [K][L]
     const uint2* ks_last_q32;        // [L][2]
     const uint2* ks_last_p32;        // [K][2]
+    // ks32 with every prime of Q and P in (2^28, 2^29): base conversions and
+    // the key inner product sum plain 32x32 -> 64-bit products (< 2^61 for
+    // up to 8 terms) and reduce once with mu60[r] = floor(2^60 / r)
+    bool ks29;
+    const uint32_t* mu60;            // [L+K]
     // 32-bit encryption / decryption constants (ks32): floor(Q/t_j) mod q_i
     // and 1 with their companions, and the secret's evaluations over Q
     const uint2* delta32;            // [T][L]

@@ -46,20 +46,61 @@ template <> struct KsTables<uint32_t> {
     __device__ static const uint2* phat(const BfvDev& d) { return d.phat_mod_sh32; }
 };
 
+// x mod q in [0, 6q) for a sum x < 2^61 of products, q in (2^28, 2^29) and
+// mu = floor(2^60 / q): the quotient of x by 2q is estimated from the top 32
+// bits of x / 2^29 (low by at most 3), so the remainder fits 32 bits.
+__device__ __forceinline__ uint32_t barrett61_lazy(uint64_t x, uint32_t mu, uint32_t two_q) {
+    const uint32_t xh = static_cast<uint32_t>(x >> 29);
+    return static_cast<uint32_t>(x) - __umulhi(xh, mu) * two_q;
+}
+
+// Per-kernel constants of the 29-bit fast path (BfvDev::ks29): base
+// conversions and the key inner product accumulate plain 32x32 -> 64-bit
+// products (one IMAD.WIDE per term) and reduce once per output.
+struct Wide29 {
+    bool on = false;
+    uint32_t mu = 0;  // floor(2^60 / q_r)
+};
+
+#ifndef LB_WIDE_CONV
+#define LB_WIDE_CONV 1
+#endif
+#ifndef LB_WIDE_MAC
+#define LB_WIDE_MAC 1  // packed Shoup-free keys; BfvDev::ks29 contexts store them (bfv.cu ensure_key)
+#endif
+
 // Fast base conversion of A source limbs (limb stride n) to one target
 // prime: sum_i y_i w_i with Shoup pairs w_i, in [0, 4r). A == 1 passes the
 // raw residue (< 4r: every prime of Q and P is within a factor 4 of every
 // other). A is a compile-time constant so all A loads of an element are
 // independent (a runtime loop serializes them).
-template <int A, int LOGN, class W, class St, class Last = std::nullptr_t>
+// WIDE (32-bit words, every prime in (2^28, 2^29), A <= 8): the sum of the A
+// plain products y_i w_i < 2^61 is accumulated in 64 bits and reduced once.
+template <int A, bool WIDE, int LOGN, class W, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
                                            const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc,
-                                           Last&& last = nullptr) {
+                                           uint32_t mu, Last&& last = nullptr) {
     const W q = static_cast<W>(P.q), two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
                        start_sync, xc, last);
+    } else if constexpr (WIDE && sizeof(W) == 4) {
+        static_assert(A <= 8, "wide accumulation holds at most 8 products below 2^58");
+        uint32_t ww[A];
+#pragma unroll
+        for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride].x;
+        const uint32_t four_q = 4 * q;
+        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
+            const St* s0 = src + rho;
+            uint32_t v[A];
+#pragma unroll
+            for (int i = 0; i < A; ++i) v[i] = static_cast<uint32_t>(__ldg(&s0[i * n + off]));
+            uint64_t acc = static_cast<uint64_t>(v[0]) * ww[0];
+#pragma unroll
+            for (int i = 1; i < A; ++i) acc += static_cast<uint64_t>(v[i]) * ww[i];
+            return csub<uint32_t>(barrett61_lazy(acc, mu, two_q), four_q);
+        }, start_sync, xc, last);
     } else {
         PairT<W> ww[A];
 #pragma unroll
@@ -80,20 +121,20 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
     }
 }
 
-template <int LOGN, class W, class St, class Last = std::nullptr_t>
+template <int LOGN, class W, bool WIDE = false, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
-                                         Xchg xc = Xchg{}, Last&& last = nullptr) {
+                                         Xchg xc = Xchg{}, uint32_t mu = 0, Last&& last = nullptr) {
     switch (A) {
-        case 1: fwd_conv_n<1, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break;
-        case 2: fwd_conv_n<2, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break;
+        case 1: fwd_conv_n<1, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break;
+        case 2: fwd_conv_n<2, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; } }
         [[fallthrough]];
-        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, last); break; } }
+        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; } }
         [[fallthrough]];
         default: {
             const W q = static_cast<W>(P.q), two_q = 2 * q;
@@ -211,7 +252,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
 // first skip the start barrier (nothing they overwrite is still being read).
 constexpr uint32_t kMaxPlanes = 3;
 
-template <int LOGN>
+template <int LOGN, bool K29 = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner_planes_kernel(BfvDev d,
                                                                                                      KsInnerArgs a) {
     using S = NttShape<LOGN>;
@@ -229,6 +270,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
     const uint32_t xt = rank * S::M + threadIdx.x;
     int own = -1;
     bool first = true;
+    const uint32_t mu = K29 ? d.mu60[r] : 0u;
     __shared__ uint64_t mbar[kMaxPlanes];
     const Xchg xc0 = xchg_init<S::CL>(mbar, kMaxPlanes);
     for (uint32_t j = 0; j < d.dnum; ++j) {
@@ -239,17 +281,65 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
         }
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         const Xchg xc{xc0.mbar ? xc0.mbar + 8 * j : 0u, 0u};
-        fwd_conv<LOGN, W>(planes + j * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, first, xc);
+        fwd_conv<LOGN, W, K29 && LB_WIDE_CONV>(planes + j * S::M, P, rank, src, hi - lo,
+                                               KsTables<W>::dhat(d) + lo * LK + r, LK, first, xc, mu);
         first = false;
     }
-    // acc_h[x] = sum_j v_j[x] * key_j[h][r][x], four elements at a time
-    const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
-    const uint64_t kstride_j = uint64_t(2 * LK) << LOGN, kstride_h = uint64_t(LK) << LOGN;
     const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
     const uint32_t sbt = swb<W>(threadIdx.x);
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
     W* out1 = out0 + uint64_t(LK) * n;
     constexpr int kChunk = 4;
+    if constexpr (K29 && LB_WIDE_MAC) {
+        // packed keys [dnum][L+K][n] of (key_j[0], key_j[1]) words, no Shoup
+        // companions: acc_h = sum_j v_j key_j[h] as 64-bit sums of at most
+        // three products below 2^59 (v_j < 2q), one reduction per output.
+        // Q limbs leave lazily (< 6 q_r: ModDown's epilogue multiplies them),
+        // P limbs below 2 p (the inverse transform's input range).
+        const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
+        const uint64_t kstride_j = uint64_t(LK) << LOGN;
+        const bool to_p = r >= d.L;
+        const W four_q = 4 * q;
+#pragma unroll
+        for (int e0 = 0; e0 < kE; e0 += kChunk) {
+            uint64_t acc0[kChunk] = {}, acc1[kChunk] = {};
+#pragma unroll
+            for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+                if (j >= d.dnum) break;
+                Pr kk[kChunk];
+                W v[kChunk];
+#pragma unroll
+                for (int e = 0; e < kChunk; ++e) {
+                    const uint32_t off = (e0 + e) * S::T;
+                    kk[e] = __ldg(&key[j * kstride_j + off]);
+                    if (static_cast<int>(j) == own) {
+                        const uint32_t x = xt + off;
+                        v[e] = __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
+                    } else {
+                        v[e] = csub<W>(sm_at(planes + j * S::M, sbt, off), two_q);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < kChunk; ++e) {
+                    acc0[e] += static_cast<uint64_t>(v[e]) * kk[e].x;
+                    acc1[e] += static_cast<uint64_t>(v[e]) * kk[e].y;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                W u0 = barrett61_lazy(acc0[e], mu, two_q), u1 = barrett61_lazy(acc1[e], mu, two_q);
+                if (to_p) {
+                    u0 = csub<W>(csub<W>(u0, four_q), two_q);
+                    u1 = csub<W>(csub<W>(u1, four_q), two_q);
+                }
+                out0[(e0 + e) * S::T] = u0;
+                out1[(e0 + e) * S::T] = u1;
+            }
+        }
+    } else {
+    // acc_h[x] = sum_j v_j[x] * key_j[h][r][x], four elements at a time
+    const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
+    const uint64_t kstride_j = uint64_t(2 * LK) << LOGN, kstride_h = uint64_t(LK) << LOGN;
 #pragma unroll
     for (int e0 = 0; e0 < kE; e0 += kChunk) {
         W acc0[kChunk] = {}, acc1[kChunk] = {};
@@ -281,6 +371,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
             out0[(e0 + e) * S::T] = csub<W>(acc0[e], q);
             out1[(e0 + e) * S::T] = csub<W>(acc1[e], q);
         }
+    }
     }
 }
 
@@ -529,7 +620,7 @@ struct MdEpilogue {
     }
 };
 
-template <int LOGN, class W>
+template <int LOGN, class W, bool K29 = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
     __shared__ __align__(16) W sm[S::M];
@@ -554,6 +645,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     if (sum) sum += c * a.sum_stride + (uint64_t(r) << LOGN);
     W* out = static_cast<W*>(h ? a.out1 : a.out0) + c * a.out_stride + (uint64_t(r) << LOGN);
     const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
+    constexpr bool kWide = K29 && LB_WIDE_CONV && sizeof(W) == 4;
+    const uint32_t mu = kWide ? d.mu60[r] : 0u;
 #if LB_MODDOWN_DIRECT
     // epilogue on the transform's last-pass groups (consecutive evaluations,
     // in registers): 16-byte loads of the Q accumulator and the second
@@ -562,13 +655,13 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     // current group's butterflies
     MdEpilogue<LOGN, W> ep{accq, add, sum, out, cta_base, a.add_galois, pinv, q};
 #if LB_MD_PREFETCH
-    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, ep);
+    fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu, ep);
 #else
-    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc,
-                      [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { ep.finish(base, rr, ep.prefetch(base)); });
+    fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu,
+                             [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { ep.finish(base, rr, ep.prefetch(base)); });
 #endif
 #else
-    fwd_conv<LOGN, W>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc);
+    fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu);
     const uint32_t sbt = swb<W>(threadIdx.x);
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
