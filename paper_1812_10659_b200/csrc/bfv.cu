@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
     const uint32_t id = blockIdx.x / S::CL;
     const uint32_t c = id / d.L, i = id % d.L, j = c % d.T;
     const uint64_t n = 1ull << LOGN;
-    const PrimeDev& P = d.primes[i];
-    const W q = static_cast<W>(P.q);
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, i);
+    const W q = P.q;
     const uint2 dl = d.delta32[j * d.L + i], one = d.one32[i];
     const uint64_t* m = mcoef + uint64_t(c) * n;
     const uint32_t* ex = extra + uint64_t(c) * n;
@@ -733,6 +733,7 @@ void bfv_setup(Context& cx) {
     d.tbase = L + K + M;
     d.seed = P.seed;
     d.primes = cx.dev_primes();
+    d.tab32 = cx.tab32();
     const auto& q = P.q;
     const auto& p = P.p;
     const auto& b = P.b;
@@ -1170,7 +1171,7 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
                 configured32 = true;
             }
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * (d.L + d.K) * S::CL));
+            cfg.gridDim = grid_xyz((d.L + d.K) * S::CL, a.count);
             cfg.blockDim = dim3(S::T);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
@@ -1215,7 +1216,7 @@ template <int LOGN, class W>
 void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     using S = NttShape<LOGN>;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(uint64_t(a.count) * 2 * d.L * S::CL));
+    cfg.gridDim = grid_xyz(d.L * S::CL, uint64_t(a.count) * 2);
     cfg.blockDim = dim3(S::T);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -22,6 +22,7 @@ struct BfvDev {
     uint32_t pbase, bbase, tbase;  // prime-table offsets of P, B, T (Q starts at 0)
     uint64_t seed;
     const PrimeDev* primes;
+    PrimeTab32 tab32;            // the context's kernel-parameter prime table (ntt.cuh)
     const uint64_t* s_ntt;       // [L+K+M][n] secret, NTT domain, table order
     const uint32_t* slot_pos;    // [n] device NTT position of slot i
     const uint32_t* pos_slot;    // [n] inverse map

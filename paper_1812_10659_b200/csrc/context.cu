@@ -12,6 +12,14 @@ std::atomic<uint64_t>& launch_counter() {
     return count;
 }
 
+// x blocks per work item, `items` work items over grid.y (and z beyond 65535)
+dim3 grid_xyz(uint32_t x, uint64_t items) {
+    const uint64_t y = std::min<uint64_t>(items, 32768);
+    const uint64_t z = (items + y - 1) / std::max<uint64_t>(y, 1);
+    if (z > 65535) throw std::invalid_argument("batch too large for one launch");
+    return dim3(x, static_cast<unsigned>(std::max<uint64_t>(y, 1)), static_cast<unsigned>(std::max<uint64_t>(z, 1)));
+}
+
 void Context::activate() const {
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess || cur != prm_.device) LB_CUDA(cudaSetDevice(prm_.device));
@@ -117,6 +125,15 @@ Context::Context(const Params& prm) : prm_(prm), n_(prm.n) {
                 d.inv1n32 = make_uint2(static_cast<uint32_t>(d.inv1n), shoup_companion32(d.inv1n, q));
             }
             LB_CUDA(cudaMemcpyAsync(d32, t32.data(), t32.size() * sizeof(uint2), cudaMemcpyHostToDevice, stream_));
+            // kernel-parameter table (q, table slot) of the 32-bit primes
+            if (all_.size() <= size_t(kTabPrimes)) {
+                tab32_.tw = d32;
+                tab32_.count = static_cast<uint32_t>(all_.size());
+                for (size_t j = 0; j < small.size(); ++j) {
+                    tab32_.q[small[j]] = static_cast<uint32_t>(all_[small[j]]);
+                    tab32_.slot[small[j]] = static_cast<uint8_t>(j);
+                }
+            }
         }
     }
     host_primes_ = devs;
@@ -140,19 +157,19 @@ Context::~Context() {
 
 namespace {
 
-template <int LOGN, class W, class St>
-void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+template <int LOGN, class W, class St, bool MAPPED>
+void launch_ntt_m(const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab, bool inverse, cudaStream_t s) {
     using S = NttShape<LOGN>;
     const uint64_t limbs = static_cast<uint64_t>(b.polys) * b.limbs;
     if (limbs == 0) return;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(limbs * S::CL));
+    cfg.gridDim = grid_xyz(b.limbs * S::CL, b.polys);
     cfg.blockDim = dim3(S::T);
     cfg.dynamicSmemBytes = inverse ? ntt_inverse_smem<LOGN, W>() : 0;
     cfg.stream = s;
     if (inverse) {
         static const bool configured = [] {
-            LB_CUDA(cudaFuncSetAttribute(ntt_inverse_kernel<LOGN, W, St>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            LB_CUDA(cudaFuncSetAttribute(ntt_inverse_kernel<LOGN, W, St, MAPPED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(ntt_inverse_smem<LOGN, W>())));
             return true;
         }();
@@ -166,31 +183,41 @@ void launch_ntt(const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (inverse)
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W, St>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W, St, MAPPED>, b, primes, tab));
     else
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W, St>, b, primes));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W, St, MAPPED>, b, primes, tab));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
+template <int LOGN, class W, class St>
+void launch_ntt(const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab, bool inverse, cudaStream_t s) {
+    if (b.prime_map)
+        launch_ntt_m<LOGN, W, St, true>(b, primes, tab, inverse, s);
+    else
+        launch_ntt_m<LOGN, W, St, false>(b, primes, tab, inverse, s);
+}
+
 template <class W, class St>
-void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+void dispatch_ntt(int logn, const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab, bool inverse,
+                  cudaStream_t s) {
     switch (logn) {
-        case 12: launch_ntt<12, W, St>(b, primes, inverse, s); break;
-        case 13: launch_ntt<13, W, St>(b, primes, inverse, s); break;
-        case 14: launch_ntt<14, W, St>(b, primes, inverse, s); break;
-        case 15: launch_ntt<15, W, St>(b, primes, inverse, s); break;
+        case 12: launch_ntt<12, W, St>(b, primes, tab, inverse, s); break;
+        case 13: launch_ntt<13, W, St>(b, primes, tab, inverse, s); break;
+        case 14: launch_ntt<14, W, St>(b, primes, tab, inverse, s); break;
+        case 15: launch_ntt<15, W, St>(b, primes, tab, inverse, s); break;
         default: throw std::invalid_argument("unsupported ring degree");
     }
 }
 
-void dispatch_ntt(bool word32, int logn, const LimbBatch& b, const PrimeDev* primes, bool inverse, cudaStream_t s) {
+void dispatch_ntt(bool word32, int logn, const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab,
+                  bool inverse, cudaStream_t s) {
     if (b.packed32) {
         if (!word32) throw std::invalid_argument("packed 32-bit limbs need primes below 2^30");
-        dispatch_ntt<uint32_t, uint32_t>(logn, b, primes, inverse, s);
+        dispatch_ntt<uint32_t, uint32_t>(logn, b, primes, tab, inverse, s);
     } else if (word32) {
-        dispatch_ntt<uint32_t, uint64_t>(logn, b, primes, inverse, s);
+        dispatch_ntt<uint32_t, uint64_t>(logn, b, primes, tab, inverse, s);
     } else {
-        dispatch_ntt<uint64_t, uint64_t>(logn, b, primes, inverse, s);
+        dispatch_ntt<uint64_t, uint64_t>(logn, b, primes, tab, inverse, s);
     }
 }
 
@@ -213,7 +240,7 @@ bool Context::word32_enabled() {
 }
 
 bool Context::batch_word32(const LimbBatch& b) const {
-    if (!word32_enabled()) return false;
+    if (!word32_enabled() || !tab32_.count) return false;
     if (b.prime_map) return b.map_small;
     if (b.last_stage && !b.last_stage32) return false;
     for (uint32_t l = 0; l < b.limbs; ++l)
@@ -223,12 +250,12 @@ bool Context::batch_word32(const LimbBatch& b) const {
 
 void Context::ntt_forward(const LimbBatch& b, cudaStream_t s) const {
     check_batch(*this, b);
-    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), false, s);
+    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), tab32_, false, s);
 }
 
 void Context::ntt_inverse(const LimbBatch& b, cudaStream_t s) const {
     check_batch(*this, b);
-    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), true, s);
+    dispatch_ntt(batch_word32(b), logn_, b, dev_primes(), tab32_, true, s);
 }
 
 }  // namespace lb

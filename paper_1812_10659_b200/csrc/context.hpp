@@ -124,6 +124,7 @@ public:
     const Params& params() const { return prm_; }
     const PrimeDev* dev_primes() const { return d_primes_.get<PrimeDev>(); }
     const PrimeDev& host_prime(uint32_t i) const { return host_primes_.at(i); }  // constants only
+    const PrimeTab32& tab32() const { return tab32_; }
     const Modulus& modulus(uint32_t i) const { return mods_.at(i); }
     cudaStream_t stream() const { return stream_; }
     int device() const { return prm_.device; }
@@ -138,6 +139,7 @@ public:
     static bool word32_enabled();
     // every prime of [first, first + count) is below 2^30
     bool primes_small(uint32_t first, uint32_t count) const {
+        if (!tab32_.count) return false;  // no kernel-parameter table: 64-bit words
         for (uint32_t i = first; i < first + count; ++i)
             if (all_.at(i) >= kWord32Bound) return false;
         return true;
@@ -163,6 +165,7 @@ private:
     std::vector<Modulus> mods_;
     std::vector<PrimeDev> host_primes_;
     DeviceBuffer d_tables32_;
+    PrimeTab32 tab32_;
     cudaStream_t stream_ = nullptr;
     DeviceBuffer d_tables_;
     DeviceBuffer d_primes_;
@@ -173,5 +176,7 @@ private:
 };
 
 void bfv_setup(Context& cx);
+
+dim3 grid_xyz(uint32_t x, uint64_t items);
 
 }  // namespace lb

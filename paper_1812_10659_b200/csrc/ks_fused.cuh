@@ -77,10 +77,10 @@ struct Wide29 {
 // WIDE (32-bit words, every prime in (2^28, 2^29), A <= 8): the sum of the A
 // plain products y_i w_i < 2^61 is accumulated in 64 bits and reduced once.
 template <int A, bool WIDE, int LOGN, class W, class St, class Last = std::nullptr_t>
-__device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t rank, const St* __restrict__ src,
+__device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_t rank, const St* __restrict__ src,
                                            const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc,
                                            uint32_t mu, Last&& last = nullptr) {
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const W q = P.q, two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
         fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
@@ -122,7 +122,7 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeDev& P, uint32_t ra
 }
 
 template <int LOGN, class W, bool WIDE = false, class St, class Last = std::nullptr_t>
-__device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank, const St* src, uint32_t A,
+__device__ __forceinline__ void fwd_conv(W* sm, const PrimeView<W>& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
                                          Xchg xc = Xchg{}, uint32_t mu = 0, Last&& last = nullptr) {
     switch (A) {
@@ -137,7 +137,7 @@ __device__ __forceinline__ void fwd_conv(W* sm, const PrimeDev& P, uint32_t rank
         case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; } }
         [[fallthrough]];
         default: {
-            const W q = static_cast<W>(P.q), two_q = 2 * q;
+            const W q = P.q, two_q = 2 * q;
             constexpr uint64_t n = 1ull << LOGN;
             fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
                 const uint32_t x = rho + off;
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
     const uint32_t c = id / LK, r = id % LK;
-    const PrimeDev& P = d.primes[r];
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const PrimeView<W> P = prime_view<W>(d.primes[r]);
+    const W q = P.q, two_q = 2 * q;
     const uint32_t cta_base = rank * S::M;
     const uint64_t n = 1ull << LOGN;
     const Pr* key = static_cast<const Pr*>(a.key);
@@ -262,10 +262,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
     W* planes = reinterpret_cast<W*>(smem_raw);
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
-    const uint32_t id = blockIdx.x / S::CL;
-    const uint32_t c = id / LK, r = id % LK;
-    const PrimeDev& P = d.primes[r];
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const uint32_t r = blockIdx.x / S::CL, c = block_yz();
+    if (c >= a.count) return;  // whole cluster
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, r);
+    const W q = P.q, two_q = 2 * q;
     const uint64_t n = 1ull << LOGN;
     const uint32_t xt = rank * S::M + threadIdx.x;
     int own = -1;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_TMEM_MINB) ks_inner_t
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
     const uint32_t c = id / LK, r = id % LK;
-    const PrimeDev& P = d.primes[r];
+    const PrimeView<uint64_t> P = prime_view<uint64_t>(d.primes[r]);
     const uint64_t q = P.q, two_q = 2 * q;
     const uint32_t cta_base = rank * S::M;
     const uint64_t n = 1ull << LOGN;
@@ -626,10 +626,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     __shared__ __align__(16) W sm[S::M];
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
-    const uint32_t id = blockIdx.x / S::CL;
-    const uint32_t r = id % d.L, h = (id / d.L) & 1, c = id / (2 * d.L);
-    const PrimeDev& P = d.primes[r];
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const uint32_t r = blockIdx.x / S::CL, ch = block_yz();
+    const uint32_t h = ch & 1, c = ch >> 1;
+    if (c >= a.count) return;  // whole cluster
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, r);
+    const W q = P.q, two_q = 2 * q;
     const uint64_t n = 1ull << LOGN;
     const W* accp = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h) * LK + d.L) * n;
     // K == 1: [acc]_p (< p < 4 q_r) feeds the lazy transform unreduced;

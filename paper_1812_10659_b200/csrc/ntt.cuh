@@ -127,6 +127,50 @@ struct LimbBatch {
     bool packed32 = false;
 };
 
+// Kernel-parameter copy of what a 32-bit word transform needs before its
+// first butterfly: q and the twiddle-table slot of every prime of the
+// context. Read from the constant bank by prime index, so the twiddle and
+// data loads of a CTA issue at once instead of behind a dependent global
+// load of the PrimeDev entry. Contexts with more than kTabPrimes primes run
+// on 64-bit words (Context::word32_enabled).
+constexpr int kTabPrimes = 64;
+struct PrimeTab32 {
+    const uint2* tw = nullptr;  // slot s: fwd32[n] then inv32[n] at tw + s * 2n
+    uint32_t count = 0;
+    uint32_t q[kTabPrimes] = {};
+    uint8_t slot[kTabPrimes] = {};
+};
+
+// What the transform cores read of a prime.
+template <class W>
+struct PrimeView {
+    W q;
+    const PairT<W>* fwd;
+    const PairT<W>* inv;
+};
+
+template <class W>
+__device__ __forceinline__ PrimeView<W> prime_view(const PrimeDev& P) {
+    if constexpr (sizeof(W) == 8)
+        return PrimeView<W>{P.q, P.fwd, P.inv};
+    else
+        return PrimeView<W>{static_cast<W>(P.q), P.fwd32, P.inv32};
+}
+
+template <class W, int LOGN>
+__device__ __forceinline__ PrimeView<W> prime_view(const PrimeTab32& tab, const PrimeDev* __restrict__ primes, int pidx) {
+    if constexpr (sizeof(W) == 4) {
+        // 32-bit word kernels only run on contexts that filled the table
+        const uint2* base = tab.tw + (static_cast<size_t>(tab.slot[pidx]) << (LOGN + 1));
+        return PrimeView<W>{tab.q[pidx], base, base + (1u << LOGN)};
+    } else {
+        return prime_view<W>(primes[pidx]);
+    }
+}
+
+// Linear block index over grid.y/z (work items beyond 65535 spill into z).
+__device__ __forceinline__ uint32_t block_yz() { return blockIdx.z * gridDim.y + blockIdx.y; }
+
 // Evaluation-domain source position of x under x -> x^g (bit-reversed order).
 // g < 2n <= 2^16 and 2k + 1 < 2n, so the product fits 32 bits.
 __device__ __forceinline__ uint32_t galois_src(uint32_t x, uint64_t g, int logn) {
@@ -335,15 +379,18 @@ struct NttShape {
     static constexpr int NE = N / kE;          // stride of the cross-CTA pass
 };
 
-// Prime-table index of a limb, or -1 when the limb is to be skipped.
-__device__ __forceinline__ int prime_index(const LimbBatch& b, uint32_t limb_id) {
-    if (b.prime_map) return b.prime_map[limb_id % b.map_period];
-    return static_cast<int>(b.first_prime + limb_id % b.limbs);
+// Prime-table index of limb l of a poly, or -1 when the limb is to be
+// skipped (the division only on mapped batches, which are off the hot path).
+template <bool MAPPED>
+__device__ __forceinline__ int prime_index(const LimbBatch& b, uint32_t poly, uint32_t l) {
+    if constexpr (MAPPED)
+        return b.prime_map[(poly * b.limbs + l) % b.map_period];
+    else
+        return static_cast<int>(b.first_prime + l);  // stays a uniform value
 }
 
 template <class St = uint64_t>
-__device__ __forceinline__ St* limb_ptr(const LimbBatch& b, uint32_t limb_id, int logn) {
-    const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
+__device__ __forceinline__ St* limb_ptr(const LimbBatch& b, uint32_t poly, uint32_t l, int logn) {
     return reinterpret_cast<St*>(b.data) + (uint64_t)poly * b.poly_stride + ((uint64_t)l << logn);
 }
 
@@ -517,12 +564,12 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
 }
 
 template <int LOGN, class W, class Load, class Last = std::nullptr_t>
-__device__ __forceinline__ void fwd_core(W* sm, const PrimeDev& P, uint32_t rank, Load&& load,
+__device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t rank, Load&& load,
                                          bool start_sync = true, Xchg xc = Xchg{}, Last&& last = nullptr) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
-    const PairT<W>* __restrict__ tw = fwd_table<W>(P);
+    const W q = P.q, two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = P.fwd;
     // Every CTA of the cluster must be running (and done reading its smem)
     // before peers write into it: arrive now, wait before the remote stores.
     if constexpr (S::CL > 1) {
@@ -599,25 +646,27 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     return cg::this_cluster().block_rank();
 }
 
-// grid.x = CL * (polys * limbs); cluster dims (CL, 1, 1).
+// grid = (CL * limbs, polys split over y and z); cluster dims (CL, 1, 1).
 #ifndef LB_NTT32_MINB
 #define LB_NTT32_MINB 5  // 51 registers: 146.3 vs 145.0 img/s at 4 CTAs/SM
 #endif
 template <class W> constexpr int ntt_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_NTT32_MINB; }
 
-template <int LOGN, class W, class St = uint64_t>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+template <int LOGN, class W, class St = uint64_t, bool MAPPED = false>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
+                                                                                                     const __grid_constant__ PrimeTab32 tab) {
     using S = NttShape<LOGN>;
     __shared__ __align__(16) W sm[S::M];
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
-    const uint32_t limb_id = blockIdx.x / S::CL;
-    const int pidx = prime_index(b, limb_id);
-    if (pidx < 0) return;  // whole cluster skips together
-    const PrimeDev& P = primes[pidx];
-    St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
+    const uint32_t l = blockIdx.x / S::CL, poly = block_yz();
+    if (poly >= b.polys) return;  // whole cluster skips together
+    const int pidx = prime_index<MAPPED>(b, poly, l);
+    if (pidx < 0) return;
+    const PrimeView<W> P = prime_view<W, LOGN>(tab, primes, pidx);
+    St* __restrict__ a = limb_ptr<St>(b, poly, l, LOGN);
     __shared__ uint64_t mbar;
     const Xchg xc = xchg_init<S::CL>(&mbar, 1);
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
+    const W q = P.q, two_q = 2 * q;
     St* out = a + rank * S::M;
     // the last pass's groups (consecutive evaluations) stored straight from
     // registers, fully reduced (16-byte stores for radix-4 groups of u32)
@@ -668,12 +717,12 @@ __device__ __forceinline__ void inv_final(W (&r)[kE], const PairT<W>* __restrict
 // input, and the loads overlap the groups' butterflies. load_group(y, r)
 // fills r[0 .. 2^kTail) with chunk elements y .. y + 2^kTail - 1.
 template <int LOGN, class W, class LoadGroup>
-__device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeDev& P, uint32_t cta_base, LoadGroup&& load_group) {
+__device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeView<W>& P, uint32_t cta_base, LoadGroup&& load_group) {
     constexpr int kTail = (LOGN - kLogE) % kLogE;
     constexpr int G = kE >> kTail;  // groups per thread
     using S = NttShape<LOGN>;
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
-    const PairT<W>* __restrict__ tw = inv_table<W>(P);
+    const W q = P.q, two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = P.inv;
     constexpr uint32_t s0 = LOGN - kTail;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -698,13 +747,13 @@ __device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeDev& P, uint32_t
 // On return r[k] = coefficient rho + k * NE (rho = rank * T + thread), fully
 // reduced, scaled by the final-stage pairs c0 (n^-1 s) and c1.
 template <int LOGN, class W>
-__device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uint32_t parity, const PrimeDev& P,
+__device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uint32_t parity, const PrimeView<W>& P,
                                               uint32_t rank, PairT<W> c0, PairT<W> c1, bool start_wait,
                                               W (&r)[kE]) {
     using S = NttShape<LOGN>;
     static_assert(S::CL > 1, "push exchange needs a cluster");
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
-    const PairT<W>* __restrict__ tw = inv_table<W>(P);
+    const W q = P.q, two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = P.inv;
     const uint32_t cta_base = rank * S::M;
     constexpr int kTail = (LOGN - kLogE) % kLogE;
     static_assert(kTail > 0, "cluster limbs have a tail pass");
@@ -760,8 +809,9 @@ template <int LOGN, class W> constexpr size_t ntt_inverse_smem() {
     return (inv_push<LOGN>() ? 2 : 1) * NttShape<LOGN>::M * sizeof(W);
 }
 
-template <int LOGN, class W, class St = uint64_t>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes) {
+template <int LOGN, class W, class St = uint64_t, bool MAPPED = false>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
+                                                                                                     const __grid_constant__ PrimeTab32 tab) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
     constexpr bool kPush = inv_push<LOGN>();
@@ -770,17 +820,18 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
     W* recv = sm + S::M;  // receive plane [kE][T] (push only)
     __shared__ uint64_t mbar;
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
-    const uint32_t limb_id = blockIdx.x / S::CL;
-    const int pidx = prime_index(b, limb_id);
-    if (pidx < 0) return;  // whole cluster skips together
+    const uint32_t l = blockIdx.x / S::CL, poly = block_yz();
+    if (poly >= b.polys) return;  // whole cluster skips together
+    const int pidx = prime_index<MAPPED>(b, poly, l);
+    if (pidx < 0) return;
     if constexpr (kPush) {
         xchg_init<S::CL>(&mbar, 1);
         cluster_arrive_relaxed();  // peers may push once every mbarrier is initialised
     }
-    const PrimeDev& P = primes[pidx];
-    const W q = static_cast<W>(P.q), two_q = 2 * q;
-    St* __restrict__ a = limb_ptr<St>(b, limb_id, LOGN);
-    const PairT<W>* __restrict__ tw = inv_table<W>(P);
+    const PrimeView<W> P = prime_view<W, LOGN>(tab, primes, pidx);
+    const W q = P.q, two_q = 2 * q;
+    St* __restrict__ a = limb_ptr<St>(b, poly, l, LOGN);
+    const PairT<W>* __restrict__ tw = P.inv;
     const uint32_t cta_base = rank * S::M;
 
     const uint32_t sbt = swb<W>(threadIdx.x);
@@ -789,7 +840,6 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         // when reading a key switch's input)
         constexpr int kTail = (LOGN - kLogE) % kLogE;
         if (b.src) {
-            const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
             const St* in = reinterpret_cast<const St*>(b.src) + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
             inv_tail_pass<LOGN, W>(sm, P, cta_base, [&](uint32_t y, W (&r)[1 << kTail]) {
 #pragma unroll
@@ -814,7 +864,6 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
             });
         }
     } else if (b.src) {
-        const uint32_t poly = limb_id / b.limbs, l = limb_id % b.limbs;
         // src holds words of the batch's storage type (the key switch reads its
         // input ciphertext, stored in the context's residue word)
         const St* in = reinterpret_cast<const St*>(b.src) + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
@@ -833,7 +882,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         }
     }
     __syncthreads();
-    PairT<W> c0 = ninv_pair<W>(P), c1 = inv1n_pair<W>(P);
+    PairT<W> c0, c1;
     {
         const PairT<W>* last = nullptr;
         if constexpr (sizeof(W) == 8)
@@ -841,9 +890,11 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         else
             last = b.last_stage32;
         if (last) {
-            const uint32_t l = limb_id % b.limbs;
             c0 = last[2 * l];
             c1 = last[2 * l + 1];
+        } else {
+            c0 = ninv_pair<W>(primes[pidx]);
+            c1 = inv1n_pair<W>(primes[pidx]);
         }
     }
     const uint32_t rho = rank * S::T + threadIdx.x;
