@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
     constexpr int C = 1 << fwd_last_radix<LOGN>();
     fwd_core<LOGN>(
         sm, P, rank,
-        [&](uint32_t rho, uint32_t off) {
+        [&](uint32_t, uint32_t rho, uint32_t off) {
             const uint32_t k = rho + off;
             const W a = shoup_full<W>(static_cast<W>(__ldg(&m[k])), dl.x, dl.y, q);
             const W b = shoup_full<W>(__ldg(&ex[k]), 1u, one.y, q);
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
         },
         true, xc,
         // the last pass's groups of consecutive evaluations, in registers
-        [&](uint32_t base, W(&rr)[C]) {
+        [&](uint32_t, uint32_t base, W(&rr)[C]) {
             const uint32_t p0 = rank * S::M + base;
             W u0[C], u1[C];
 #pragma unroll
@@ -1130,6 +1130,17 @@ bool ks_use_tmem() {
     return on;
 }
 
+// paired key-switch kernels (29-bit fast path): bit 0 ModDown (both
+// components per cluster), bit 1 the inner product (two ciphertexts per
+// cluster); LB_KS_PAIR overrides
+int ks_pairs() {
+    static const int mask = [] {
+        const char* e = std::getenv("LB_KS_PAIR");
+        return e ? std::atoi(e) : 3;
+    }();
+    return mask;
+}
+
 bool ks_use_planes() {
     static const bool on = [] {
         const char* e = std::getenv("LB_KS_PLANES");
@@ -1227,6 +1238,12 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if constexpr (sizeof(W) == 4) {
+        if (d.ks29 && (ks_pairs() & 1)) {
+            cfg.gridDim = grid_xyz(d.L * S::CL, a.count);
+            LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_pair_kernel<LOGN>, d, a));
+            launch_counter().fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
         if (d.ks29) {
             LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_kernel<LOGN, W, true>, d, a));
             launch_counter().fetch_add(1, std::memory_order_relaxed);

@@ -157,20 +157,21 @@ Context::~Context() {
 
 namespace {
 
-template <int LOGN, class W, class St, bool MAPPED>
+template <int LOGN, class W, class St, bool MAPPED, int NT>
 void launch_ntt_m(const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab, bool inverse, cudaStream_t s) {
     using S = NttShape<LOGN>;
     const uint64_t limbs = static_cast<uint64_t>(b.polys) * b.limbs;
     if (limbs == 0) return;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid_xyz(b.limbs * S::CL, b.polys);
+    cfg.gridDim = grid_xyz(b.limbs * S::CL, b.polys / NT);
     cfg.blockDim = dim3(S::T);
-    cfg.dynamicSmemBytes = inverse ? ntt_inverse_smem<LOGN, W>() : 0;
+    cfg.dynamicSmemBytes = inverse ? ntt_inverse_smem<LOGN, W, NT>() : 0;
     cfg.stream = s;
     if (inverse) {
         static const bool configured = [] {
-            LB_CUDA(cudaFuncSetAttribute(ntt_inverse_kernel<LOGN, W, St, MAPPED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ntt_inverse_smem<LOGN, W>())));
+            LB_CUDA(cudaFuncSetAttribute(ntt_inverse_kernel<LOGN, W, St, MAPPED, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(ntt_inverse_smem<LOGN, W, NT>())));
             return true;
         }();
         (void)configured;
@@ -183,18 +184,39 @@ void launch_ntt_m(const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (inverse)
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W, St, MAPPED>, b, primes, tab));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_inverse_kernel<LOGN, W, St, MAPPED, NT>, b, primes, tab));
     else
-        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W, St, MAPPED>, b, primes, tab));
+        LB_CUDA(cudaLaunchKernelEx(&cfg, ntt_forward_kernel<LOGN, W, St, MAPPED, NT>, b, primes, tab));
     launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
+// the batch's polys [first, first + count)
+template <class St>
+LimbBatch sub_batch(const LimbBatch& b, uint32_t first, uint32_t count) {
+    LimbBatch o = b;
+    o.polys = count;
+    o.data = reinterpret_cast<uint64_t*>(reinterpret_cast<St*>(b.data) + uint64_t(first) * b.poly_stride);
+    if (b.src) o.src = reinterpret_cast<const uint64_t*>(reinterpret_cast<const St*>(b.src) + uint64_t(first) * b.src_stride);
+    return o;
 }
 
 template <int LOGN, class W, class St>
 void launch_ntt(const LimbBatch& b, const PrimeDev* primes, const PrimeTab32& tab, bool inverse, cudaStream_t s) {
-    if (b.prime_map)
-        launch_ntt_m<LOGN, W, St, true>(b, primes, tab, inverse, s);
-    else
-        launch_ntt_m<LOGN, W, St, false>(b, primes, tab, inverse, s);
+    if (b.prime_map) {
+        launch_ntt_m<LOGN, W, St, true, 1>(b, primes, tab, inverse, s);
+        return;
+    }
+    // 32-bit word transforms run two polys per cluster (shared twiddles);
+    // an odd poly is left to the single-transform instance
+    if constexpr (sizeof(W) == 4 && inv_push<LOGN>()) {
+        if ((Context::ntt_pairs() & (inverse ? 2 : 1)) && b.polys >= 2) {
+            const uint32_t even = b.polys & ~1u;
+            launch_ntt_m<LOGN, W, St, false, 2>(sub_batch<St>(b, 0, even), primes, tab, inverse, s);
+            if (b.polys & 1u) launch_ntt_m<LOGN, W, St, false, 1>(sub_batch<St>(b, even, 1), primes, tab, inverse, s);
+            return;
+        }
+    }
+    launch_ntt_m<LOGN, W, St, false, 1>(b, primes, tab, inverse, s);
 }
 
 template <class W, class St>
@@ -237,6 +259,14 @@ bool Context::word32_enabled() {
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+int Context::ntt_pairs() {
+    static const int mask = [] {
+        const char* e = std::getenv("LB_NTT_PAIR");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mask;
 }
 
 bool Context::batch_word32(const LimbBatch& b) const {

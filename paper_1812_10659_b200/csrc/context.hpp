@@ -137,6 +137,10 @@ public:
     // the transform then runs on 32-bit words
     bool batch_word32(const LimbBatch& b) const;
     static bool word32_enabled();
+    // paired 32-bit transforms: bit 0 forward (default on: 0.55 -> 0.62 of the
+    // roof), bit 1 inverse (off: 64 KiB of planes leave 3 CTAs per SM, no gain);
+    // LB_NTT_PAIR overrides
+    static int ntt_pairs();
     // every prime of [first, first + count) is below 2^30
     bool primes_small(uint32_t first, uint32_t count) const {
         if (!tab32_.count) return false;  // no kernel-parameter table: 64-bit words

@@ -76,23 +76,26 @@ struct Wide29 {
 // independent (a runtime loop serializes them).
 // WIDE (32-bit words, every prime in (2^28, 2^29), A <= 8): the sum of the A
 // plain products y_i w_i < 2^61 is accumulated in 64 bits and reduced once.
-template <int A, bool WIDE, int LOGN, class W, class St, class Last = std::nullptr_t>
+// NT > 1: transform u converts the sources at src + u * pair_stride (same
+// target prime and weights), all NT side by side (fwd_core).
+template <int A, bool WIDE, int LOGN, int NT, class W, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_t rank, const St* __restrict__ src,
                                            const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc,
-                                           uint32_t mu, Last&& last = nullptr) {
+                                           uint32_t mu, uint64_t pair_stride, Last&& last = nullptr) {
     const W q = P.q, two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldg(&(src + rho)[off])); },
-                       start_sync, xc, last);
+        fwd_core<LOGN, NT>(sm, P, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
+            return static_cast<W>(__ldg(&(src + u * pair_stride + rho)[off]));
+        }, start_sync, xc, last);
     } else if constexpr (WIDE && sizeof(W) == 4) {
         static_assert(A <= 8, "wide accumulation holds at most 8 products below 2^58");
         uint32_t ww[A];
 #pragma unroll
         for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride].x;
         const uint32_t four_q = 4 * q;
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
-            const St* s0 = src + rho;
+        fwd_core<LOGN, NT>(sm, P, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
+            const St* s0 = src + u * pair_stride + rho;
             uint32_t v[A];
 #pragma unroll
             for (int i = 0; i < A; ++i) v[i] = static_cast<uint32_t>(__ldg(&s0[i * n + off]));
@@ -105,8 +108,8 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_
         PairT<W> ww[A];
 #pragma unroll
         for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride];
-        fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
-            const St* s0 = src + rho;
+        fwd_core<LOGN, NT>(sm, P, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
+            const St* s0 = src + u * pair_stride + rho;
             W v[A];
 #pragma unroll
             for (int i = 0; i < A; ++i) v[i] = static_cast<W>(__ldg(&s0[i * n + off]));
@@ -121,30 +124,32 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_
     }
 }
 
-template <int LOGN, class W, bool WIDE = false, class St, class Last = std::nullptr_t>
+template <int LOGN, class W, bool WIDE = false, int NT = 1, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeView<W>& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
-                                         Xchg xc = Xchg{}, uint32_t mu = 0, Last&& last = nullptr) {
+                                         Xchg xc = Xchg{}, uint32_t mu = 0, Last&& last = nullptr,
+                                         uint64_t pair_stride = 0) {
     switch (A) {
-        case 1: fwd_conv_n<1, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break;
-        case 2: fwd_conv_n<2, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break;
+        case 1: fwd_conv_n<1, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break;
+        case 2: fwd_conv_n<2, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; } }
         [[fallthrough]];
-        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, last); break; } }
+        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; } }
         [[fallthrough]];
         default: {
             const W q = P.q, two_q = 2 * q;
             constexpr uint64_t n = 1ull << LOGN;
-            fwd_core<LOGN>(sm, P, rank, [&](uint32_t rho, uint32_t off) {
+            fwd_core<LOGN, NT>(sm, P, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
                 const uint32_t x = rho + off;
+                const St* su = src + u * pair_stride;
                 W v = 0;
                 for (uint32_t i = 0; i < A; ++i) {
                     const PairT<W> wi = w[i * w_stride];
-                    v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&src[i * n + x])), wi.x, wi.y, q), two_q);
+                    v = add_lazy2<W>(v, shoup_lazy<W>(static_cast<W>(__ldg(&su[i * n + x])), wi.x, wi.y, q), two_q);
                 }
                 return v;
             }, start_sync, xc, last);
@@ -620,6 +625,49 @@ struct MdEpilogue {
     }
 };
 
+// Paired instance (32-bit words): one cluster runs both accumulator
+// components of (ciphertext, q_r) side by side — same prime, twiddles,
+// conversion weights, P^-1 and automorphism positions (fwd_core NT = 2).
+#ifndef LB_MD_PAIR_MINB
+#define LB_MD_PAIR_MINB 4
+#endif
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pair_kernel(BfvDev d, ModDownArgs a) {
+    using S = NttShape<LOGN>;
+    using W = uint32_t;
+    __shared__ __align__(16) W sm[2 * S::M];
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t r = blockIdx.x / S::CL, c = block_yz();
+    if (c >= a.count) return;  // whole cluster
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, r);
+    const W q = P.q;
+    const uint64_t n = 1ull << LOGN;
+    const W* accp = static_cast<const W*>(a.acc) + (uint64_t(c) * 2 * LK + d.L) * n;  // component h at + h LK n
+    __shared__ uint64_t mbar;
+    const Xchg xc = xchg_init<S::CL>(&mbar, 1);
+    const uint32_t cta_base = rank * S::M;
+    const W* accq = static_cast<const W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n;
+    const uint64_t lo = c * a.add_stride + (uint64_t(r) << LOGN), ls = c * a.sum_stride + (uint64_t(r) << LOGN);
+    const W* add0 = a.add0 ? static_cast<const W*>(a.add0) + lo : nullptr;
+    const W* add1 = a.add1 ? static_cast<const W*>(a.add1) + lo : nullptr;
+    const W* sum0 = a.sum0 ? static_cast<const W*>(a.sum0) + ls : nullptr;
+    const W* sum1 = a.sum1 ? static_cast<const W*>(a.sum1) + ls : nullptr;
+    const uint64_t oo = c * a.out_stride + (uint64_t(r) << LOGN);
+    const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
+    const uint32_t mu = d.mu60[r];
+    const MdEpilogue<LOGN, W> ep0{accq, add0, sum0, static_cast<W*>(a.out0) + oo, cta_base, a.add_galois, pinv, q};
+    const MdEpilogue<LOGN, W> ep1{accq + uint64_t(LK) * n, add1, sum1, static_cast<W*>(a.out1) + oo, cta_base, a.add_galois, pinv, q};
+    fwd_conv<LOGN, W, true, 2>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu,
+                               [&](uint32_t u, uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) {
+                                   if (u)
+                                       ep1.finish(base, rr, ep1.prefetch(base));
+                                   else
+                                       ep0.finish(base, rr, ep0.prefetch(base));
+                               },
+                               uint64_t(LK) * n);
+}
+
 template <int LOGN, class W, bool K29 = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
@@ -659,7 +707,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
     fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu, ep);
 #else
     fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu,
-                             [&](uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { ep.finish(base, rr, ep.prefetch(base)); });
+                             [&](uint32_t, uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { ep.finish(base, rr, ep.prefetch(base)); });
 #endif
 #else
     fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu);

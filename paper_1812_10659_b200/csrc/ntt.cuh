@@ -286,55 +286,62 @@ __device__ __forceinline__ void load_twiddles(const PairT<W>* __restrict__ p, Pa
     }
 }
 
-// stage Lv of a radix-2^C group (compile-time Lv so the twiddle array is sized)
-template <int C, int Lv, bool INVERSE, class W>
-__device__ __forceinline__ void group_stage(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                            W two_q) {
+// stage Lv of a radix-2^C group (compile-time Lv so the twiddle array is
+// sized) over NT transforms of the SAME prime held side by side in registers:
+// every twiddle is loaded once and applied to all NT (r[u] = transform u).
+template <int C, int Lv, bool INVERSE, class W, int NT>
+__device__ __forceinline__ void group_stage(W (&r)[NT][1 << C], const PairT<W>* __restrict__ tw, uint32_t s0,
+                                            uint32_t B, W q, W two_q) {
     constexpr int half = 1 << (C - 1 - Lv);
     PairT<W> t[1 << Lv];
     load_twiddles<W>(tw + (1u << (s0 + Lv)) + (B << Lv), t);
 #pragma unroll
     for (int k = 0; k < (1 << C); ++k) {
         if (k & half) continue;
-        if constexpr (INVERSE)
-            gs_bfly(r[k], r[k + half], t[k >> (C - Lv)], q, two_q);
-        else
-            ct_bfly(r[k], r[k + half], t[k >> (C - Lv)], q, two_q);
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            if constexpr (INVERSE)
+                gs_bfly(r[u][k], r[u][k + half], t[k >> (C - Lv)], q, two_q);
+            else
+                ct_bfly(r[u][k], r[u][k + half], t[k >> (C - Lv)], q, two_q);
+        }
     }
 }
 
-template <int C, int Lv, class W>
-__device__ __forceinline__ void fwd_stages(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                           W two_q) {
-    group_stage<C, Lv, false, W>(r, tw, s0, B, q, two_q);
-    if constexpr (Lv + 1 < C) fwd_stages<C, Lv + 1, W>(r, tw, s0, B, q, two_q);
+template <int C, int Lv, class W, int NT>
+__device__ __forceinline__ void fwd_stages(W (&r)[NT][1 << C], const PairT<W>* __restrict__ tw, uint32_t s0,
+                                           uint32_t B, W q, W two_q) {
+    group_stage<C, Lv, false, W, NT>(r, tw, s0, B, q, two_q);
+    if constexpr (Lv + 1 < C) fwd_stages<C, Lv + 1, W, NT>(r, tw, s0, B, q, two_q);
 }
 
 // stages Lv down to LAST (inclusive)
-template <int C, int Lv, int LAST, class W>
-__device__ __forceinline__ void inv_stages(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                           W two_q) {
-    group_stage<C, Lv, true, W>(r, tw, s0, B, q, two_q);
-    if constexpr (Lv > LAST) inv_stages<C, Lv - 1, LAST, W>(r, tw, s0, B, q, two_q);
+template <int C, int Lv, int LAST, class W, int NT>
+__device__ __forceinline__ void inv_stages(W (&r)[NT][1 << C], const PairT<W>* __restrict__ tw, uint32_t s0,
+                                           uint32_t B, W q, W two_q) {
+    group_stage<C, Lv, true, W, NT>(r, tw, s0, B, q, two_q);
+    if constexpr (Lv > LAST) inv_stages<C, Lv - 1, LAST, W, NT>(r, tw, s0, B, q, two_q);
 }
 
-template <int C, class W>
-__device__ __forceinline__ void fwd_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                          W two_q) {
-    fwd_stages<C, 0, W>(r, tw, s0, B, q, two_q);
+template <int C, class W, int NT>
+__device__ __forceinline__ void fwd_group(W (&r)[NT][1 << C], const PairT<W>* __restrict__ tw, uint32_t s0,
+                                          uint32_t B, W q, W two_q) {
+    fwd_stages<C, 0, W, NT>(r, tw, s0, B, q, two_q);
 }
-template <int C, class W>
-__device__ __forceinline__ void inv_group(W* r, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t B, W q,
-                                          W two_q) {
-    inv_stages<C, C - 1, 0, W>(r, tw, s0, B, q, two_q);
+template <int C, class W, int NT>
+__device__ __forceinline__ void inv_group(W (&r)[NT][1 << C], const PairT<W>* __restrict__ tw, uint32_t s0,
+                                          uint32_t B, W q, W two_q) {
+    inv_stages<C, C - 1, 0, W, NT>(r, tw, s0, B, q, two_q);
 }
 
 // One local radix-2^C pass over the CTA's smem chunk (global stages
 // s0..s0+C-1; every block at stage s0 lies inside one CTA).
-template <int LOGN, int C, bool INVERSE, class W>
+// NT > 1: transform u lives in the plane at sm + u * (chunk words).
+template <int LOGN, int C, bool INVERSE, class W, int NT = 1>
 __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t cta_base,
                                            W q, W two_q) {
     constexpr int G = kE >> C;  // groups per thread
+    constexpr uint32_t kPlane = kCtaCoeffs < (1 << LOGN) ? kCtaCoeffs : (1 << LOGN);
     const uint32_t stride = (1u << LOGN) >> (s0 + C);
     const uint32_t log_bs = LOGN - s0;
 #pragma unroll
@@ -345,27 +352,31 @@ __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ t
         const uint32_t B = (cta_base >> log_bs) + b;
         // base has no bits in [log2 stride, log_bs), where k * stride lives
         const uint32_t sb = swb<W>(base);
-        W r[1 << C];
+        W r[NT][1 << C];
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k * stride);
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int k = 0; k < (1 << C); ++k) r[u][k] = sm_at(sm + u * kPlane, sb, k * stride);
         if (INVERSE)
             inv_group<C>(r, tw, s0, B, q, two_q);
         else
             fwd_group<C>(r, tw, s0, B, q, two_q);
 #pragma unroll
-        for (int k = 0; k < (1 << C); ++k) sm_at(sm, sb, k * stride) = r[k];
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int k = 0; k < (1 << C); ++k) sm_at(sm + u * kPlane, sb, k * stride) = r[u][k];
     }
 }
 
 // local pass of C stages, C chosen at run time among 1..kLogE
-template <int LOGN, bool INVERSE, int C = kLogE, class W>
+template <int LOGN, bool INVERSE, int NT = 1, int C = kLogE, class W>
 __device__ __forceinline__ void local_pass_n(int c, W* sm, const PairT<W>* __restrict__ tw, uint32_t s0,
                                              uint32_t cta_base, W q, W two_q) {
     if constexpr (C >= 1) {
         if (c == C)
-            local_pass<LOGN, C, INVERSE>(sm, tw, s0, cta_base, q, two_q);
+            local_pass<LOGN, C, INVERSE, W, NT>(sm, tw, s0, cta_base, q, two_q);
         else
-            local_pass_n<LOGN, INVERSE, C - 1, W>(c, sm, tw, s0, cta_base, q, two_q);
+            local_pass_n<LOGN, INVERSE, NT, C - 1, W>(c, sm, tw, s0, cta_base, q, two_q);
     }
 }
 
@@ -526,13 +537,14 @@ struct has_prefetch : std::false_type {};
 template <class T>
 struct has_prefetch<T, std::void_t<decltype(&std::decay_t<T>::prefetch)>> : std::true_type {};
 
-template <int LOGN, class W, class Last>
+template <int LOGN, int NT, class W, class Last>
 __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t cta_base, W q,
                                               W two_q, Last&& last) {
     constexpr int C = fwd_last_radix<LOGN>();
     constexpr int G = kE >> C;
     constexpr uint32_t s0 = LOGN - C;
-    if constexpr (has_prefetch<Last>::value) {
+    constexpr uint32_t kPlane = kCtaCoeffs < (1 << LOGN) ? kCtaCoeffs : (1 << LOGN);
+    if constexpr (has_prefetch<Last>::value && NT == 1) {
         auto ops = last.prefetch(threadIdx.x << C);
 #pragma unroll
         for (int i = 0; i < G; ++i) {
@@ -541,11 +553,11 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
             decltype(ops) nxt = ops;
             if (i + 1 < G) nxt = last.prefetch((g + kThreads) << C);
             const uint32_t sb = swb<W>(base);
-            W r[1 << C];
+            W r[1][1 << C];
 #pragma unroll
-            for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
+            for (int k = 0; k < (1 << C); ++k) r[0][k] = sm_at(sm, sb, k);
             fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
-            last.finish(base, r, ops);
+            last.finish(base, r[0], ops);
             ops = nxt;
         }
     } else {
@@ -554,16 +566,22 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
             const uint32_t g = threadIdx.x + i * kThreads;
             const uint32_t base = g << C;
             const uint32_t sb = swb<W>(base);
-            W r[1 << C];
+            W r[NT][1 << C];
 #pragma unroll
-            for (int k = 0; k < (1 << C); ++k) r[k] = sm_at(sm, sb, k);
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+                for (int k = 0; k < (1 << C); ++k) r[u][k] = sm_at(sm + u * kPlane, sb, k);
             fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
-            last(base, r);
+#pragma unroll
+            for (int u = 0; u < NT; ++u) last(u, base, r[u]);
         }
     }
 }
 
-template <int LOGN, class W, class Load, class Last = std::nullptr_t>
+// NT transforms of the same prime side by side (twiddles, addresses and the
+// exchange handshake shared): transform u is loaded with load(u, rho, off),
+// lives in the plane at sm + u * M and ends in last(u, base, r).
+template <int LOGN, int NT = 1, class W, class Load, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t rank, Load&& load,
                                          bool start_sync = true, Xchg xc = Xchg{}, Last&& last = nullptr) {
     using S = NttShape<LOGN>;
@@ -577,9 +595,11 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
     }
     {
         const uint32_t rho = rank * S::T + threadIdx.x;
-        W r[kE];
+        W r[NT][kE];
 #pragma unroll
-        for (int k = 0; k < kE; ++k) r[k] = static_cast<W>(load(rho, k * S::NE));
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int k = 0; k < kE; ++k) r[u][k] = static_cast<W>(load(u, rho, k * S::NE));
         fwd_group<kLogE>(r, tw, 0, 0, q, two_q);
         if (start_sync) {
             if constexpr (S::CL > 1) cluster_wait();
@@ -592,33 +612,41 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
             for (int dst = 0; dst < S::CL; ++dst) {
                 if (dst == static_cast<int>(rank)) {
 #pragma unroll
-                    for (int i = 0; i < S::PER_CTA; ++i) sm_at(sm, sb, i * S::NE) = r[dst * S::PER_CTA + i];
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int i = 0; i < S::PER_CTA; ++i)
+                            sm_at(sm + u * S::M, sb, i * S::NE) = r[u][dst * S::PER_CTA + i];
                 } else {
                     const uint32_t rbase = mapa_rank(lbase, dst), rmbar = mapa_rank(xc.mbar, dst);
 #pragma unroll
-                    for (int i = 0; i < S::PER_CTA; ++i)
-                        st_async(rbase + (sb ^ swb<W>(i * S::NE)), r[dst * S::PER_CTA + i], rmbar);
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int i = 0; i < S::PER_CTA; ++i)
+                            st_async(rbase + u * static_cast<uint32_t>(S::M * sizeof(W)) + (sb ^ swb<W>(i * S::NE)),
+                                     r[u][dst * S::PER_CTA + i], rmbar);
                 }
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < kE; ++k) {
-                const uint32_t dst = k / S::PER_CTA;
-                const uint32_t c = (k % S::PER_CTA) * S::NE;
-                if constexpr (S::CL > 1) {
-                    W* remote = cg::this_cluster().map_shared_rank(sm, dst);
-                    sm_at(remote, sb, c) = r[k];
-                } else {
-                    sm_at(sm, sb, c) = r[k];
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+                for (int k = 0; k < kE; ++k) {
+                    const uint32_t dst = k / S::PER_CTA;
+                    const uint32_t c = (k % S::PER_CTA) * S::NE;
+                    if constexpr (S::CL > 1) {
+                        W* remote = cg::this_cluster().map_shared_rank(sm + u * S::M, dst);
+                        sm_at(remote, sb, c) = r[u][k];
+                    } else {
+                        sm_at(sm + u * S::M, sb, c) = r[u][k];
+                    }
                 }
-            }
         }
     }
     if constexpr (S::CL > 1) {
         if constexpr (LB_NTT_MBAR) {
             // remote bytes this CTA receives: PER_CTA words from every thread of
             // every peer
-            constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+            constexpr uint32_t kRemoteBytes = NT * (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
             if (threadIdx.x == 0)
                 mbar_arrive_tx(xc.mbar, kRemoteBytes);
             else
@@ -635,10 +663,10 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
     constexpr int kEnd = kDirect ? LOGN - fwd_last_radix<LOGN>() : LOGN;
 #pragma unroll
     for (int s0 = kLogE; s0 < kEnd; s0 += kLogE) {
-        local_pass_n<LOGN, false>(LOGN - s0 < kLogE ? LOGN - s0 : kLogE, sm, tw, s0, cta_base, q, two_q);
+        local_pass_n<LOGN, false, NT>(LOGN - s0 < kLogE ? LOGN - s0 : kLogE, sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
-    if constexpr (kDirect) fwd_last_pass<LOGN, W>(sm, tw, cta_base, q, two_q, last);
+    if constexpr (kDirect) fwd_last_pass<LOGN, NT, W>(sm, tw, cta_base, q, two_q, last);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -650,16 +678,27 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 #ifndef LB_NTT32_MINB
 #define LB_NTT32_MINB 5  // 51 registers: 146.3 vs 145.0 img/s at 4 CTAs/SM
 #endif
-template <class W> constexpr int ntt_min_blocks() { return sizeof(W) == 8 ? kMinBlocks : LB_NTT32_MINB; }
+// Paired transforms (NT = 2, 32-bit words): a cluster runs limb l of polys
+// 2p and 2p + 1 side by side, so twiddle loads, smem addresses and the
+// exchange handshake are paid once for two transforms and every warp carries
+// two independent butterfly chains. Registers per thread allow one CTA less
+// per SM than the single-transform instance, which still means more
+// transforms in flight per SM.
+#ifndef LB_NTT_PAIR_MINB
+#define LB_NTT_PAIR_MINB 4
+#endif
+template <class W, int NT = 1> constexpr int ntt_min_blocks() {
+    return sizeof(W) == 8 ? kMinBlocks : NT == 1 ? LB_NTT32_MINB : LB_NTT_PAIR_MINB;
+}
 
-template <int LOGN, class W, class St = uint64_t, bool MAPPED = false>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
+template <int LOGN, class W, class St = uint64_t, bool MAPPED = false, int NT = 1>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W, NT>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
                                                                                                      const __grid_constant__ PrimeTab32 tab) {
     using S = NttShape<LOGN>;
-    __shared__ __align__(16) W sm[S::M];
+    __shared__ __align__(16) W sm[NT * S::M];
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
-    const uint32_t l = blockIdx.x / S::CL, poly = block_yz();
-    if (poly >= b.polys) return;  // whole cluster skips together
+    const uint32_t l = blockIdx.x / S::CL, poly = block_yz() * NT;
+    if (poly >= b.polys) return;  // whole cluster skips together (polys is a multiple of NT)
     const int pidx = prime_index<MAPPED>(b, poly, l);
     if (pidx < 0) return;
     const PrimeView<W> P = prime_view<W, LOGN>(tab, primes, pidx);
@@ -667,12 +706,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
     __shared__ uint64_t mbar;
     const Xchg xc = xchg_init<S::CL>(&mbar, 1);
     const W q = P.q, two_q = 2 * q;
-    St* out = a + rank * S::M;
     // the last pass's groups (consecutive evaluations) stored straight from
     // registers, fully reduced (16-byte stores for radix-4 groups of u32)
-    fwd_core<LOGN>(
-        sm, P, rank, [&](uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + rho)[off])); }, true, xc,
-        [&](uint32_t base, W(&r)[1 << fwd_last_radix<LOGN>()]) {
+    fwd_core<LOGN, NT>(
+        sm, P, rank,
+        [&](uint32_t u, uint32_t rho, uint32_t off) { return static_cast<W>(__ldcs(&(a + u * b.poly_stride + rho)[off])); },
+        true, xc,
+        [&](uint32_t u, uint32_t base, W(&r)[1 << fwd_last_radix<LOGN>()]) {
+            St* out = a + u * b.poly_stride + rank * S::M;
             constexpr int C = fwd_last_radix<LOGN>();
             if constexpr (sizeof(St) == 4 && C == 2) {
                 __stcs(reinterpret_cast<uint4*>(out + base),
@@ -694,29 +735,32 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_fo
 
 // Cross-CTA pass tail: stages 3, 2, 1 as usual; stage 0 with the scaled
 // n^-1 pairs merged (c0 for the first half, c1 = psi^-bitrev(1) n^-1 s).
-template <class W>
-__device__ __forceinline__ void inv_final(W (&r)[kE], const PairT<W>* __restrict__ tw, W q, PairT<W> c0,
+template <class W, int NT>
+__device__ __forceinline__ void inv_final(W (&r)[NT][kE], const PairT<W>* __restrict__ tw, W q, PairT<W> c0,
                                           PairT<W> c1) {
     const W two_q = 2 * q;
-    inv_stages<kLogE, kLogE - 1, 1, W>(r, tw, 0, 0, q, two_q);
+    inv_stages<kLogE, kLogE - 1, 1, W, NT>(r, tw, 0, 0, q, two_q);
     constexpr int half0 = kE / 2;
 #pragma unroll
-    for (int k = 0; k < half0; ++k) {
-        W x = r[k], y = r[k + half0];
-        W s = add_alu<W>(x, y);  // < 4q
-        W d = x - y + two_q;
-        r[k] = shoup_full<W>(s, c0.x, c0.y, q);
-        r[k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
-    }
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int k = 0; k < half0; ++k) {
+            W x = r[u][k], y = r[u][k + half0];
+            W s = add_alu<W>(x, y);  // < 4q
+            W d = x - y + two_q;
+            r[u][k] = shoup_full<W>(s, c0.x, c0.y, q);
+            r[u][k + half0] = shoup_full<W>(d, c1.x, c1.y, q);
+        }
 }
 
 // The inverse's first (tail) pass, stages LOGN-1 .. LOGN-kTail, straight from
 // global memory: its butterfly groups are 2^kTail consecutive coefficients
 // (stride 1), so each group is one vector load (16 bytes for kTail = 2 on
 // u32), and the results go to smem once — no staging store + reload of the
-// input, and the loads overlap the groups' butterflies. load_group(y, r)
-// fills r[0 .. 2^kTail) with chunk elements y .. y + 2^kTail - 1.
-template <int LOGN, class W, class LoadGroup>
+// input, and the loads overlap the groups' butterflies. load_group(u, y, r)
+// fills r[0 .. 2^kTail) with chunk elements y .. y + 2^kTail - 1 of
+// transform u (plane sm + u * M).
+template <int LOGN, class W, int NT = 1, class LoadGroup>
 __device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeView<W>& P, uint32_t cta_base, LoadGroup&& load_group) {
     constexpr int kTail = (LOGN - kLogE) % kLogE;
     constexpr int G = kE >> kTail;  // groups per thread
@@ -728,12 +772,15 @@ __device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeView<W>& P, uint
     for (int i = 0; i < G; ++i) {
         const uint32_t g = threadIdx.x + i * S::T;
         const uint32_t base = g << kTail;
-        W r[1 << kTail];
-        load_group(base, r);
+        W r[NT][1 << kTail];
+#pragma unroll
+        for (int u = 0; u < NT; ++u) load_group(u, base, r[u]);
         inv_group<kTail>(r, tw, s0, (cta_base >> kTail) + g, q, two_q);
         const uint32_t sb = swb<W>(base);
 #pragma unroll
-        for (int k = 0; k < (1 << kTail); ++k) sm_at(sm, sb, k) = r[k];
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int k = 0; k < (1 << kTail); ++k) sm_at(sm + u * S::M, sb, k) = r[u][k];
     }
 }
 
@@ -746,10 +793,11 @@ __device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeView<W>& P, uint
 // (start_wait: wait here on the cluster barrier the caller arrived on).
 // On return r[k] = coefficient rho + k * NE (rho = rank * T + thread), fully
 // reduced, scaled by the final-stage pairs c0 (n^-1 s) and c1.
-template <int LOGN, class W>
+// NT transforms: planes sm + u * M and recv + u * M, one mbarrier for all.
+template <int LOGN, class W, int NT>
 __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uint32_t parity, const PrimeView<W>& P,
                                               uint32_t rank, PairT<W> c0, PairT<W> c1, bool start_wait,
-                                              W (&r)[kE]) {
+                                              W (&r)[NT][kE]) {
     using S = NttShape<LOGN>;
     static_assert(S::CL > 1, "push exchange needs a cluster");
     const W q = P.q, two_q = 2 * q;
@@ -759,7 +807,7 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     static_assert(kTail > 0, "cluster limbs have a tail pass");
 #pragma unroll
     for (int s0 = LOGN - kTail - kLogE; s0 >= 2 * kLogE; s0 -= kLogE) {
-        local_pass<LOGN, kLogE, true, W>(sm, tw, s0, cta_base, q, two_q);
+        local_pass<LOGN, kLogE, true, W, NT>(sm, tw, s0, cta_base, q, two_q);
         __syncthreads();
     }
     // stages 7..4 (s0 = kLogE, one radix-16 group per thread): block bb,
@@ -771,7 +819,9 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
     const uint32_t sb = swb<W>(bb * S::NE + o);
 #pragma unroll
-    for (int k = 0; k < kE; ++k) r[k] = sm_at(sm, sb, k * stride);
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[u][k] = sm_at(sm + u * S::M, sb, k * stride);
     inv_group<kLogE>(r, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
     if (start_wait) cluster_wait();
     const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
@@ -780,23 +830,30 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     for (int dst = 0; dst < S::CL; ++dst) {
         if (dst == static_cast<int>(rank)) {
 #pragma unroll
-            for (int i = 0; i < S::PER_CTA; ++i) recv[slot + i * stride] = r[dst * S::PER_CTA + i];
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i) recv[u * S::M + slot + i * stride] = r[u][dst * S::PER_CTA + i];
         } else {
             const uint32_t rb = mapa_rank(lrecv, dst), rm = mapa_rank(mbar, dst);
 #pragma unroll
-            for (int i = 0; i < S::PER_CTA; ++i)
-                st_async(rb + i * stride * static_cast<uint32_t>(sizeof(W)), r[dst * S::PER_CTA + i], rm);
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i)
+                    st_async(rb + (u * S::M + i * stride) * static_cast<uint32_t>(sizeof(W)), r[u][dst * S::PER_CTA + i],
+                             rm);
         }
     }
-    constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+    constexpr uint32_t kRemoteBytes = NT * (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
     if (threadIdx.x == 0)
         mbar_arrive_tx(mbar, kRemoteBytes);
     else
         mbar_arrive(mbar);
     mbar_wait(mbar, parity);
 #pragma unroll
-    for (int k = 0; k < kE; ++k) r[k] = recv[k * S::T + threadIdx.x];
-    inv_final<W>(r, tw, q, c0, c1);
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[u][k] = recv[u * S::M + k * S::T + threadIdx.x];
+    inv_final<W, NT>(r, tw, q, c0, c1);
 }
 
 // Inverse transform. With LB_NTT_MBAR the cross-CTA pass is push-based: the
@@ -805,23 +862,30 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
 // on its own mbarrier instead of two cluster-wide barriers around remote
 // loads. Dynamic smem: M words (+ M receive words when pushing).
 template <int LOGN> constexpr bool inv_push() { return NttShape<LOGN>::CL > 1 && LB_NTT_MBAR; }
-template <int LOGN, class W> constexpr size_t ntt_inverse_smem() {
-    return (inv_push<LOGN>() ? 2 : 1) * NttShape<LOGN>::M * sizeof(W);
+template <int LOGN, class W, int NT = 1> constexpr size_t ntt_inverse_smem() {
+    return NT * (inv_push<LOGN>() ? 2 : 1) * NttShape<LOGN>::M * sizeof(W);
+}
+#ifndef LB_INV_PAIR_MINB
+#define LB_INV_PAIR_MINB 3  // 64 KiB of planes per paired CTA
+#endif
+template <class W, int NT> constexpr int inv_min_blocks() {
+    return NT == 1 ? ntt_min_blocks<W>() : LB_INV_PAIR_MINB;
 }
 
-template <int LOGN, class W, class St = uint64_t, bool MAPPED = false>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
+template <int LOGN, class W, class St = uint64_t, bool MAPPED = false, int NT = 1>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) ntt_inverse_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
                                                                                                      const __grid_constant__ PrimeTab32 tab) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
     constexpr bool kPush = inv_push<LOGN>();
+    static_assert(NT == 1 || kPush, "paired inverse transforms use the push exchange");
     extern __shared__ __align__(16) uint8_t inv_smem_raw[];
-    W* sm = reinterpret_cast<W*>(inv_smem_raw);
-    W* recv = sm + S::M;  // receive plane [kE][T] (push only)
+    W* sm = reinterpret_cast<W*>(inv_smem_raw);  // planes sm + u * M
+    W* recv = sm + NT * S::M;                    // receive planes [kE][T] (push only)
     __shared__ uint64_t mbar;
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
-    const uint32_t l = blockIdx.x / S::CL, poly = block_yz();
-    if (poly >= b.polys) return;  // whole cluster skips together
+    const uint32_t l = blockIdx.x / S::CL, poly = block_yz() * NT;
+    if (poly >= b.polys) return;  // whole cluster skips together (polys is a multiple of NT)
     const int pidx = prime_index<MAPPED>(b, poly, l);
     if (pidx < 0) return;
     if constexpr (kPush) {
@@ -841,25 +905,26 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         constexpr int kTail = (LOGN - kLogE) % kLogE;
         if (b.src) {
             const St* in = reinterpret_cast<const St*>(b.src) + uint64_t(poly) * b.src_stride + (uint64_t(l) << LOGN);
-            inv_tail_pass<LOGN, W>(sm, P, cta_base, [&](uint32_t y, W (&r)[1 << kTail]) {
+            inv_tail_pass<LOGN, W, NT>(sm, P, cta_base, [&](uint32_t u, uint32_t y, W (&r)[1 << kTail]) {
 #pragma unroll
                 for (int k = 0; k < (1 << kTail); ++k) {
                     const uint32_t x = cta_base + y + k;
-                    r[k] = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
+                    r[k] = static_cast<W>(__ldg(&(in + u * b.src_stride)[b.galois ? galois_src(x, b.galois, LOGN) : x]));
                 }
             });
         } else {
             const St* in = a + cta_base;
-            inv_tail_pass<LOGN, W>(sm, P, cta_base, [&](uint32_t y, W (&r)[1 << kTail]) {
+            inv_tail_pass<LOGN, W, NT>(sm, P, cta_base, [&](uint32_t u, uint32_t y, W (&r)[1 << kTail]) {
+                const St* inu = in + u * b.poly_stride;
                 if constexpr (sizeof(St) == 4 && kTail == 2) {
-                    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in + y));
+                    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(inu + y));
                     r[0] = v.x;
                     r[1] = v.y;
                     r[2] = v.z;
                     r[3] = v.w;
                 } else {
 #pragma unroll
-                    for (int k = 0; k < (1 << kTail); ++k) r[k] = static_cast<W>(__ldcs(&in[y + k]));
+                    for (int k = 0; k < (1 << kTail); ++k) r[k] = static_cast<W>(__ldcs(&inu[y + k]));
                 }
             });
         }
@@ -898,9 +963,9 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
         }
     }
     const uint32_t rho = rank * S::T + threadIdx.x;
-    W r[kE];
+    W r[NT][kE];
     if constexpr (kPush) {
-        inv_core_push<LOGN, W>(sm, recv, smem_addr(&mbar), 0, P, rank, c0, c1, true, r);
+        inv_core_push<LOGN, W, NT>(sm, recv, smem_addr(&mbar), 0, P, rank, c0, c1, true, r);
     } else {
         // local passes in reverse: the last (possibly short) chunk first
         constexpr int kTail = (LOGN - kLogE) % kLogE;
@@ -922,15 +987,17 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W>()) ntt_in
             const uint32_t c = (k % S::PER_CTA) * S::NE;
             if constexpr (S::CL > 1) {
                 W* remote = cg::this_cluster().map_shared_rank(sm, src);
-                r[k] = sm_at(remote, sb, c);
+                r[0][k] = sm_at(remote, sb, c);
             } else {
-                r[k] = sm_at(sm, sb, c);
+                r[0][k] = sm_at(sm, sb, c);
             }
         }
-        inv_final<W>(r, tw, q, c0, c1);
+        inv_final<W, NT>(r, tw, q, c0, c1);
     }
 #pragma unroll
-    for (int k = 0; k < kE; ++k) __stcs(&a[rho + k * S::NE], static_cast<St>(r[k]));
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) __stcs(&(a + u * b.poly_stride)[rho + k * S::NE], static_cast<St>(r[u][k]));
     if constexpr (S::CL > 1 && !kPush) {  // keep smem alive for peers' remote loads
         cluster_arrive_relaxed();
         cluster_wait();

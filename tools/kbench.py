@@ -18,7 +18,8 @@ def main():
     prm = lola_mnist_params_w32()
     cx = BfvContext(prm)
     cx.keygen(bench_galois(prm.n))
-    ks = bench.ks_roofline(cx, 80)
+    import os
+    ks = bench.ks_roofline(cx, int(os.environ.get("KB_COUNT", "320")))
     ntt = bench.ntt_roofline(cx, 64 * 5 * prm.dnum * (prm.L + prm.K - 1))
     print(json.dumps({"ks_frac": round(ks["frac"], 4), "ks_ms": round(ks["launch_set_ms"], 4),
                       "ntt_frac": round(ntt["frac"], 4), "ntt_fwd": round(ntt["frac_forward"], 4),
