@@ -1169,6 +1169,48 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         return;
     }
     if constexpr (sizeof(W) == 4) {
+        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= 2 && d.dnum <= 2 && d.L % d.alpha == 0 &&
+            S::CL > 1) {
+            // two ciphertexts per cluster; targets in Q have dnum - 1 foreign
+            // digits, targets in P dnum: separate launches sized for each
+            static bool configured_pair = false;
+            if (!configured_pair) {
+                LB_CUDA(cudaFuncSetAttribute(ks_inner_pair_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(2 * 2 * S::M * sizeof(W))));
+                configured_pair = true;
+            }
+            KsInnerArgs ap = a;
+            ap.count = a.count & ~1u;
+            {
+                // one launch over every target of Q ∪ P (planes sized for the
+                // targets in P: dnum foreign digits x 2 ciphertexts)
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = grid_xyz((d.L + d.K) * S::CL, ap.count / 2);
+                cfg.blockDim = dim3(S::T);
+                cfg.dynamicSmemBytes = size_t(d.dnum) * 2 * S::M * sizeof(W);
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = S::CL;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_pair_kernel<LOGN>, d, ap, 0u));
+                launch_counter().fetch_add(1, std::memory_order_relaxed);
+            }
+            if (!(a.count & 1u)) return;
+            // the odd ciphertext goes through the single-ciphertext kernel below
+            KsInnerArgs al = a;
+            const uint32_t c = a.count - 1;
+            const size_t wb = sizeof(W);
+            al.dc = static_cast<const uint8_t*>(a.dc) + uint64_t(c) * d.L * d.n * wb;
+            al.dn = static_cast<const uint8_t*>(a.dn) + uint64_t(c) * a.d_stride * wb;
+            al.acc = static_cast<uint8_t*>(a.acc) + uint64_t(c) * 2 * (d.L + d.K) * d.n * wb;
+            al.count = 1;
+            launch_ks_inner<LOGN, W>(d, al, s);
+            return;
+        }
         if (d.dnum <= kMaxPlanes && ks_use_planes()) {
             const size_t smem = size_t(d.dnum) * S::M * sizeof(W);
             static bool configured32 = false;

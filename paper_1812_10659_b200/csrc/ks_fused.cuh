@@ -380,6 +380,113 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
     }
 }
 
+// ---- paired plane variant (29-bit fast path) ---------------------------------------
+// One cluster per (ciphertext pair, target prime): the ModUp transforms of
+// ciphertexts c and c + 1 run side by side (fwd_core NT = 2: shared twiddles,
+// conversion weights, addresses, exchange) and the inner product loads every
+// key word and automorphism position once for both. Planes: dnum foreign
+// digits x 2 ciphertexts (64 KiB at dnum = 2: 3 CTAs per SM, which the 80
+// registers per thread allow anyway); r = r_first + blockIdx.x / CL.
+#ifndef LB_KS_PAIR_MINB
+#define LB_KS_PAIR_MINB 3
+#endif
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_pair_kernel(BfvDev d, KsInnerArgs a,
+                                                                                          uint32_t r_first) {
+    using S = NttShape<LOGN>;
+    using W = uint32_t;
+    using Pr = uint2;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    W* planes = reinterpret_cast<W*>(smem_raw);  // [foreign digit][pair member][M]
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t r = r_first + blockIdx.x / S::CL, c = 2 * block_yz();
+    if (c >= a.count) return;  // whole cluster (count is even)
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, r);
+    const W q = P.q, two_q = 2 * q, four_q = 4 * q;
+    const uint64_t n = 1ull << LOGN;
+    const uint32_t xt = rank * S::M + threadIdx.x;
+    const uint32_t mu = d.mu60[r];
+    int own = -1;
+    bool first = true;
+    uint32_t pl = 0;
+    __shared__ uint64_t mbar[kMaxPlanes];
+    const Xchg xc0 = xchg_init<S::CL>(mbar, kMaxPlanes);
+    for (uint32_t j = 0; j < d.dnum; ++j) {
+        const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+        if (r >= lo && r < hi) {
+            own = static_cast<int>(j);
+            continue;
+        }
+        const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
+        const Xchg xc{xc0.mbar ? xc0.mbar + 8 * pl : 0u, 0u};
+        fwd_conv<LOGN, W, true, 2>(planes + pl * 2 * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK,
+                                   first, xc, mu, nullptr, uint64_t(d.L) * n);
+        first = false;
+        ++pl;
+    }
+    const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
+    const uint64_t kstride_j = uint64_t(LK) << LOGN;
+    const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
+    const uint32_t sbt = swb<W>(threadIdx.x);
+    W* out = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
+    const uint64_t out_h = uint64_t(LK) * n, out_u = 2 * out_h;
+    const bool to_p = r >= d.L;
+    constexpr int kChunk = 4;
+#pragma unroll
+    for (int e0 = 0; e0 < kE; e0 += kChunk) {
+        Pr kk[kMaxPlanes][kChunk];
+        uint32_t xs[kChunk];
+#pragma unroll
+        for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+            if (j >= d.dnum) break;
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) kk[j][e] = __ldg(&key[j * kstride_j + (e0 + e) * S::T]);
+        }
+        if (own >= 0) {
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                const uint32_t x = xt + (e0 + e) * S::T;
+                xs[e] = a.d_galois ? galois_src(x, a.d_galois, LOGN) : x;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            uint64_t acc0[kChunk] = {}, acc1[kChunk] = {};
+            uint32_t pj = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+                if (j >= d.dnum) break;
+                W v[kChunk];
+                if (static_cast<int>(j) == own) {
+#pragma unroll
+                    for (int e = 0; e < kChunk; ++e) v[e] = __ldg(&(dn + u * a.d_stride)[xs[e]]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < kChunk; ++e)
+                        v[e] = csub<W>(sm_at(planes + (pj * 2 + u) * S::M, sbt, (e0 + e) * S::T), two_q);
+                    ++pj;
+                }
+#pragma unroll
+                for (int e = 0; e < kChunk; ++e) {
+                    acc0[e] += static_cast<uint64_t>(v[e]) * kk[j][e].x;
+                    acc1[e] += static_cast<uint64_t>(v[e]) * kk[j][e].y;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                W u0 = barrett61_lazy(acc0[e], mu, two_q), u1 = barrett61_lazy(acc1[e], mu, two_q);
+                if (to_p) {
+                    u0 = csub<W>(csub<W>(u0, four_q), two_q);
+                    u1 = csub<W>(csub<W>(u1, four_q), two_q);
+                }
+                out[u * out_u + (e0 + e) * S::T] = u0;
+                out[u * out_u + out_h + (e0 + e) * S::T] = u1;
+            }
+        }
+    }
+}
+
 // ---- TMEM-accumulator variant ------------------------------------------------------
 // Same algorithm as ks_inner_kernel; the two accumulators of every element
 // live in Tensor Memory instead of shared memory (128 TMEM columns per CTA:
