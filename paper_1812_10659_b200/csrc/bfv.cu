@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<uint32_t>())
                 const int8_t* __restrict__ err, uint64_t id_base, uint32_t* __restrict__ ct) {
     using S = NttShape<LOGN>;
     using W = uint32_t;
-    __shared__ __align__(16) W sm[S::M];
+    __shared__ __align__(16) W sm[plane_words<LOGN, W>()];
     __shared__ uint64_t mbar;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
@@ -1176,7 +1176,7 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
             static bool configured_pair = false;
             if (!configured_pair) {
                 LB_CUDA(cudaFuncSetAttribute(ks_inner_pair_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(2 * 2 * S::M * sizeof(W))));
+                                             int(2 * 2 * plane_words<LOGN, W>() * sizeof(W))));
                 configured_pair = true;
             }
             KsInnerArgs ap = a;
@@ -1187,7 +1187,7 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = grid_xyz((d.L + d.K) * S::CL, ap.count / 2);
                 cfg.blockDim = dim3(S::T);
-                cfg.dynamicSmemBytes = size_t(d.dnum) * 2 * S::M * sizeof(W);
+                cfg.dynamicSmemBytes = size_t(d.dnum) * 2 * plane_words<LOGN, W>() * sizeof(W);
                 cfg.stream = s;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1212,15 +1212,15 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
             return;
         }
         if (d.dnum <= kMaxPlanes && ks_use_planes()) {
-            const size_t smem = size_t(d.dnum) * S::M * sizeof(W);
+            const size_t smem = size_t(d.dnum) * plane_words<LOGN, W>() * sizeof(W);
             static bool configured32 = false;
             if (!configured32) {
                 LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(kMaxPlanes * S::M * sizeof(W))));
+                                             int(kMaxPlanes * plane_words<LOGN, W>() * sizeof(W))));
                 LB_CUDA(cudaFuncSetAttribute(ks_inner_planes_kernel<LOGN, true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(kMaxPlanes * S::M * sizeof(W))));
+                                             int(kMaxPlanes * plane_words<LOGN, W>() * sizeof(W))));
                 configured32 = true;
             }
             cudaLaunchConfig_t cfg = {};
@@ -1243,7 +1243,7 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
             return;
         }
     }
-    const size_t smem = 3ull * S::M * sizeof(W);
+    const size_t smem = (plane_words<LOGN, W>() + 2ull * S::M) * sizeof(W);
     static bool configured = false;
     if (!configured) {
         LB_CUDA(cudaFuncSetAttribute(ks_inner_kernel<LOGN, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
     using Pr = PairT<W>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     W* sm = reinterpret_cast<W*>(smem_raw);
-    W* acc0 = sm + S::M;
-    W* acc1 = sm + 2 * S::M;
+    W* acc0 = sm + plane_words<LOGN, W>();  // linear accumulator planes behind the transform plane
+    W* acc1 = acc0 + S::M;
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t id = blockIdx.x / S::CL;
@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, ks_min_blocks<W>()) ks_inne
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, W>(sm, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, true, xc);
         xc.parity ^= 1;  // the same plane (and mbarrier) serves every digit
-        const uint32_t sbt = swb<W>(threadIdx.x);
-        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm_at(sm, sbt, y - threadIdx.x), q, two_q); });
+        const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
+        mac_all(j, [&](uint32_t y, uint32_t) { return reduce_4q<W>(sm_at<LOGN>(sm, sbt, y - threadIdx.x), q, two_q); });
     }
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + cta_base;
     W* out1 = out0 + uint64_t(LK) * n;
@@ -286,12 +286,12 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
         }
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         const Xchg xc{xc0.mbar ? xc0.mbar + 8 * j : 0u, 0u};
-        fwd_conv<LOGN, W, K29 && LB_WIDE_CONV>(planes + j * S::M, P, rank, src, hi - lo,
+        fwd_conv<LOGN, W, K29 && LB_WIDE_CONV>(planes + j * plane_words<LOGN, W>(), P, rank, src, hi - lo,
                                                KsTables<W>::dhat(d) + lo * LK + r, LK, first, xc, mu);
         first = false;
     }
     const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
-    const uint32_t sbt = swb<W>(threadIdx.x);
+    const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
     W* out0 = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
     W* out1 = out0 + uint64_t(LK) * n;
     constexpr int kChunk = 4;
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
                         const uint32_t x = xt + off;
                         v[e] = __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
                     } else {
-                        v[e] = csub<W>(sm_at(planes + j * S::M, sbt, off), two_q);
+                        v[e] = csub<W>(sm_at<LOGN>(planes + j * plane_words<LOGN, W>(), sbt, off), two_q);
                     }
                 }
 #pragma unroll
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
                     const uint32_t x = xt + off;
                     v[e] = __ldg(&dn[a.d_galois ? galois_src(x, a.d_galois, LOGN) : x]);
                 } else {
-                    v[e] = reduce_4q<W>(sm_at(planes + j * S::M, sbt, off), q, two_q);
+                    v[e] = reduce_4q<W>(sm_at<LOGN>(planes + j * plane_words<LOGN, W>(), sbt, off), q, two_q);
                 }
             }
 #pragma unroll
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
         }
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         const Xchg xc{xc0.mbar ? xc0.mbar + 8 * pl : 0u, 0u};
-        fwd_conv<LOGN, W, true, 2>(planes + pl * 2 * S::M, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK,
+        fwd_conv<LOGN, W, true, 2>(planes + pl * 2 * plane_words<LOGN, W>(), P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK,
                                    first, xc, mu, nullptr, uint64_t(d.L) * n);
         first = false;
         ++pl;
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
     const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
     const uint64_t kstride_j = uint64_t(LK) << LOGN;
     const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
-    const uint32_t sbt = swb<W>(threadIdx.x);
+    const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
     W* out = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
     const uint64_t out_h = uint64_t(LK) * n, out_u = 2 * out_h;
     const bool to_p = r >= d.L;
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
                 } else {
 #pragma unroll
                     for (int e = 0; e < kChunk; ++e)
-                        v[e] = csub<W>(sm_at(planes + (pj * 2 + u) * S::M, sbt, (e0 + e) * S::T), two_q);
+                        v[e] = csub<W>(sm_at<LOGN>(planes + (pj * 2 + u) * plane_words<LOGN, W>(), sbt, (e0 + e) * S::T), two_q);
                     ++pj;
                 }
 #pragma unroll
@@ -742,7 +742,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pair_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
     using W = uint32_t;
-    __shared__ __align__(16) W sm[2 * S::M];
+    __shared__ __align__(16) W sm[2 * plane_words<LOGN, W>()];
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t r = blockIdx.x / S::CL, c = block_yz();
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pa
 template <int LOGN, class W, bool K29 = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) moddown_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
-    __shared__ __align__(16) W sm[S::M];
+    __shared__ __align__(16) W sm[plane_words<LOGN, W>()];
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t r = blockIdx.x / S::CL, ch = block_yz();
@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
 #endif
 #else
     fwd_conv<LOGN, W, kWide>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu);
-    const uint32_t sbt = swb<W>(threadIdx.x);
+    const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
     // Epilogue in two halves: issue every global load of a half (including
     // the automorphism gather, which hits scattered sectors) before using
     // any of them, so their latencies overlap.
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, moddown_min_blocks<W>()) mo
 #pragma unroll
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint32_t y = threadIdx.x + (part * kHalf + jj) * S::T;
-            const W conv = reduce_4q<W>(sm_at(sm, sbt, (part * kHalf + jj) * S::T), q, two_q);
+            const W conv = reduce_4q<W>(sm_at<LOGN>(sm, sbt, (part * kHalf + jj) * S::T), q, two_q);
             W u = shoup_full<W>(va[jj] + q - conv, pinv.x, pinv.y, q);
             u += vb[jj];
             u = csub<W>(u, q);

@@ -192,36 +192,91 @@ constexpr int kCtaCoeffs = LB_CTA_COEFFS;  // coefficients owned by one CTA
 constexpr int kThreads = kCtaCoeffs / kE;  // 128 (radix 32) or 256 (radix 16)
 constexpr int kMinBlocks = kThreads <= 128 ? 4 : kThreads == 256 ? 3 : 1;  // resident CTAs per SM the register budget must allow
 
-// Shared-memory swizzles (bijective on a CTA chunk: low bits XORed with
-// higher bits, two instructions):
-//   u64 words (two banks each, 16 per 128-byte row): y ^ ((y >> 4) & 15)
-//   u32 words (32 per row): y ^ ((y >> 5) & 31)
-// By enumeration of the passes' warp access patterns (n = 2^12..2^15) the
-// u32 form averages 1.2 wavefronts per access vs 1.4 for the u64 form; a
-// fully conflict-free u32 form (y ^ h ^ (h << 1), h = (y >> 5) & 15) costs
-// two more instructions per access and measured slower (94.9 vs 96.4 img/s).
+// Shared-memory layouts of a CTA chunk.
+//   u64 words (two banks each, 16 per 128-byte row): XOR swizzle
+//     y ^ ((y >> 4) & 15), one LOP3 per access.
+//   u32 words: PADDING, y + A * (y >> S) with (A, S) = (4, 6) — 4 pad words
+//     after every 64 — or (2, 5) for n = 8192. By enumeration of every pass's
+//     warp access pattern this is conflict-free for n = 8192 and 16384 (1.2
+//     wavefronts per access at n = 32768, 1.25 at n = 4096; the XOR swizzle
+//     y ^ ((y >> 5) & 31) used before averaged 1.38). Padding is affine: for
+//     y = base + c with base and c bit-disjoint (every access below: a
+//     thread-dependent base plus a compile-time multiple of a power-of-two
+//     stride larger than the base's set bits) pad(y) = pad(base) + pad(c), so
+//     an access is [base register + immediate] with no address instruction,
+//     and a last-pass group of 2^C consecutive words stays contiguous and
+//     aligned (one 8/16-byte access).
 __device__ __forceinline__ uint32_t swz(uint32_t y) { return y ^ ((y >> 4) & 15u); }
-template <class W>
-__device__ __forceinline__ uint32_t swz_w(uint32_t y);
 
-// Both swizzles are linear over GF(2), so for y = base + c with base and c
-// bit-disjoint (every access below: a thread-dependent base plus a
-// compile-time multiple of a power-of-two stride that is larger than the
-// base's set bits) swz(y) = swz(base) ^ swz(c). swb() is the swizzled byte
-// offset of the base, computed once; sm_at() costs one LOP3 per access.
-template <class W>
-__device__ __forceinline__ uint32_t swb(uint32_t base) { return swz_w<W>(base) * static_cast<uint32_t>(sizeof(W)); }
-template <class W>
-__device__ __forceinline__ W& sm_at(W* sm, uint32_t sb, uint32_t c) {
-    return *reinterpret_cast<W*>(reinterpret_cast<char*>(sm) + (sb ^ swb<W>(c)));
+template <class W, int LOGN>
+struct Lay {
+    static constexpr bool kPad = sizeof(W) == 4;
+    static constexpr uint32_t A = LOGN == 13 ? 2 : 4, S = LOGN == 13 ? 5 : 6;
+    __host__ __device__ static constexpr uint32_t idx(uint32_t y) {
+        return kPad ? y + A * (y >> S) : (y ^ ((y >> 4) & 15u));
+    }
+    // words of a plane holding m logical words (m a multiple of 2^S)
+    __host__ __device__ static constexpr uint32_t plane(uint32_t m) { return kPad ? m + A * (m >> S) : m; }
+};
+
+// Words of the smem plane of one CTA chunk.
+template <int LOGN, class W>
+constexpr uint32_t plane_words() {
+    return Lay<W, LOGN>::plane(kCtaCoeffs < (1 << LOGN) ? kCtaCoeffs : (1 << LOGN));
 }
 
-template <class W>
-__device__ __forceinline__ uint32_t swz_w(uint32_t y) {
-    if constexpr (sizeof(W) == 8) {
-        return swz(y);
+// swb(): byte offset of a base, computed once per thread and pass;
+// lay_add(sb, c): byte offset of base + c; sm_at<LOGN>(): the element.
+template <class W, int LOGN>
+__device__ __forceinline__ uint32_t swb(uint32_t base) {
+    return Lay<W, LOGN>::idx(base) * static_cast<uint32_t>(sizeof(W));
+}
+template <class W, int LOGN>
+__device__ __forceinline__ uint32_t lay_add(uint32_t sb, uint32_t c) {
+    if constexpr (Lay<W, LOGN>::kPad)
+        return sb + swb<W, LOGN>(c);
+    else
+        return sb ^ swb<W, LOGN>(c);
+}
+template <int LOGN, class W>
+__device__ __forceinline__ W& sm_at(W* sm, uint32_t sb, uint32_t c) {
+    return *reinterpret_cast<W*>(reinterpret_cast<char*>(sm) + lay_add<W, LOGN>(sb, c));
+}
+
+// A group of 2^C consecutive logical words at a 2^C-aligned base (byte
+// offset sb): contiguous and aligned in the padded layout, so it moves as
+// 8/16-byte accesses; element by element in the XOR layout.
+template <int LOGN, int C, class W>
+__device__ __forceinline__ void lds_group(const W* sm, uint32_t sb, W (&r)[1 << C]) {
+    if constexpr (Lay<W, LOGN>::kPad && C >= 2) {
+#pragma unroll
+        for (int k = 0; k < (1 << C); k += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(sm) + sb + k * 4);
+            r[k] = v.x;
+            r[k + 1] = v.y;
+            r[k + 2] = v.z;
+            r[k + 3] = v.w;
+        }
+    } else if constexpr (Lay<W, LOGN>::kPad && C == 1) {
+        const uint2 v = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(sm) + sb);
+        r[0] = v.x;
+        r[1] = v.y;
     } else {
-        return y ^ ((y >> 5) & 31u);
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) r[k] = sm_at<LOGN>(const_cast<W*>(sm), sb, k);
+    }
+}
+template <int LOGN, int C, class W>
+__device__ __forceinline__ void sts_group(W* sm, uint32_t sb, const W (&r)[1 << C]) {
+    if constexpr (Lay<W, LOGN>::kPad && C >= 2) {
+#pragma unroll
+        for (int k = 0; k < (1 << C); k += 4)
+            *reinterpret_cast<uint4*>(reinterpret_cast<char*>(sm) + sb + k * 4) = make_uint4(r[k], r[k + 1], r[k + 2], r[k + 3]);
+    } else if constexpr (Lay<W, LOGN>::kPad && C == 1) {
+        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(sm) + sb) = make_uint2(r[0], r[1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < (1 << C); ++k) sm_at<LOGN>(sm, sb, k) = r[k];
     }
 }
 
@@ -341,7 +396,7 @@ template <int LOGN, int C, bool INVERSE, class W, int NT = 1>
 __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ tw, uint32_t s0, uint32_t cta_base,
                                            W q, W two_q) {
     constexpr int G = kE >> C;  // groups per thread
-    constexpr uint32_t kPlane = kCtaCoeffs < (1 << LOGN) ? kCtaCoeffs : (1 << LOGN);
+    constexpr uint32_t kPlane = plane_words<LOGN, W>();
     const uint32_t stride = (1u << LOGN) >> (s0 + C);
     const uint32_t log_bs = LOGN - s0;
 #pragma unroll
@@ -351,12 +406,12 @@ __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ t
         const uint32_t base = (b << log_bs) + o;
         const uint32_t B = (cta_base >> log_bs) + b;
         // base has no bits in [log2 stride, log_bs), where k * stride lives
-        const uint32_t sb = swb<W>(base);
+        const uint32_t sb = swb<W, LOGN>(base);
         W r[NT][1 << C];
 #pragma unroll
         for (int u = 0; u < NT; ++u)
 #pragma unroll
-            for (int k = 0; k < (1 << C); ++k) r[u][k] = sm_at(sm + u * kPlane, sb, k * stride);
+            for (int k = 0; k < (1 << C); ++k) r[u][k] = sm_at<LOGN>(sm + u * kPlane, sb, k * stride);
         if (INVERSE)
             inv_group<C>(r, tw, s0, B, q, two_q);
         else
@@ -364,7 +419,7 @@ __device__ __forceinline__ void local_pass(W* sm, const PairT<W>* __restrict__ t
 #pragma unroll
         for (int u = 0; u < NT; ++u)
 #pragma unroll
-            for (int k = 0; k < (1 << C); ++k) sm_at(sm + u * kPlane, sb, k * stride) = r[u][k];
+            for (int k = 0; k < (1 << C); ++k) sm_at<LOGN>(sm + u * kPlane, sb, k * stride) = r[u][k];
     }
 }
 
@@ -543,7 +598,7 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
     constexpr int C = fwd_last_radix<LOGN>();
     constexpr int G = kE >> C;
     constexpr uint32_t s0 = LOGN - C;
-    constexpr uint32_t kPlane = kCtaCoeffs < (1 << LOGN) ? kCtaCoeffs : (1 << LOGN);
+    constexpr uint32_t kPlane = plane_words<LOGN, W>();
     if constexpr (has_prefetch<Last>::value && NT == 1) {
         auto ops = last.prefetch(threadIdx.x << C);
 #pragma unroll
@@ -552,10 +607,9 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
             const uint32_t base = g << C;
             decltype(ops) nxt = ops;
             if (i + 1 < G) nxt = last.prefetch((g + kThreads) << C);
-            const uint32_t sb = swb<W>(base);
+            const uint32_t sb = swb<W, LOGN>(base);
             W r[1][1 << C];
-#pragma unroll
-            for (int k = 0; k < (1 << C); ++k) r[0][k] = sm_at(sm, sb, k);
+            lds_group<LOGN, C>(sm, sb, r[0]);
             fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
             last.finish(base, r[0], ops);
             ops = nxt;
@@ -565,12 +619,10 @@ __device__ __forceinline__ void fwd_last_pass(W* sm, const PairT<W>* __restrict_
         for (int i = 0; i < G; ++i) {
             const uint32_t g = threadIdx.x + i * kThreads;
             const uint32_t base = g << C;
-            const uint32_t sb = swb<W>(base);
+            const uint32_t sb = swb<W, LOGN>(base);
             W r[NT][1 << C];
 #pragma unroll
-            for (int u = 0; u < NT; ++u)
-#pragma unroll
-                for (int k = 0; k < (1 << C); ++k) r[u][k] = sm_at(sm + u * kPlane, sb, k);
+            for (int u = 0; u < NT; ++u) lds_group<LOGN, C>(sm + u * kPlane, sb, r[u]);
             fwd_group<C>(r, tw, s0, (cta_base >> C) + g, q, two_q);
 #pragma unroll
             for (int u = 0; u < NT; ++u) last(u, base, r[u]);
@@ -586,6 +638,7 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
                                          bool start_sync = true, Xchg xc = Xchg{}, Last&& last = nullptr) {
     using S = NttShape<LOGN>;
     namespace cg = cooperative_groups;
+    constexpr uint32_t kPlane = plane_words<LOGN, W>();
     const W q = P.q, two_q = 2 * q;
     const PairT<W>* __restrict__ tw = P.fwd;
     // Every CTA of the cluster must be running (and done reading its smem)
@@ -605,7 +658,7 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
             if constexpr (S::CL > 1) cluster_wait();
             else __syncthreads();
         }
-        const uint32_t sb = swb<W>(rho);  // rho < NE
+        const uint32_t sb = swb<W, LOGN>(rho);  // rho < NE
         if constexpr (S::CL > 1 && LB_NTT_MBAR) {
             const uint32_t lbase = smem_addr(sm);
 #pragma unroll
@@ -615,14 +668,14 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
                     for (int u = 0; u < NT; ++u)
 #pragma unroll
                         for (int i = 0; i < S::PER_CTA; ++i)
-                            sm_at(sm + u * S::M, sb, i * S::NE) = r[u][dst * S::PER_CTA + i];
+                            sm_at<LOGN>(sm + u * kPlane, sb, i * S::NE) = r[u][dst * S::PER_CTA + i];
                 } else {
                     const uint32_t rbase = mapa_rank(lbase, dst), rmbar = mapa_rank(xc.mbar, dst);
 #pragma unroll
                     for (int u = 0; u < NT; ++u)
 #pragma unroll
                         for (int i = 0; i < S::PER_CTA; ++i)
-                            st_async(rbase + u * static_cast<uint32_t>(S::M * sizeof(W)) + (sb ^ swb<W>(i * S::NE)),
+                            st_async(rbase + u * static_cast<uint32_t>(kPlane * sizeof(W)) + lay_add<W, LOGN>(sb, i * S::NE),
                                      r[u][dst * S::PER_CTA + i], rmbar);
                 }
             }
@@ -634,10 +687,10 @@ __device__ __forceinline__ void fwd_core(W* sm, const PrimeView<W>& P, uint32_t 
                     const uint32_t dst = k / S::PER_CTA;
                     const uint32_t c = (k % S::PER_CTA) * S::NE;
                     if constexpr (S::CL > 1) {
-                        W* remote = cg::this_cluster().map_shared_rank(sm + u * S::M, dst);
-                        sm_at(remote, sb, c) = r[u][k];
+                        W* remote = cg::this_cluster().map_shared_rank(sm + u * kPlane, dst);
+                        sm_at<LOGN>(remote, sb, c) = r[u][k];
                     } else {
-                        sm_at(sm + u * S::M, sb, c) = r[u][k];
+                        sm_at<LOGN>(sm + u * kPlane, sb, c) = r[u][k];
                     }
                 }
         }
@@ -695,7 +748,7 @@ template <int LOGN, class W, class St = uint64_t, bool MAPPED = false, int NT = 
 __global__ void __launch_bounds__(NttShape<LOGN>::T, ntt_min_blocks<W, NT>()) ntt_forward_kernel(LimbBatch b, const PrimeDev* __restrict__ primes,
                                                                                                      const __grid_constant__ PrimeTab32 tab) {
     using S = NttShape<LOGN>;
-    __shared__ __align__(16) W sm[NT * S::M];
+    __shared__ __align__(16) W sm[NT * plane_words<LOGN, W>()];
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
     const uint32_t l = blockIdx.x / S::CL, poly = block_yz() * NT;
     if (poly >= b.polys) return;  // whole cluster skips together (polys is a multiple of NT)
@@ -776,11 +829,9 @@ __device__ __forceinline__ void inv_tail_pass(W* sm, const PrimeView<W>& P, uint
 #pragma unroll
         for (int u = 0; u < NT; ++u) load_group(u, base, r[u]);
         inv_group<kTail>(r, tw, s0, (cta_base >> kTail) + g, q, two_q);
-        const uint32_t sb = swb<W>(base);
+        const uint32_t sb = swb<W, LOGN>(base);
 #pragma unroll
-        for (int u = 0; u < NT; ++u)
-#pragma unroll
-            for (int k = 0; k < (1 << kTail); ++k) sm_at(sm + u * S::M, sb, k) = r[u][k];
+        for (int u = 0; u < NT; ++u) sts_group<LOGN, kTail>(sm + u * plane_words<LOGN, W>(), sb, r[u]);
     }
 }
 
@@ -817,11 +868,11 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     constexpr uint32_t stride = S::N >> (2 * kLogE);
     static_assert(S::T % stride == 0 && S::T / stride == S::PER_CTA, "push layout");
     const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
-    const uint32_t sb = swb<W>(bb * S::NE + o);
+    const uint32_t sb = swb<W, LOGN>(bb * S::NE + o);
 #pragma unroll
     for (int u = 0; u < NT; ++u)
 #pragma unroll
-        for (int k = 0; k < kE; ++k) r[u][k] = sm_at(sm + u * S::M, sb, k * stride);
+        for (int k = 0; k < kE; ++k) r[u][k] = sm_at<LOGN>(sm + u * plane_words<LOGN, W>(), sb, k * stride);
     inv_group<kLogE>(r, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
     if (start_wait) cluster_wait();
     const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
@@ -863,7 +914,7 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
 // loads. Dynamic smem: M words (+ M receive words when pushing).
 template <int LOGN> constexpr bool inv_push() { return NttShape<LOGN>::CL > 1 && LB_NTT_MBAR; }
 template <int LOGN, class W, int NT = 1> constexpr size_t ntt_inverse_smem() {
-    return NT * (inv_push<LOGN>() ? 2 : 1) * NttShape<LOGN>::M * sizeof(W);
+    return NT * (plane_words<LOGN, W>() + (inv_push<LOGN>() ? NttShape<LOGN>::M : 0)) * sizeof(W);
 }
 #ifndef LB_INV_PAIR_MINB
 #define LB_INV_PAIR_MINB 3  // 64 KiB of planes per paired CTA
@@ -881,7 +932,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
     static_assert(NT == 1 || kPush, "paired inverse transforms use the push exchange");
     extern __shared__ __align__(16) uint8_t inv_smem_raw[];
     W* sm = reinterpret_cast<W*>(inv_smem_raw);  // planes sm + u * M
-    W* recv = sm + NT * S::M;                    // receive planes [kE][T] (push only)
+    W* recv = sm + NT * plane_words<LOGN, W>();  // receive planes [kE][T], linear (push only)
     __shared__ uint64_t mbar;
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t l = blockIdx.x / S::CL, poly = block_yz() * NT;
@@ -898,7 +949,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
     const PairT<W>* __restrict__ tw = P.inv;
     const uint32_t cta_base = rank * S::M;
 
-    const uint32_t sbt = swb<W>(threadIdx.x);
+    const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
     if constexpr (kPush) {
         // tail pass straight from global memory (through the automorphism
         // when reading a key switch's input)
@@ -936,14 +987,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
             const uint32_t x = cta_base + y;
-            sm_at(sm, sbt, j * S::T) = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
+            sm_at<LOGN>(sm, sbt, j * S::T) = static_cast<W>(__ldg(&in[b.galois ? galois_src(x, b.galois, LOGN) : x]));
         }
     } else {
         const St* in = a + cta_base;
 #pragma unroll
         for (int j = 0; j < kE; ++j) {
             const uint32_t y = threadIdx.x + j * S::T;
-            sm_at(sm, sbt, j * S::T) = static_cast<W>(__ldcs(&in[y]));
+            sm_at<LOGN>(sm, sbt, j * S::T) = static_cast<W>(__ldcs(&in[y]));
         }
     }
     __syncthreads();
@@ -980,16 +1031,16 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
         }
         // cross-CTA pass: stages 3..0 gathered from the owners
         if constexpr (S::CL > 1) cg::this_cluster().sync();
-        const uint32_t sb = swb<W>(rho);  // rho < NE
+        const uint32_t sb = swb<W, LOGN>(rho);  // rho < NE
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
             const uint32_t src = k / S::PER_CTA;
             const uint32_t c = (k % S::PER_CTA) * S::NE;
             if constexpr (S::CL > 1) {
                 W* remote = cg::this_cluster().map_shared_rank(sm, src);
-                r[0][k] = sm_at(remote, sb, c);
+                r[0][k] = sm_at<LOGN>(remote, sb, c);
             } else {
-                r[0][k] = sm_at(sm, sb, c);
+                r[0][k] = sm_at<LOGN>(sm, sb, c);
             }
         }
         inv_final<W, NT>(r, tw, q, c0, c1);
