@@ -609,7 +609,7 @@ def value_w64(a, net, strategy, B, imgs) -> dict:
     par = parity_check(net, imgs, scores)
     del sess
     torch.cuda.empty_cache()
-    ks = ks_roofline(cx, 16 * len(prm.t))
+    ks = ks_roofline(cx, B * len(prm.t))
     ntt = ntt_roofline(cx, B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1))
     del cx
     torch.cuda.empty_cache()
@@ -864,9 +864,10 @@ def run_ours(a, world, rank, local):
                                 "graph_parity": g_par["mismatches"] == 0}
         del one
         torch.cuda.empty_cache()
-        # roofline of the dominant unit (the key switch, at a typical plan
-        # launch size) and of its NTT component alone
-        extras["roofline"] = ks_roofline(cx, 16 * len(prm.t))
+        # roofline of the dominant unit (the key switch, at the size the plan
+        # launches it: every rotation of the step runs over all B x T
+        # ciphertexts of the batch) and of its NTT component alone
+        extras["roofline"] = ks_roofline(cx, B * len(prm.t))
         ks_limbs = B * len(prm.t) * prm.dnum * (prm.L + prm.K - 1)
         extras["roofline_ntt"] = ntt_roofline(cx, ks_limbs)
         if a.workload == "lola-mnist" and a.word == 32:

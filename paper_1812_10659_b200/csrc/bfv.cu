@@ -1132,7 +1132,10 @@ bool ks_use_tmem() {
 
 // paired key-switch kernels (29-bit fast path): bit 0 ModDown (both
 // components per cluster), bit 1 the inner product (two ciphertexts per
-// cluster); LB_KS_PAIR overrides
+// cluster), bit 2 ModDown with two target primes per cluster on top of
+// bit 0 (shared P-limb loads; off: measured slower, 1.61 vs 1.54 ms per
+// 320-ciphertext key switch — the stash and the second start barrier cost
+// more than the halved L2 reads save); LB_KS_PAIR overrides
 int ks_pairs() {
     static const int mask = [] {
         const char* e = std::getenv("LB_KS_PAIR");
@@ -1280,6 +1283,19 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if constexpr (sizeof(W) == 4) {
+        if (d.ks29 && (ks_pairs() & 4) && d.K >= 2 && d.K <= 5 && d.L >= 2) {
+            static const bool configured = [] {
+                LB_CUDA(cudaFuncSetAttribute(moddown_quad_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(moddown_quad_smem<LOGN>())));
+                return true;
+            }();
+            (void)configured;
+            cfg.gridDim = grid_xyz(((d.L + 1) / 2) * S::CL, a.count);
+            cfg.dynamicSmemBytes = moddown_quad_smem<LOGN>();
+            LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_quad_kernel<LOGN>, d, a));
+            launch_counter().fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
         if (d.ks29 && (ks_pairs() & 1)) {
             cfg.gridDim = grid_xyz(d.L * S::CL, a.count);
             LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_pair_kernel<LOGN>, d, a));
