@@ -448,8 +448,8 @@ def ntt_roofline(cx, limbs: int, reps: int = 20) -> dict:
     hbm_peak = float(_peaks().get("hbm_gbs", 6552.6))
     per_limb, src = (None, None)
     if word == 32:
-        f_b, f_s = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned int>"))
-        i_b, i_s = ncu_traffic(lambda k: k.startswith("ntt_inverse_kernel<14, unsigned int, unsigned int>"))
+        f_b, f_s = ncu_traffic(lambda k: k.startswith("ntt_forward_kernel<14, unsigned int, unsigned int"))
+        i_b, i_s = ncu_traffic(lambda k: k.startswith("ntt_inverse_kernel<14, unsigned int, unsigned int"))
         if f_b and i_b:
             per_limb, src = (f_b + i_b) / 2, f"{f_s}; {i_s}"
     return {

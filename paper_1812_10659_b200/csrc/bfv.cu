@@ -1172,8 +1172,8 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         return;
     }
     if constexpr (sizeof(W) == 4) {
-        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= 2 && d.dnum <= 2 && d.L % d.alpha == 0 &&
-            S::CL > 1) {
+        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= Context::pair_min_count() && d.dnum <= 2 &&
+            d.L % d.alpha == 0 && S::CL > 1) {
             // two ciphertexts per cluster; targets in Q have dnum - 1 foreign
             // digits, targets in P dnum: separate launches sized for each
             static bool configured_pair = false;
@@ -1296,7 +1296,7 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
             launch_counter().fetch_add(1, std::memory_order_relaxed);
             return;
         }
-        if (d.ks29 && (ks_pairs() & 1)) {
+        if (d.ks29 && (ks_pairs() & 1) && a.count >= Context::pair_min_count()) {
             cfg.gridDim = grid_xyz(d.L * S::CL, a.count);
             LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_pair_kernel<LOGN>, d, a));
             launch_counter().fetch_add(1, std::memory_order_relaxed);

@@ -141,6 +141,9 @@ public:
     // roof), bit 1 inverse (off: 64 KiB of planes leave 3 CTAs per SM, no gain);
     // LB_NTT_PAIR overrides
     static int ntt_pairs();
+    // smallest batch (polys / ciphertexts per launch) that runs the paired
+    // kernels (LB_PAIR_MIN overrides; default 32)
+    static uint32_t pair_min_count();
     // every prime of [first, first + count) is below 2^30
     bool primes_small(uint32_t first, uint32_t count) const {
         if (!tab32_.count) return false;  // no kernel-parameter table: 64-bit words

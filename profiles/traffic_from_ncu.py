@@ -4,8 +4,9 @@ for `roofline.traffic`.
 
 Units: key-switch kernels per ciphertext (the launch's ciphertext count is
 recovered from its grid: ks_inner = count*(L+K)*CL CTAs, moddown =
-count*2L*CL, input INTT = count*L*CL, P-limb INTT = count*2K*CL), NTTs per
-limb transform (grid = limbs*CL).
+count*2L*CL, input INTT = count*L*CL, P-limb INTT = count*2K*CL; the paired
+kernels cover two ciphertexts, components or limbs per cluster), NTTs per
+limb transform (grid = limbs*CL / transforms per cluster).
 
 usage: python traffic_from_ncu.py OUT.json L K CL full_1.csv full_2.csv ...
 """
@@ -40,16 +41,18 @@ def main():
     for path in sys.argv[5:]:
         for name, grid, rd, wr, dur in read(path):
             base = name.split("(")[0].replace("void ", "").replace("lb::", "").strip()
+            pair = 2 if "_pair_" in base else 1
             if "ks_inner" in base:
-                unit, per, launches = "ciphertext", grid // ((L + K) * CL), 1
+                unit, per, launches = "ciphertext", pair * grid // ((L + K) * CL), 1
             elif "moddown" in base:
-                unit, per, launches = "ciphertext", grid // (2 * L * CL), 1
-            elif "ntt_inverse_kernel" in base and base.endswith("unsigned int, unsigned int>"):
-                # the key switch's two inverse transforms (input: L limbs, P limbs of
-                # both accumulators: 2K limbs) share this instance
-                unit, per, launches = "limb", grid // CL, None
+                unit, per, launches = "ciphertext", pair * grid // (2 * L * CL), 1
             elif "ntt_" in base:
-                unit, per, launches = "limb", grid // CL, None
+                # <LOGN, word, storage, mapped, transforms per cluster>; the key
+                # switch's two inverse transforms (input: L limbs, P limbs of both
+                # accumulators: 2K limbs) share one instance
+                args = base[base.index("<") + 1:base.rindex(">")].split(",")
+                nt = int(args[4]) if len(args) > 4 else 1
+                unit, per, launches = "limb", nt * grid // CL, None
             else:
                 unit, per, launches = "launch", 1, None
             a = acc.setdefault(base, {"unit": unit, "units": 0, "bytes": 0.0, "us": 0.0, "n": 0})
@@ -65,7 +68,7 @@ def main():
     for base, v in res["kernels"].items():
         if "ks_inner" in base or "moddown" in base:
             per_ct += v["bytes_per_unit"]
-        elif "ntt_inverse_kernel" in base and base.endswith("unsigned int, unsigned int>"):
+        elif base.startswith("ntt_inverse_kernel<14, unsigned int, unsigned int"):
             per_ct += v["bytes_per_unit"] * (L + 2 * K)
     res["key_switch_bytes_per_ciphertext"] = per_ct
     json.dump(res, open(out_path, "w"), indent=1)
