@@ -1144,6 +1144,18 @@ int ks_pairs() {
     return mask;
 }
 
+// smallest launch (ciphertexts) that runs the paired key-switch kernels: below
+// it half as many clusters at 3-4 CTAs per SM under-fill the GPU (80
+// ciphertexts: 0.441 vs 0.423 ms unpaired; 320: 1.543 vs 1.553 and +3.4% on
+// the bench); LB_KS_PAIR_MIN overrides
+uint32_t ks_pair_min() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("LB_KS_PAIR_MIN");
+        return e ? static_cast<uint32_t>(std::max(2, std::atoi(e))) : 128u;
+    }();
+    return v;
+}
+
 bool ks_use_planes() {
     static const bool on = [] {
         const char* e = std::getenv("LB_KS_PLANES");
@@ -1172,7 +1184,7 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         return;
     }
     if constexpr (sizeof(W) == 4) {
-        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= Context::pair_min_count() && d.dnum <= 2 &&
+        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= ks_pair_min() && d.dnum <= 2 &&
             d.L % d.alpha == 0 && S::CL > 1) {
             // two ciphertexts per cluster; targets in Q have dnum - 1 foreign
             // digits, targets in P dnum: separate launches sized for each
@@ -1296,7 +1308,7 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
             launch_counter().fetch_add(1, std::memory_order_relaxed);
             return;
         }
-        if (d.ks29 && (ks_pairs() & 1) && a.count >= Context::pair_min_count()) {
+        if (d.ks29 && (ks_pairs() & 1) && a.count >= ks_pair_min()) {
             cfg.gridDim = grid_xyz(d.L * S::CL, a.count);
             LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_pair_kernel<LOGN>, d, a));
             launch_counter().fetch_add(1, std::memory_order_relaxed);
