@@ -1135,11 +1135,14 @@ bool ks_use_tmem() {
 // cluster), bit 2 ModDown with two target primes per cluster on top of
 // bit 0 (shared P-limb loads; off: measured slower, 1.61 vs 1.54 ms per
 // 320-ciphertext key switch — the stash and the second start barrier cost
-// more than the halved L2 reads save); LB_KS_PAIR overrides
+// more than the halved L2 reads save), bit 3 the mixed inner-product kernel
+// (pairs for the targets in Q, single ciphertexts for the targets in P: two
+// planes, 4 CTAs per SM; 1.42 vs 1.54 ms per 320-ciphertext key switch against
+// bit 1's kernel, which stays as the fallback for dnum = 1); LB_KS_PAIR overrides
 int ks_pairs() {
     static const int mask = [] {
         const char* e = std::getenv("LB_KS_PAIR");
-        return e ? std::atoi(e) : 3;
+        return e ? std::atoi(e) : 11;
     }();
     return mask;
 }
@@ -1184,6 +1187,36 @@ void launch_ks_inner(const BfvDev& d, const KsInnerArgs& a, cudaStream_t s) {
         return;
     }
     if constexpr (sizeof(W) == 4) {
+        if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 8) && a.count >= ks_pair_min() && d.dnum == 2 &&
+            d.L == 2 * d.alpha && S::CL > 1) {
+            // mixed kernel: pairs for the targets in Q, single ciphertexts for the
+            // targets in P, two planes and 4 CTAs per SM everywhere
+            KsInnerArgs ap = a;
+            ap.count = a.count & ~1u;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = grid_xyz((d.L + 2 * d.K) * S::CL, ap.count / 2);
+            cfg.blockDim = dim3(S::T);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = S::CL;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            LB_CUDA(cudaLaunchKernelEx(&cfg, ks_inner_mix_kernel<LOGN>, d, ap));
+            launch_counter().fetch_add(1, std::memory_order_relaxed);
+            if (!(a.count & 1u)) return;
+            KsInnerArgs al = a;
+            const uint32_t c = a.count - 1;
+            const size_t wb = sizeof(W);
+            al.dc = static_cast<const uint8_t*>(a.dc) + uint64_t(c) * d.L * d.n * wb;
+            al.dn = static_cast<const uint8_t*>(a.dn) + uint64_t(c) * a.d_stride * wb;
+            al.acc = static_cast<uint8_t*>(a.acc) + uint64_t(c) * 2 * (d.L + d.K) * d.n * wb;
+            al.count = 1;
+            launch_ks_inner<LOGN, W>(d, al, s);
+            return;
+        }
         if (d.ks29 && LB_WIDE_MAC && (ks_pairs() & 2) && a.count >= ks_pair_min() && d.dnum <= 2 &&
             d.L % d.alpha == 0 && S::CL > 1) {
             // two ciphertexts per cluster; targets in Q have dnum - 1 foreign

@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PLANES_MINB) ks_inner
 #ifndef LB_KS_PAIR_MINB
 #define LB_KS_PAIR_MINB 3
 #endif
+constexpr uint32_t kPairDigits = 2;  // the paired kernel covers dnum <= 2 (launch_ks_inner)
+
 template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_pair_kernel(BfvDev d, KsInnerArgs a,
                                                                                           uint32_t r_first) {
@@ -410,8 +412,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
     int own = -1;
     bool first = true;
     uint32_t pl = 0;
-    __shared__ uint64_t mbar[kMaxPlanes];
-    const Xchg xc0 = xchg_init<S::CL>(mbar, kMaxPlanes);
+    __shared__ uint64_t mbar[kPairDigits];
+    const Xchg xc0 = xchg_init<S::CL>(mbar, kPairDigits);
     for (uint32_t j = 0; j < d.dnum; ++j) {
         const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
         if (r >= lo && r < hi) {
@@ -435,10 +437,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
     constexpr int kChunk = 4;
 #pragma unroll
     for (int e0 = 0; e0 < kE; e0 += kChunk) {
-        Pr kk[kMaxPlanes][kChunk];
+        Pr kk[kPairDigits][kChunk];
         uint32_t xs[kChunk];
 #pragma unroll
-        for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+        for (uint32_t j = 0; j < kPairDigits; ++j) {
             if (j >= d.dnum) break;
 #pragma unroll
             for (int e = 0; e < kChunk; ++e) kk[j][e] = __ldg(&key[j * kstride_j + (e0 + e) * S::T]);
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
             uint64_t acc0[kChunk] = {}, acc1[kChunk] = {};
             uint32_t pj = 0;
 #pragma unroll
-            for (uint32_t j = 0; j < kMaxPlanes; ++j) {
+            for (uint32_t j = 0; j < kPairDigits; ++j) {
                 if (j >= d.dnum) break;
                 W v[kChunk];
                 if (static_cast<int>(j) == own) {
@@ -482,6 +484,115 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
                 }
                 out[u * out_u + (e0 + e) * S::T] = u0;
                 out[u * out_u + out_h + (e0 + e) * S::T] = u1;
+            }
+        }
+    }
+}
+
+// ---- mixed variant (29-bit fast path, dnum = 2) ---------------------------------------
+// Every cluster needs exactly two smem planes, so 4 CTAs fit per SM (the
+// paired kernel above needs four planes for the targets in P: 3 CTAs):
+//   targets in Q (one foreign digit + the own digit): ciphertexts 2y, 2y+1
+//     side by side, as in the paired kernel;
+//   targets in P (two foreign digits): ONE ciphertext per cluster, its two
+//     digit transforms in the two planes.
+// grid.x = CL * (L + 2K) virtual targets v: v < L is q_v for the pair;
+// v >= L is p_{(v-L)/2} for ciphertext 2y + ((v-L) & 1). grid.y/z = pairs.
+#ifndef LB_KS_MIX_MINB
+#define LB_KS_MIX_MINB 4
+#endif
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_MIX_MINB) ks_inner_mix_kernel(BfvDev d, KsInnerArgs a) {
+    using S = NttShape<LOGN>;
+    using W = uint32_t;
+    using Pr = uint2;
+    constexpr uint32_t kPlane = plane_words<LOGN, W>();
+    __shared__ __align__(16) W planes[2 * kPlane];
+    __shared__ uint64_t mbar[2];
+    const uint32_t LK = d.L + d.K;
+    const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
+    const uint32_t v = blockIdx.x / S::CL, y = block_yz();
+    if (2 * y >= a.count) return;  // whole cluster (count is even)
+    const bool in_q = v < d.L;
+    const uint32_t r = in_q ? v : d.L + ((v - d.L) >> 1);
+    const uint32_t c = 2 * y + (in_q ? 0u : ((v - d.L) & 1u));
+    const PrimeView<W> P = prime_view<W, LOGN>(d.tab32, d.primes, r);
+    const W q = P.q, two_q = 2 * q, four_q = 4 * q;
+    const uint64_t n = 1ull << LOGN;
+    const uint32_t xt = rank * S::M + threadIdx.x;
+    const uint32_t mu = d.mu60[r];
+    const Xchg xc0 = xchg_init<S::CL>(mbar, 2);
+    const Pr* key = static_cast<const Pr*>(a.key) + (uint64_t(r) << LOGN) + xt;
+    const uint64_t kstride_j = uint64_t(LK) << LOGN;
+    const uint32_t sbt = swb<W, LOGN>(threadIdx.x);
+    W* out = static_cast<W*>(a.acc) + (uint64_t(c) * 2 * LK + r) * n + xt;
+    const uint64_t out_h = uint64_t(LK) * n;
+    constexpr int kChunk = 4;
+    if (in_q) {
+        // one foreign digit (pair of transforms in the two planes) + the own digit
+        const uint32_t own = r / d.alpha, fj = own ^ 1u;
+        const uint32_t lo = fj * d.alpha, hi = min(d.L, lo + d.alpha);
+        const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
+        fwd_conv<LOGN, W, true, 2>(planes, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, true,
+                                   Xchg{xc0.mbar, 0u}, mu, nullptr, uint64_t(d.L) * n);
+        const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
+        const uint64_t out_u = 2 * out_h;
+#pragma unroll
+        for (int e0 = 0; e0 < kE; e0 += kChunk) {
+            Pr ko[kChunk], kf[kChunk];
+            uint32_t xs[kChunk];
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                ko[e] = __ldg(&key[own * kstride_j + (e0 + e) * S::T]);
+                kf[e] = __ldg(&key[fj * kstride_j + (e0 + e) * S::T]);
+                const uint32_t x = xt + (e0 + e) * S::T;
+                xs[e] = a.d_galois ? galois_src(x, a.d_galois, LOGN) : x;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                W vo[kChunk], vf[kChunk];
+#pragma unroll
+                for (int e = 0; e < kChunk; ++e) {
+                    vo[e] = __ldg(&(dn + u * a.d_stride)[xs[e]]);
+                    vf[e] = csub<W>(sm_at<LOGN>(planes + u * kPlane, sbt, (e0 + e) * S::T), two_q);
+                }
+#pragma unroll
+                for (int e = 0; e < kChunk; ++e) {
+                    const uint64_t a0 = static_cast<uint64_t>(vo[e]) * ko[e].x + static_cast<uint64_t>(vf[e]) * kf[e].x;
+                    const uint64_t a1 = static_cast<uint64_t>(vo[e]) * ko[e].y + static_cast<uint64_t>(vf[e]) * kf[e].y;
+                    // Q limbs leave lazily (< 6 q_r: ModDown's epilogue multiplies them)
+                    out[u * out_u + (e0 + e) * S::T] = barrett61_lazy(a0, mu, two_q);
+                    out[u * out_u + out_h + (e0 + e) * S::T] = barrett61_lazy(a1, mu, two_q);
+                }
+            }
+        }
+    } else {
+        // two foreign digits of one ciphertext, one plane each
+#pragma unroll
+        for (uint32_t j = 0; j < 2; ++j) {
+            const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
+            const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
+            fwd_conv<LOGN, W, true>(planes + j * kPlane, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK,
+                                    j == 0, Xchg{xc0.mbar ? xc0.mbar + 8 * j : 0u, 0u}, mu);
+        }
+#pragma unroll
+        for (int e0 = 0; e0 < kE; e0 += kChunk) {
+            Pr k0[kChunk], k1[kChunk];
+            W v0[kChunk], v1[kChunk];
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                k0[e] = __ldg(&key[(e0 + e) * S::T]);
+                k1[e] = __ldg(&key[kstride_j + (e0 + e) * S::T]);
+                v0[e] = csub<W>(sm_at<LOGN>(planes, sbt, (e0 + e) * S::T), two_q);
+                v1[e] = csub<W>(sm_at<LOGN>(planes + kPlane, sbt, (e0 + e) * S::T), two_q);
+            }
+#pragma unroll
+            for (int e = 0; e < kChunk; ++e) {
+                const uint64_t a0 = static_cast<uint64_t>(v0[e]) * k0[e].x + static_cast<uint64_t>(v1[e]) * k1[e].x;
+                const uint64_t a1 = static_cast<uint64_t>(v0[e]) * k0[e].y + static_cast<uint64_t>(v1[e]) * k1[e].y;
+                // P limbs below 2p: the inverse transform's input range
+                out[(e0 + e) * S::T] = csub<W>(csub<W>(barrett61_lazy(a0, mu, two_q), four_q), two_q);
+                out[out_h + (e0 + e) * S::T] = csub<W>(csub<W>(barrett61_lazy(a1, mu, two_q), four_q), two_q);
             }
         }
     }
