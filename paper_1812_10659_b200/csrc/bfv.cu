@@ -1328,16 +1328,31 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if constexpr (sizeof(W) == 4) {
-        if (d.ks29 && (ks_pairs() & 4) && d.K >= 2 && d.K <= 5 && d.L >= 2) {
-            static const bool configured = [] {
-                LB_CUDA(cudaFuncSetAttribute(moddown_quad_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(moddown_quad_smem<LOGN>())));
-                return true;
-            }();
-            (void)configured;
-            cfg.gridDim = grid_xyz(((d.L + 1) / 2) * S::CL, a.count);
-            cfg.dynamicSmemBytes = moddown_quad_smem<LOGN>();
-            LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_quad_kernel<LOGN>, d, a));
+        if (d.ks29 && (ks_pairs() & (4 | 16)) && d.K >= 2 && d.K <= 5 && d.L >= 2) {
+            // two target primes per cluster (bit 2: with both components; bit 4: one component)
+            if (ks_pairs() & 16) {
+                static const bool configured = [] {
+                    LB_CUDA(cudaFuncSetAttribute(moddown_quad_kernel<LOGN, 1>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(moddown_quad_smem<LOGN, 1>())));
+                    return true;
+                }();
+                (void)configured;
+                cfg.gridDim = grid_xyz(((d.L + 1) / 2) * S::CL, uint64_t(a.count) * 2);
+                cfg.dynamicSmemBytes = moddown_quad_smem<LOGN, 1>();
+                LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_quad_kernel<LOGN, 1>, d, a));
+            } else {
+                static const bool configured = [] {
+                    LB_CUDA(cudaFuncSetAttribute(moddown_quad_kernel<LOGN, 2>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(moddown_quad_smem<LOGN, 2>())));
+                    return true;
+                }();
+                (void)configured;
+                cfg.gridDim = grid_xyz(((d.L + 1) / 2) * S::CL, a.count);
+                cfg.dynamicSmemBytes = moddown_quad_smem<LOGN, 2>();
+                LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_quad_kernel<LOGN, 2>, d, a));
+            }
             launch_counter().fetch_add(1, std::memory_order_relaxed);
             return;
         }

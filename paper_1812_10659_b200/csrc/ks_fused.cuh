@@ -895,11 +895,15 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pa
 #ifndef LB_MD_QUAD_MINB
 #define LB_MD_QUAD_MINB 3
 #endif
-template <int LOGN> constexpr size_t moddown_quad_smem() {
-    return (2 * plane_words<LOGN, uint32_t>() + 2 * NttShape<LOGN>::M) * sizeof(uint32_t);
+#ifndef LB_MD_RPAIR_MINB
+#define LB_MD_RPAIR_MINB 5
+#endif
+// NT = 2: both components (the quad); NT = 1: one component, two targets
+template <int LOGN, int NT> constexpr size_t moddown_quad_smem() {
+    return NT * (plane_words<LOGN, uint32_t>() + NttShape<LOGN>::M) * sizeof(uint32_t);
 }
 
-template <int A, int LOGN, class Last>
+template <int A, int LOGN, int NT, class Last>
 __device__ __forceinline__ void md_quad_first(uint32_t* planes, uint32_t* stash, const PrimeView<uint32_t>& P1,
                                               uint32_t q2, uint32_t mu1, uint32_t mu2, uint32_t rank,
                                               const uint32_t* __restrict__ accp, uint64_t comp_stride,
@@ -913,7 +917,7 @@ __device__ __forceinline__ void md_quad_first(uint32_t* planes, uint32_t* stash,
         w2[i] = w[i * w_stride + 1].x;
     }
     const uint32_t q1 = P1.q;
-    fwd_core<LOGN, 2>(planes, P1, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
+    fwd_core<LOGN, NT>(planes, P1, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
         const uint32_t* s0 = accp + u * comp_stride + rho;
         uint32_t v[A];
 #pragma unroll
@@ -929,38 +933,43 @@ __device__ __forceinline__ void md_quad_first(uint32_t* planes, uint32_t* stash,
     }, true, xc, last);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_QUAD_MINB) moddown_quad_kernel(BfvDev d, ModDownArgs a) {
+// NT = 2: grid.y/z = ciphertexts (both components per cluster);
+// NT = 1: grid.y/z = ciphertext x component.
+template <int LOGN, int NT>
+__global__ void __launch_bounds__(NttShape<LOGN>::T, NT == 2 ? LB_MD_QUAD_MINB : LB_MD_RPAIR_MINB)
+    moddown_quad_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
     using W = uint32_t;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     W* planes = reinterpret_cast<W*>(smem_raw);
-    W* stash = planes + 2 * plane_words<LOGN, W>();  // [2][kE][T], thread-private columns
+    W* stash = planes + NT * plane_words<LOGN, W>();  // [NT][kE][T], thread-private columns
     const uint32_t LK = d.L + d.K;
     const uint32_t rank = S::CL > 1 ? cluster_rank() : 0;
-    const uint32_t r1 = 2 * (blockIdx.x / S::CL), c = block_yz();
+    const uint32_t r1 = 2 * (blockIdx.x / S::CL), yz = block_yz();
+    const uint32_t c = NT == 2 ? yz : yz >> 1, h0 = NT == 2 ? 0u : (yz & 1u);
     if (c >= a.count) return;  // whole cluster
     const bool two = r1 + 1 < d.L;
     const uint32_t r2 = two ? r1 + 1 : r1;
     const PrimeView<W> P1 = prime_view<W, LOGN>(d.tab32, d.primes, r1);
     const PrimeView<W> P2 = prime_view<W, LOGN>(d.tab32, d.primes, r2);
     const uint64_t n = 1ull << LOGN, comp = uint64_t(LK) * n;
-    const W* accp = static_cast<const W*>(a.acc) + (uint64_t(c) * 2 * LK + d.L) * n;
+    const W* accp = static_cast<const W*>(a.acc) + ((uint64_t(c) * 2 + h0) * LK + d.L) * n;
     __shared__ uint64_t mbar;
     Xchg xc = xchg_init<S::CL>(&mbar, 1);
     const uint32_t cta_base = rank * S::M;
-    const W* accq = static_cast<const W*>(a.acc) + uint64_t(c) * 2 * LK * n;
+    const W* accq = static_cast<const W*>(a.acc) + (uint64_t(c) * 2 + h0) * LK * n;
     const uint64_t lo = c * a.add_stride, ls = c * a.sum_stride, oo = c * a.out_stride;
     const PairT<W>* pinvs = static_cast<const PairT<W>*>(a.p_inv);
-    // epilogue of component u at prime r
+    // epilogue of component h0 + u at prime r
     auto finish = [&](uint32_t u, uint32_t r, W q, uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) {
         const uint64_t ro = uint64_t(r) << LOGN;
-        const W* add = static_cast<const W*>(u ? a.add1 : a.add0);
-        const W* sum = static_cast<const W*>(u ? a.sum1 : a.sum0);
+        const bool h = (h0 + u) != 0;
+        const W* add = static_cast<const W*>(h ? a.add1 : a.add0);
+        const W* sum = static_cast<const W*>(h ? a.sum1 : a.sum0);
         const MdEpilogue<LOGN, W> ep{accq + u * comp + ro,
                                      add ? add + lo + ro : nullptr,
                                      sum ? sum + ls + ro : nullptr,
-                                     static_cast<W*>(u ? a.out1 : a.out0) + oo + ro,
+                                     static_cast<W*>(h ? a.out1 : a.out0) + oo + ro,
                                      cta_base, a.add_galois, pinvs[r], q};
         ep.finish(base, rr, ep.prefetch(base));
     };
@@ -968,15 +977,15 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_QUAD_MINB) moddown_qu
     const uint32_t mu1 = d.mu60[r1], mu2 = d.mu60[r2];
     auto last1 = [&](uint32_t u, uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { finish(u, r1, P1.q, base, rr); };
     switch (d.K) {
-        case 2: md_quad_first<2, LOGN>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
-        case 3: md_quad_first<3, LOGN>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
-        case 4: md_quad_first<4, LOGN>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
-        default: md_quad_first<5, LOGN>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
+        case 2: md_quad_first<2, LOGN, NT>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
+        case 3: md_quad_first<3, LOGN, NT>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
+        case 4: md_quad_first<4, LOGN, NT>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
+        default: md_quad_first<5, LOGN, NT>(planes, stash, P1, P2.q, mu1, mu2, rank, accp, comp, w, d.L, xc, last1); break;
     }
     if (!two) return;  // whole cluster
     xc.parity ^= 1;
     const W four_q2 = 4 * P2.q;
-    fwd_core<LOGN, 2>(planes, P2, rank, [&](uint32_t u, uint32_t, uint32_t off) {
+    fwd_core<LOGN, NT>(planes, P2, rank, [&](uint32_t u, uint32_t, uint32_t off) {
         return csub<W>(stash[(u * kE + off / S::NE) * S::T + threadIdx.x], four_q2);
     }, true, xc, [&](uint32_t u, uint32_t base, W(&rr)[1 << fwd_last_radix<LOGN>()]) { finish(u, r2, P2.q, base, rr); });
 }
