@@ -907,17 +907,88 @@ __device__ __forceinline__ void inv_core_push(W* sm, W* recv, uint32_t mbar, uin
     inv_final<W, NT>(r, tw, q, c0, c1);
 }
 
+// Paired push core on THREE planes (two chunks + one receive plane, 4 CTAs
+// per SM instead of 3): the second transform's receive plane aliases the
+// first transform's chunk, which is dead once every thread of the cluster has
+// read it in its push pass — a second cluster barrier says so (arrive after
+// the reads, wait before the second push, its latency behind the second
+// transform's butterflies). The tail and local passes and the final stages
+// stay paired (shared twiddles); the two push passes run one after the other.
+// `mbar`: two consecutive mbarriers (count = threads), phase 0.
+template <int LOGN, class W>
+__device__ __forceinline__ void inv_core_push_alias(W* sm, W* recv0, uint32_t mbar, const PrimeView<W>& P,
+                                                    uint32_t rank, PairT<W> c0, PairT<W> c1, W (&r)[2][kE]) {
+    using S = NttShape<LOGN>;
+    static_assert(S::CL > 1, "push exchange needs a cluster");
+    const W q = P.q, two_q = 2 * q;
+    const PairT<W>* __restrict__ tw = P.inv;
+    const uint32_t cta_base = rank * S::M;
+    constexpr int kTail = (LOGN - kLogE) % kLogE;
+    static_assert(kTail > 0, "cluster limbs have a tail pass");
+    constexpr uint32_t kPlane = plane_words<LOGN, W>();
+    static_assert(kPlane >= S::M, "receive plane fits a chunk plane");
+#pragma unroll
+    for (int s0 = LOGN - kTail - kLogE; s0 >= 2 * kLogE; s0 -= kLogE) {
+        local_pass<LOGN, kLogE, true, W, 2>(sm, tw, s0, cta_base, q, two_q);
+        __syncthreads();
+    }
+    constexpr uint32_t stride = S::N >> (2 * kLogE);
+    static_assert(S::T % stride == 0 && S::T / stride == S::PER_CTA, "push layout");
+    const uint32_t bb = threadIdx.x / stride, o = threadIdx.x % stride;
+    const uint32_t sb = swb<W, LOGN>(bb * S::NE + o);
+    const uint32_t slot = (rank * S::PER_CTA + bb) * S::T + o;
+    constexpr uint32_t kRemoteBytes = (S::CL - 1) * S::T * S::PER_CTA * sizeof(W);
+    W* recv1 = sm;  // transform 1 lands in transform 0's chunk plane
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        W(&x)[1][kE] = reinterpret_cast<W(&)[1][kE]>(r[u]);
+#pragma unroll
+        for (int k = 0; k < kE; ++k) x[0][k] = sm_at<LOGN>(sm + u * kPlane, sb, k * stride);
+        inv_group<kLogE>(x, tw, kLogE, (cta_base >> (LOGN - kLogE)) + bb, q, two_q);
+        cluster_wait();  // u = 0: peers' mbarriers are initialised; u = 1: every chunk-0 read of the cluster is done
+        W* recv = u ? recv1 : recv0;
+        const uint32_t mb = mbar + 8 * u;
+        const uint32_t lrecv = smem_addr(recv + slot);
+#pragma unroll
+        for (int dst = 0; dst < S::CL; ++dst) {
+            if (dst == static_cast<int>(rank)) {
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i) recv[slot + i * stride] = x[0][dst * S::PER_CTA + i];
+            } else {
+                const uint32_t rb = mapa_rank(lrecv, dst), rm = mapa_rank(mb, dst);
+#pragma unroll
+                for (int i = 0; i < S::PER_CTA; ++i)
+                    st_async(rb + i * stride * static_cast<uint32_t>(sizeof(W)), x[0][dst * S::PER_CTA + i], rm);
+            }
+        }
+        if (threadIdx.x == 0)
+            mbar_arrive_tx(mb, kRemoteBytes);
+        else
+            mbar_arrive(mb);
+        if (u == 0) cluster_arrive_relaxed();
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        mbar_wait(mbar + 8 * u, 0);
+        const W* recv = u ? recv1 : recv0;
+#pragma unroll
+        for (int k = 0; k < kE; ++k) r[u][k] = recv[k * S::T + threadIdx.x];
+    }
+    inv_final<W, 2>(r, tw, q, c0, c1);
+}
+
 // Inverse transform. With LB_NTT_MBAR the cross-CTA pass is push-based: the
 // last local pass (stages 7..4) sends its outputs straight from registers to
 // the owning CTA's receive plane (st.async + complete_tx), so the owner waits
 // on its own mbarrier instead of two cluster-wide barriers around remote
 // loads. Dynamic smem: M words (+ M receive words when pushing).
 template <int LOGN> constexpr bool inv_push() { return NttShape<LOGN>::CL > 1 && LB_NTT_MBAR; }
+// (paired: two chunk planes and ONE receive plane, inv_core_push_alias)
 template <int LOGN, class W, int NT = 1> constexpr size_t ntt_inverse_smem() {
-    return NT * (plane_words<LOGN, W>() + (inv_push<LOGN>() ? NttShape<LOGN>::M : 0)) * sizeof(W);
+    return (NT * plane_words<LOGN, W>() + (inv_push<LOGN>() ? NttShape<LOGN>::M : 0)) * sizeof(W);
 }
 #ifndef LB_INV_PAIR_MINB
-#define LB_INV_PAIR_MINB 3  // 64 KiB of planes per paired CTA
+#define LB_INV_PAIR_MINB 4  // 51 KiB per paired CTA
 #endif
 template <class W, int NT> constexpr int inv_min_blocks() {
     return NT == 1 ? ntt_min_blocks<W>() : LB_INV_PAIR_MINB;
@@ -933,14 +1004,14 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
     extern __shared__ __align__(16) uint8_t inv_smem_raw[];
     W* sm = reinterpret_cast<W*>(inv_smem_raw);  // planes sm + u * M
     W* recv = sm + NT * plane_words<LOGN, W>();  // receive planes [kE][T], linear (push only)
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar[NT];
     const uint32_t rank = S::CL > 1 ? cg::this_cluster().block_rank() : 0;
     const uint32_t l = blockIdx.x / S::CL, poly = block_yz() * NT;
     if (poly >= b.polys) return;  // whole cluster skips together (polys is a multiple of NT)
     const int pidx = prime_index<MAPPED>(b, poly, l);
     if (pidx < 0) return;
     if constexpr (kPush) {
-        xchg_init<S::CL>(&mbar, 1);
+        xchg_init<S::CL>(mbar, NT);
         cluster_arrive_relaxed();  // peers may push once every mbarrier is initialised
     }
     const PrimeView<W> P = prime_view<W, LOGN>(tab, primes, pidx);
@@ -1016,7 +1087,10 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, inv_min_blocks<W, NT>()) nt
     const uint32_t rho = rank * S::T + threadIdx.x;
     W r[NT][kE];
     if constexpr (kPush) {
-        inv_core_push<LOGN, W, NT>(sm, recv, smem_addr(&mbar), 0, P, rank, c0, c1, true, r);
+        if constexpr (NT == 2)
+            inv_core_push_alias<LOGN, W>(sm, recv, smem_addr(mbar), P, rank, c0, c1, r);
+        else
+            inv_core_push<LOGN, W, NT>(sm, recv, smem_addr(mbar), 0, P, rank, c0, c1, true, r);
     } else {
         // local passes in reverse: the last (possibly short) chunk first
         constexpr int kTail = (LOGN - kLogE) % kLogE;

@@ -20,3 +20,13 @@ def test_ciphertext_tests_through_paired_kernels():
                         "tests/test_sweep_gpu.py", "-m", "gpu", "-x", "-q"], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_paired_inverse_transforms():
+    """LB_NTT_PAIR=3 adds the paired inverse NTT (three smem planes, the second
+    receive plane aliasing the first chunk behind a cluster barrier)."""
+    env = dict(os.environ, LB_PAIR_MIN="2", LB_KS_PAIR_MIN="2", LB_NTT_PAIR="3")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_bfv_gpu.py", "tests/test_sweep_gpu.py", "-m", "gpu",
+                        "-x", "-q"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
