@@ -65,6 +65,9 @@ struct Wide29 {
 #ifndef LB_WIDE_CONV
 #define LB_WIDE_CONV 1
 #endif
+#ifndef LB_MD_L2PF
+#define LB_MD_L2PF 1  // bulk L2 prefetch of operands read late from HBM (key switch 1.421 -> 1.408 ms)
+#endif
 #ifndef LB_WIDE_MAC
 #define LB_WIDE_MAC 1  // packed Shoup-free keys; BfvDev::ks29 contexts store them (bfv.cu ensure_key)
 #endif
@@ -532,11 +535,22 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_MIX_MINB) ks_inner_mi
         // one foreign digit (pair of transforms in the two planes) + the own digit
         const uint32_t own = r / d.alpha, fj = own ^ 1u;
         const uint32_t lo = fj * d.alpha, hi = min(d.L, lo + d.alpha);
+        const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
+        const uint64_t out_u = 2 * out_h;
+#if LB_MD_L2PF
+        // the own digit's evaluations (the input ciphertext, in HBM) are only
+        // read after the transform: bulk L2 prefetch of this CTA's chunk of
+        // both ciphertexts (the automorphism maps a chunk into one chunk)
+        if (threadIdx.x == 0) {
+            const uint32_t cb = rank * S::M;
+            const uint32_t gb = a.d_galois ? (galois_src(cb, a.d_galois, LOGN) & ~uint32_t(S::M - 1)) : cb;
+            prefetch_l2(dn + gb, S::M * sizeof(W));
+            prefetch_l2(dn + a.d_stride + gb, S::M * sizeof(W));
+        }
+#endif
         const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
         fwd_conv<LOGN, W, true, 2>(planes, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK, true,
                                    Xchg{xc0.mbar, 0u}, mu, nullptr, uint64_t(d.L) * n);
-        const W* dn = static_cast<const W*>(a.dn) + c * a.d_stride + (uint64_t(r) << LOGN);
-        const uint64_t out_u = 2 * out_h;
 #pragma unroll
         for (int e0 = 0; e0 < kE; e0 += kChunk) {
             Pr ko[kChunk], kf[kChunk];
@@ -849,6 +863,7 @@ struct MdEpilogue {
 #ifndef LB_MD_PAIR_MINB
 #define LB_MD_PAIR_MINB 4
 #endif
+
 template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pair_kernel(BfvDev d, ModDownArgs a) {
     using S = NttShape<LOGN>;
@@ -874,6 +889,22 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_MD_PAIR_MINB) moddown_pa
     const uint64_t oo = c * a.out_stride + (uint64_t(r) << LOGN);
     const PairT<W> pinv = static_cast<const PairT<W>*>(a.p_inv)[r];
     const uint32_t mu = d.mu60[r];
+#if LB_MD_L2PF
+    // the epilogue's operands come from HBM (the accumulators and the addends
+    // were written a kernel or more ago): one bulk L2 prefetch per operand
+    // chunk at entry, so the last pass finds them in L2. The automorphism maps
+    // this CTA's chunk of positions into ONE chunk of the addend.
+    if (threadIdx.x == 0) {
+        constexpr uint32_t kBytes = S::M * sizeof(W);
+        prefetch_l2(accq + cta_base, kBytes);
+        prefetch_l2(accq + uint64_t(LK) * n + cta_base, kBytes);
+        if (sum0) prefetch_l2(sum0 + cta_base, kBytes);
+        if (sum1) prefetch_l2(sum1 + cta_base, kBytes);
+        const uint32_t gb = a.add_galois ? (galois_src(cta_base, a.add_galois, LOGN) & ~uint32_t(S::M - 1)) : cta_base;
+        if (add0) prefetch_l2(add0 + gb, kBytes);
+        if (add1) prefetch_l2(add1 + gb, kBytes);
+    }
+#endif
     const MdEpilogue<LOGN, W> ep0{accq, add0, sum0, static_cast<W*>(a.out0) + oo, cta_base, a.add_galois, pinv, q};
     const MdEpilogue<LOGN, W> ep1{accq + uint64_t(LK) * n, add1, sum1, static_cast<W*>(a.out1) + oo, cta_base, a.add_galois, pinv, q};
     fwd_conv<LOGN, W, true, 2>(sm, P, rank, accp, d.K, KsTables<W>::phat(d) + r, d.L, true, xc, mu,
