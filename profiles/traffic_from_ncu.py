@@ -42,7 +42,10 @@ def main():
         for name, grid, rd, wr, dur in read(path):
             base = name.split("(")[0].replace("void ", "").replace("lb::", "").strip()
             pair = 2 if "_pair_" in base else 1
-            if "ks_inner" in base:
+            if "ks_inner_mix" in base:
+                # grid.x covers L + 2K virtual targets, grid.y ciphertext pairs
+                unit, per, launches = "ciphertext", 2 * grid // ((L + 2 * K) * CL), 1
+            elif "ks_inner" in base:
                 unit, per, launches = "ciphertext", pair * grid // ((L + K) * CL), 1
             elif "moddown" in base:
                 unit, per, launches = "ciphertext", pair * grid // (2 * L * CL), 1

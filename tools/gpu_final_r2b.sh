@@ -14,7 +14,7 @@ for f in mnist small cifar simd ref; do python -c "
 import json;d=json.loads(open('gpurun_out/r02_bench_$f.jsonl').read().strip().splitlines()[-1])
 print('$f', round(d.get('value',0),3), (d.get('e2e') or {}).get('value'), d.get('parity'), d.get('config',{}).get('workload'), (d.get('clocks') or {}).get('reasons'), (d.get('roofline') or {}).get('frac'), (d.get('roofline_ntt') or {}).get('frac'))"; done
 python tools/pipes.py > gpurun_out/r02_pipes.json 2>&1
-bash tools/gpu_profile.sh 64 "ks_inner_pair moddown_pair ntt_inverse_kernel" > gpurun_out/prof64.log 2>&1; echo "profile rc=$?"
+bash tools/gpu_profile.sh 64 "ks_inner_mix moddown_pair ntt_inverse_kernel" > gpurun_out/prof64.log 2>&1; echo "profile rc=$?"
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k "regex:ntt_" -c 2 -o /tmp/prof_ntt python tools/ntt_launch.py > gpurun_out/ncu_ntt.log 2>&1; echo "ncu ntt rc=$?"
 ncu -i /tmp/prof_ntt.ncu-rep --page raw --csv > gpurun_out/full_ntt.csv
