@@ -84,7 +84,8 @@ struct Wide29 {
 template <int A, bool WIDE, int LOGN, int NT, class W, class St, class Last = std::nullptr_t>
 __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_t rank, const St* __restrict__ src,
                                            const PairT<W>* w, uint32_t w_stride, bool start_sync, Xchg xc,
-                                           uint32_t mu, uint64_t pair_stride, Last&& last = nullptr) {
+                                           uint32_t mu, uint64_t pair_stride, Last&& last = nullptr,
+                                           uint32_t w_pair = 0) {
     const W q = P.q, two_q = 2 * q;
     constexpr uint64_t n = 1ull << LOGN;
     if constexpr (A == 1) {
@@ -93,18 +94,22 @@ __device__ __forceinline__ void fwd_conv_n(W* sm, const PrimeView<W>& P, uint32_
         }, start_sync, xc, last);
     } else if constexpr (WIDE && sizeof(W) == 4) {
         static_assert(A <= 8, "wide accumulation holds at most 8 products below 2^58");
-        uint32_t ww[A];
+        // (w_pair: transform u uses the weights at w + u * w_pair — two digits
+        // of one ciphertext to the same target prime; 0: the same weights)
+        uint32_t ww[NT][A];
 #pragma unroll
-        for (int i = 0; i < A; ++i) ww[i] = w[i * w_stride].x;
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int i = 0; i < A; ++i) ww[u][i] = w[u * w_pair + i * w_stride].x;
         const uint32_t four_q = 4 * q;
         fwd_core<LOGN, NT>(sm, P, rank, [&](uint32_t u, uint32_t rho, uint32_t off) {
             const St* s0 = src + u * pair_stride + rho;
             uint32_t v[A];
 #pragma unroll
             for (int i = 0; i < A; ++i) v[i] = static_cast<uint32_t>(__ldg(&s0[i * n + off]));
-            uint64_t acc = static_cast<uint64_t>(v[0]) * ww[0];
+            uint64_t acc = static_cast<uint64_t>(v[0]) * ww[u][0];
 #pragma unroll
-            for (int i = 1; i < A; ++i) acc += static_cast<uint64_t>(v[i]) * ww[i];
+            for (int i = 1; i < A; ++i) acc += static_cast<uint64_t>(v[i]) * ww[u][i];
             return csub<uint32_t>(barrett61_lazy(acc, mu, two_q), four_q);
         }, start_sync, xc, last);
     } else {
@@ -131,17 +136,17 @@ template <int LOGN, class W, bool WIDE = false, int NT = 1, class St, class Last
 __device__ __forceinline__ void fwd_conv(W* sm, const PrimeView<W>& P, uint32_t rank, const St* src, uint32_t A,
                                          const PairT<W>* w, uint32_t w_stride, bool start_sync = true,
                                          Xchg xc = Xchg{}, uint32_t mu = 0, Last&& last = nullptr,
-                                         uint64_t pair_stride = 0) {
+                                         uint64_t pair_stride = 0, uint32_t w_pair = 0) {
     switch (A) {
-        case 1: fwd_conv_n<1, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break;
-        case 2: fwd_conv_n<2, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break;
+        case 1: fwd_conv_n<1, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last, w_pair); break;
+        case 2: fwd_conv_n<2, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last, w_pair); break;
         // (64-bit words: unrolling 3 and 4 costs registers the common
         // K, alpha <= 2 configurations need)
-        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; }
+        case 3: if constexpr (sizeof(W) == 4) { fwd_conv_n<3, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last, w_pair); break; }
         [[fallthrough]];
-        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; } }
+        case 4: if constexpr (sizeof(W) == 4) { if (A == 4) { fwd_conv_n<4, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last, w_pair); break; } }
         [[fallthrough]];
-        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last); break; } }
+        case 5: if constexpr (sizeof(W) == 4) { if (A == 5) { fwd_conv_n<5, WIDE, LOGN, NT, W, St>(sm, P, rank, src, w, w_stride, start_sync, xc, mu, pair_stride, last, w_pair); break; } }
         [[fallthrough]];
         default: {
             const W q = P.q, two_q = 2 * q;
@@ -498,7 +503,8 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_PAIR_MINB) ks_inner_p
 //   targets in Q (one foreign digit + the own digit): ciphertexts 2y, 2y+1
 //     side by side, as in the paired kernel;
 //   targets in P (two foreign digits): ONE ciphertext per cluster, its two
-//     digit transforms in the two planes.
+//     digit transforms side by side in the two planes (same prime: they
+//     pair up like two ciphertexts do).
 // grid.x = CL * (L + 2K) virtual targets v: v < L is q_v for the pair;
 // v >= L is p_{(v-L)/2} for ciphertext 2y + ((v-L) & 1). grid.y/z = pairs.
 #ifndef LB_KS_MIX_MINB
@@ -581,14 +587,12 @@ __global__ void __launch_bounds__(NttShape<LOGN>::T, LB_KS_MIX_MINB) ks_inner_mi
             }
         }
     } else {
-        // two foreign digits of one ciphertext, one plane each
-#pragma unroll
-        for (uint32_t j = 0; j < 2; ++j) {
-            const uint32_t lo = j * d.alpha, hi = min(d.L, lo + d.alpha);
-            const W* src = static_cast<const W*>(a.dc) + (uint64_t(c) * d.L + lo) * n;
-            fwd_conv<LOGN, W, true>(planes + j * kPlane, P, rank, src, hi - lo, KsTables<W>::dhat(d) + lo * LK + r, LK,
-                                    j == 0, Xchg{xc0.mbar ? xc0.mbar + 8 * j : 0u, 0u}, mu);
-        }
+        // two foreign digits of one ciphertext, one plane each: both go to
+        // the same prime, so they run as a transform pair too (u = digit; its
+        // alpha source limbs and conversion weights follow digit 0's)
+        const W* src = static_cast<const W*>(a.dc) + uint64_t(c) * d.L * n;
+        fwd_conv<LOGN, W, true, 2>(planes, P, rank, src, d.alpha, KsTables<W>::dhat(d) + r, LK, true,
+                                   Xchg{xc0.mbar, 0u}, mu, nullptr, uint64_t(d.alpha) * n, d.alpha * LK);
 #pragma unroll
         for (int e0 = 0; e0 < kE; e0 += kChunk) {
             Pr k0[kChunk], k1[kChunk];
