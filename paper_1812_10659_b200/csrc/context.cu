@@ -266,7 +266,7 @@ bool Context::word32_enabled() {
 int Context::ntt_pairs() {
     static const int mask = [] {
         const char* e = std::getenv("LB_NTT_PAIR");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 3;
     }();
     return mask;
 }

@@ -137,9 +137,9 @@ public:
     // the transform then runs on 32-bit words
     bool batch_word32(const LimbBatch& b) const;
     static bool word32_enabled();
-    // paired 32-bit transforms: bit 0 forward (default on: 0.55 -> 0.63 of the
-    // roof), bit 1 inverse (three planes, 4 CTAs per SM: 0.51 -> 0.545 alone, but
-    // -1% in the multi-stream plan, so off); LB_NTT_PAIR overrides
+    // paired 32-bit transforms: bit 0 forward (0.55 -> 0.63 of the roof), bit 1
+    // inverse (three planes, 4 CTAs per SM: 0.51 -> 0.545); both on,
+    // LB_NTT_PAIR overrides
     static int ntt_pairs();
     // smallest batch (polys / ciphertexts per launch) that runs the paired
     // kernels (LB_PAIR_MIN overrides; default 32)
