@@ -18,8 +18,10 @@
 //     shared memory (st/ld.shared::cluster) — forward: stages 0-3 read
 //     straight from HBM and scatter into the owners' smem; inverse: stages
 //     3-0 gather from the owners' smem and write straight to HBM;
-//   * shared memory is XOR-swizzled (bits 0-3 ^= bits 4-7) so every pass is
-//     bank-conflict free;
+//   * shared memory is padded (32-bit words: conflict-free, accesses as base
+//     + immediate) or XOR-swizzled (64-bit words), see Lay below;
+//   * on 32-bit words a cluster runs TWO limbs of the same prime side by
+//     side (NT = 2): twiddles, addresses and the exchange are shared;
 //   * butterflies are Harvey lazy Cooley-Tukey / Gentleman-Sande with Shoup
 //     twiddles, values kept in [0, 4q) and reduced once at the end.
 #pragma once
