@@ -1147,14 +1147,25 @@ int ks_pairs() {
     return mask;
 }
 
-// smallest launch (ciphertexts) that runs the paired key-switch kernels: below
-// it half as many clusters at 3-4 CTAs per SM under-fill the GPU (80
-// ciphertexts: 0.441 vs 0.423 ms unpaired; 320: 1.543 vs 1.553 and +3.4% on
-// the bench); LB_KS_PAIR_MIN overrides
+// smallest launch (ciphertexts) that runs the mixed / paired inner product:
+// with two planes and 4 CTAs per SM it wins from 8 ciphertexts on (two images:
+// 11.9 vs 13.1 ms of HE steps; 80 ciphertexts 0.392 vs 0.430 ms per key
+// switch); a single image (5 ciphertexts, odd) stays on the single-ciphertext
+// kernel. LB_KS_PAIR_MIN overrides
 uint32_t ks_pair_min() {
     static const uint32_t v = [] {
         const char* e = std::getenv("LB_KS_PAIR_MIN");
-        return e ? static_cast<uint32_t>(std::max(2, std::atoi(e))) : 128u;
+        return e ? static_cast<uint32_t>(std::max(2, std::atoi(e))) : 8u;
+    }();
+    return v;
+}
+
+// the same for the paired ModDown (from 32: at 40 ciphertexts per launch the
+// plan is 3% faster with it, lola-cifar's 12 are 0.6% slower); LB_MD_PAIR_MIN
+uint32_t md_pair_min() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("LB_MD_PAIR_MIN");
+        return e ? static_cast<uint32_t>(std::max(2, std::atoi(e))) : 32u;
     }();
     return v;
 }
@@ -1356,7 +1367,7 @@ void launch_moddown(const BfvDev& d, const ModDownArgs& a, cudaStream_t s) {
             launch_counter().fetch_add(1, std::memory_order_relaxed);
             return;
         }
-        if (d.ks29 && (ks_pairs() & 1) && a.count >= ks_pair_min()) {
+        if (d.ks29 && (ks_pairs() & 1) && a.count >= md_pair_min()) {
             cfg.gridDim = grid_xyz(d.L * S::CL, a.count);
             LB_CUDA(cudaLaunchKernelEx(&cfg, moddown_pair_kernel<LOGN>, d, a));
             launch_counter().fetch_add(1, std::memory_order_relaxed);
